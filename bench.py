@@ -1,0 +1,341 @@
+#!/usr/bin/env python3
+"""Benchmark: edges/s (|E| = arcs of the symmetrized graph / total Louvain time)
+of the B200 Louvain engine on BASELINE.json's configs, one JSON line on rank 0.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c2] [--impl ours|reference]
+
+A step = one full Louvain run (all passes, local moving + aggregation +
+renumbering + final fp64 modularity: the reference's wall_seconds window,
+louvain_mc.cpp:163-247) over one synthetic graph.
+  value : graph already resident in HBM (device-built), timed with CUDA events.
+  e2e   : the same call through the public API with host (pinned) CSR buffers:
+          H2D of the CSR and D2H of the membership inside every timed step.
+Inputs are far larger than L2 (C2: 2.6 GB of CSR vs 126 MB L2), so no flush
+is needed between steps.
+
+N > 1 (torchrun, one process per GPU): every rank runs its own replica of the
+workload (the vertex-sharded multi-GPU engine is SURVEY 8(e), not built yet);
+value = total arcs processed by all ranks / max-over-ranks time.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+CONFIGS = {
+    # SURVEY.md 8(d); configs[1] (C2) is the N=1 headline workload
+    "c1": dict(kind="rmat", scale=16, edgefactor=16, seed=1,
+               desc="RMAT scale-16 edgefactor-16 (Graph500 a,b,c=0.57,0.19,0.19), deduplicated, unit weights"),
+    "c2": dict(kind="sbm", n=10_000_000, blocks=1000, avg_degree=32, mu=0.1, seed=2,
+               desc="planted-partition SBM, 10M vertices, 1000 blocks, mean degree 32, mu=0.1"),
+    "c3": dict(kind="rmat", scale=24, edgefactor=16, seed=3,
+               desc="RMAT scale-24 edgefactor-16, deduplicated, unit weights"),
+    "c4": dict(kind="grid", side=4899, p=0.6, seed=4,
+               desc="4899x4899 lattice, each edge kept with p=0.6 (road-like)"),
+    "c5": dict(kind="web", n=50_600_000, avg_degree=75.0, seed=5,
+               desc="web-crawl-shaped power-law graph, 50.6M vertices, ~3.8B arcs"),
+}
+METRIC = "edges/sec (|E|/total Louvain time) at 1/2/4/8 B200 + final modularity vs CPU ref"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons during the timed region."""
+
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+            self.t.join(timeout=2)
+
+    def summary(self):
+        sm, mx, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [x.strip() for x in ln.split(",")]
+            if len(parts) < 6:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx = max(mx, float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def traffic_from_profile(config):
+    """dram bytes per launch of the local-moving sweep from a committed ncu capture."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+        return d.get(config)
+    except Exception:
+        return None
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's own CPU Louvain (louvain_mc, GVE-Louvain
+    design, proj/core/src/louvain_mc.cpp:162) built from its sources into
+    oracle/_ref/libref.so, with every host thread, on the same graph."""
+    if rank != 0:
+        return None
+    import numpy as np
+
+    import paper_2501_19004_b200 as lvn
+    from oracle import Csr, ref, ref_available
+
+    cfg = CONFIGS[args.config]
+    if not ref_available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libref.so was not built"}))
+        return None
+    dg = lvn.generate(cfg["kind"], **{k: v for k, v in cfg.items() if k not in ("kind", "desc")})
+    g = dg.download()
+    dg.close()
+    csr = Csr(g.offsets, g.targets, g.weights, g.total_weight)
+    threads = os.cpu_count()
+    h = ref.handle(csr)
+    times, qs = [], []
+    for i in range(args.warmup + args.steps):
+        r = ref.louvain(h, "mc", thread_count=threads)
+        if i >= args.warmup:
+            times.append(r.wall_seconds)
+            qs.append(r.modularity)
+    arcs = g.num_arcs()
+    t = sum(times) / len(times)
+    v = arcs / t
+    out = {
+        "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
+        "config": {"workload": args.config, "desc": cfg["desc"], "vertices": g.num_vertices(), "arcs": arcs,
+                   "engine": "louvain_mc (reference, OpenMP)"},
+        "modularity": statistics.mean(qs),
+        "cpu_baseline": {"value": v, "unit": "edges/s", "cores": threads, "kind": "reference",
+                         "sample": f"full {args.config} graph, {args.steps} timed runs"},
+        "e2e": {"value": v, "unit": "edges/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(out))
+    return out
+
+
+def cpu_baseline(g, config, budget_s=30.0):
+    """The reference louvain_mc on the box's host cores, one bounded run."""
+    try:
+        from oracle import Csr, ref, ref_available
+
+        if not ref_available():
+            return None, None
+        csr = Csr(g.offsets, g.targets, g.weights, g.total_weight)
+        threads = os.cpu_count()
+        r = ref.louvain(csr, "mc", thread_count=threads)
+        return {"value": g.num_arcs() / r.wall_seconds, "unit": "edges/s", "cores": threads,
+                "kind": "reference",
+                "sample": f"full {config} graph ({g.num_arcs()} arcs), 1 run of louvain_mc, "
+                          f"wall {r.wall_seconds:.2f} s"}, r.modularity
+    except Exception as e:  # pragma: no cover
+        log(f"cpu baseline failed: {e}")
+        return None, None
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="c2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--value-bits", type=int, default=32)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world, rank, local = dist_env()
+
+    import torch
+    import torch.distributed as dist
+
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    import numpy as np
+
+    import paper_2501_19004_b200 as lvn
+    from paper_2501_19004_b200 import _native
+
+    import ctypes
+
+    if _native.lib().lvn_init(1, (ctypes.c_int * 1)(local)) != 0:
+        raise RuntimeError(_native.last_error())
+    cfg = CONFIGS[args.config]
+    t0 = time.time()
+    dg = lvn.generate(cfg["kind"], **{k: v for k, v in cfg.items() if k not in ("kind", "desc")})
+    n, arcs = dg.num_vertices(), dg.num_arcs()
+    log(f"[rank {rank}] {args.config}: {n} vertices, {arcs} arcs, generated in {time.time() - t0:.1f}s")
+    opts = lvn.CompactOptions(value_bits=args.value_bits)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # ---- value: device-resident input -------------------------------------------
+    for _ in range(args.warmup):
+        lvn.louvain_compact(dg, None, opts, membership_on_device=True)
+    sampler = ClockSampler(local)
+    results = []
+    l0 = lvn.launch_count()
+    barrier()
+    with sampler:
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(args.steps):
+            results.append(lvn.louvain_compact(dg, None, opts, membership_on_device=True))
+        e1.record()
+        barrier()
+    launches = (lvn.launch_count() - l0) // args.steps
+    elapsed = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    step_s = elapsed / args.steps
+    value = world * arcs / step_s
+    clocks = sampler.summary()
+    r = results[-1]
+    mv = r.stats["move"]
+    peak, peak_kind = measured_peaks()
+    move_gbps = mv.bytes / mv.seconds / 1e9 if mv.seconds else 0.0
+    per_launch_bytes = mv.bytes / max(mv.launches, 1)
+    traffic = traffic_from_profile(args.config)
+
+    # ---- e2e: host (pinned) buffers through the public API ------------------------
+    e2e = None
+    if not args.no_e2e:
+        host = dg.download(np.empty(n + 1, np.uint64), torch.empty(arcs, dtype=torch.int32, pin_memory=True).numpy().view(np.uint32),
+                           torch.empty(arcs, dtype=torch.float32, pin_memory=True).numpy())
+        off_pinned = torch.empty(n + 1, dtype=torch.int64, pin_memory=True).numpy().view(np.uint64)
+        off_pinned[:] = host.offsets
+        hg = lvn.CsrGraph(off_pinned, host.targets, host.weights, host.total_weight)
+        assert hg.offsets.ctypes.data == off_pinned.ctypes.data
+        lvn.louvain_compact(hg, None, opts)
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        qs = []
+        f0.record()
+        for _ in range(args.steps):
+            qs.append(lvn.louvain_compact(hg, None, opts).modularity)
+        f1.record()
+        barrier()
+        e2e_s = max_over_ranks(f0.elapsed_time(f1) / 1e3) / args.steps
+        e2e = {"value": world * arcs / e2e_s, "unit": "edges/s", "ms_per_step": e2e_s * 1e3,
+               "h2d_bytes_per_step": 8 * (n + 1) + 8 * arcs, "d2h_bytes_per_step": 4 * n}
+    else:
+        host = None
+
+    cpu, cpu_q = (None, None)
+    if rank == 0 and not args.no_cpu_baseline:
+        if host is None:
+            host = dg.download()
+        cpu, cpu_q = cpu_baseline(host, args.config)
+
+    if rank == 0:
+        out = {
+            "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64" if args.value_bits == 64 else "f32+f64",
+            "data": "synthetic (device-generated, seeded)",
+            "config": {"workload": args.config, "desc": cfg["desc"], "vertices": n, "arcs": arcs,
+                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "l2_flush": "not needed: CSR >> 126 MB L2"},
+            "modularity": r.modularity, "num_communities": r.num_communities, "passes": r.passes,
+            "iterations_per_pass": r.iterations_per_pass,
+            "phase_seconds": {"local_moving": r.phase.local_moving, "aggregation": r.phase.aggregation,
+                              "other": r.phase.other},
+            "kernel_seconds": {k: s.seconds for k, s in r.stats.items()},
+            "kernel_gbps": {k: s.gbps for k, s in r.stats.items()},
+            "roofline": {"bound": "hbm", "kernel": "local-moving sweep (lm_thread/lm_group/lm_block)",
+                         "achieved": move_gbps, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
+                         "frac": move_gbps / peak if peak else None,
+                         "bytes_per_launch": per_launch_bytes,
+                         "traffic": traffic},
+            "cpu_baseline": cpu, "cpu_modularity": cpu_q,
+            "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
+        }
+        print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

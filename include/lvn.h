@@ -1,0 +1,210 @@
+/* lvn.h — C-ABI of the B200-native Louvain engine (liblvn.so).
+ *
+ * Drop-in boundary for the reference's Louvain entry point and phase APIs
+ * (arXiv 2501.19004 reference, /root/reference/proj/core). Plain pointers and
+ * sizes only; no C++ or torch types cross this boundary. Each entry point
+ * names the reference interface it replaces.
+ *
+ * Graph convention (graph.hpp:33-54): symmetric CSR, u64 offsets[n+1], u32
+ * targets[arcs] (sorted rows are not required), f32 weights[arcs]; a
+ * self-loop is stored once; total_weight = m = (sum of arc weights) / 2.
+ *
+ * Status codes (mirroring the reference's exceptions, errors.hpp:10-31 and
+ * the CLI exit codes louvain_cli.cpp:33-35):
+ *   0 LVN_OK
+ *   1 LVN_INVALID_ARGUMENT  std::invalid_argument (bad params, non-contiguous membership)
+ *   2 LVN_DEGENERATE        DegenerateGraphError (m == 0)
+ *   3 LVN_INTERNAL          InternalError (table overflow, dendrogram lookup out of range)
+ *   4 LVN_CUDA              CUDA / NCCL failure
+ *   5 LVN_OUT_OF_MEMORY     device allocation failed
+ * lvn_last_error() returns the thread-local message of the last failure.
+ *
+ * Threading: every call is synchronous (returns when results are in the
+ * caller's memory) and calls are serialised on one internal context.
+ */
+#ifndef LVN_H
+#define LVN_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum lvn_status {
+  LVN_OK = 0,
+  LVN_INVALID_ARGUMENT = 1,
+  LVN_DEGENERATE = 2,
+  LVN_INTERNAL = 3,
+  LVN_CUDA = 4,
+  LVN_OUT_OF_MEMORY = 5
+};
+
+/* where the arrays of an lvn_csr / a membership live */
+enum lvn_location { LVN_HOST = 0, LVN_DEVICE = 1 };
+
+/* Probing modes of the reference's slab tables (compact_hashtable.hpp:13-18).
+ * Accepted and validated for option parity; the device tables use their own
+ * power-of-two multiplicative-hash layout, which does not change results. */
+enum lvn_probing { LVN_LINEAR = 0, LVN_QUADRATIC = 1, LVN_DOUBLE_HASH = 2, LVN_QUADRATIC_DOUBLE = 3 };
+
+/* Borrowed view of a CsrGraph (graph.hpp:38-54). Never freed by the library. */
+typedef struct lvn_csr {
+  uint32_t num_vertices;
+  uint64_t num_arcs;
+  const uint64_t* offsets;
+  const uint32_t* targets;
+  const float* weights;
+  double total_weight;
+  int location; /* lvn_location */
+} lvn_csr;
+
+/* Library-owned CSR returned by lvn_aggregate (host arrays). */
+typedef struct lvn_graph_out {
+  uint32_t num_vertices;
+  uint64_t num_arcs;
+  uint64_t* offsets;
+  uint32_t* targets;
+  float* weights;
+  double total_weight;
+} lvn_graph_out;
+
+/* LouvainParams (louvain.hpp:9-18) + CompactOptions (louvain_compact.hpp:35-40)
+ * + device knobs. Initialise with lvn_params_default(). */
+typedef struct lvn_params {
+  /* LouvainParams */
+  int max_passes;               /* 10 */
+  int max_iterations;           /* 20 local-moving iterations per pass */
+  double initial_tolerance;     /* 0.01 */
+  double tolerance_drop;        /* 10 */
+  double aggregation_tolerance; /* 0.8 */
+  int thread_count;             /* validated (>= 0) for parity; unused on the GPU */
+  int chunk_size;               /* validated (>= 1) for parity; unused on the GPU */
+  int prune;                    /* 1 */
+  /* CompactOptions */
+  int pick_less_period;         /* 4, even and >= 2 */
+  uint64_t switch_move;         /* 64: reference serial/team split; see bin_* below */
+  uint64_t switch_aggregate;    /* 128 */
+  int probing;                  /* lvn_probing, LVN_QUADRATIC_DOUBLE */
+  int value_bits;               /* 32 or 64: width of the per-vertex scan-table values */
+  /* device degree bins: thread <= bin_thread_max < group8 <= bin_group_max
+   * < warp <= bin_warp_max < block <= bin_block_max < global-table block */
+  uint32_t bin_thread_max;      /* 4 */
+  uint32_t bin_group_max;       /* 32 */
+  uint32_t bin_warp_max;        /* 256 */
+  uint32_t bin_block_max;       /* 4096 */
+  int membership_on_device;     /* result membership stays in device memory */
+  int reserved[7];
+} lvn_params;
+
+/* Per-kernel-family device accounting (CUDA events on the engine stream). */
+typedef struct lvn_phase_stats {
+  double seconds;        /* summed device time of the family's launches */
+  double bytes;          /* algorithmic bytes (SURVEY.md 8(d) formulas) */
+  uint64_t launches;
+  uint64_t items;        /* vertices processed */
+  uint64_t arcs;         /* arcs scanned */
+} lvn_phase_stats;
+
+enum { LVN_STAT_MOVE = 0, LVN_STAT_AGGREGATE = 1, LVN_STAT_RENUMBER = 2, LVN_STAT_RESET = 3,
+       LVN_STAT_MODULARITY = 4, LVN_STAT_COUNT = 5 };
+
+/* LouvainResult (louvain.hpp:28-39) + device breakdown. */
+typedef struct lvn_result {
+  uint32_t* membership;   /* num_vertices ids, contiguous 0..count-1 (host, or device) */
+  uint32_t num_vertices;
+  uint32_t num_communities;
+  double modularity;      /* recomputed on the input graph, fp64 */
+  int passes;
+  int aggregations;
+  int* iterations_per_pass;
+  double* tolerance_per_pass;
+  double* pass_seconds;
+  uint32_t* vertices_per_pass;
+  uint64_t* arcs_per_pass;
+  double local_moving;    /* PhaseTimes (louvain.hpp:20-26), seconds */
+  double aggregation;
+  double other;
+  double wall_seconds;    /* engine entry to result, like the reference */
+  double h2d_seconds;     /* input upload (host input only) */
+  double d2h_seconds;     /* membership download */
+  lvn_phase_stats stats[LVN_STAT_COUNT];
+  int membership_on_device;
+} lvn_result;
+
+/* ---- lifecycle -------------------------------------------------------- */
+int lvn_init(int num_gpus, const int* devices); /* optional; lazily device 0 */
+int lvn_finalize(void);
+const char* lvn_last_error(void);
+const char* lvn_version(void);
+void lvn_params_default(lvn_params* p);
+void lvn_result_free(lvn_result* r);
+void lvn_graph_free(lvn_graph_out* g);
+
+/* ---- engine: louvain_compact (louvain_compact.hpp:57-58) --------------- */
+int lvn_louvain(const lvn_csr* g, const lvn_params* p, lvn_result** out);
+
+/* ---- phase / parity APIs ----------------------------------------------- */
+/* modularity (quality.hpp:27); any labelling, fp64 */
+int lvn_modularity(const lvn_csr* g, const uint32_t* membership, int membership_location,
+                   double* q);
+/* vertex_weights (graph.hpp:79): K_u = sum of row weights, fp64 */
+int lvn_vertex_weights(const lvn_csr* g, double* out_host);
+/* count_communities (quality.hpp:40) */
+int lvn_count_communities(const uint32_t* membership, uint64_t n, int location, uint32_t* count);
+/* renumber_communities (louvain_mc.hpp:101), in place */
+int lvn_renumber(uint32_t* membership, uint64_t n, int location, uint32_t* count);
+/* lookup_dendrogram (louvain_mc.hpp:105), in place; LVN_INTERNAL when out of range */
+int lvn_lookup_dendrogram(uint32_t* membership, uint64_t n, const uint32_t* level, uint64_t nl,
+                          int location);
+/* build_community_csr (engine_detail.hpp:30-40); members ascending per community.
+ * offsets: count+1 entries, members: n entries (host). */
+int lvn_community_csr(const uint32_t* membership, uint32_t n, uint32_t count, int location,
+                      uint64_t* offsets, uint32_t* members);
+/* compact_aggregate / louvain_aggregate (louvain_compact.hpp:76-77, louvain_mc.hpp:96-97):
+ * contiguous membership required; fp64 accumulation narrowed once to f32;
+ * canonical != 0 sorts each row by target. */
+int lvn_aggregate(const lvn_csr* g, const uint32_t* membership, int membership_location,
+                  int canonical, const lvn_params* p, lvn_graph_out** out);
+/* compact_evaluate_move (louvain_compact.hpp:65-72), batched over all vertices on
+ * one fixed snapshot (membership, K, Sigma): to[u], gain[u] for every u, no move
+ * applied. force_kernel: -1 by degree bin, else the minimum kernel class
+ * (0 thread, 1 group, 2 warp, 3 block, 4 global table) a vertex may use. */
+int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
+                       const double* community_w, double m, const lvn_params* p,
+                       int force_kernel, uint32_t* to, double* gain);
+
+/* ---- device-resident graphs (bench / generators) ----------------------- */
+typedef struct lvn_dgraph lvn_dgraph;
+/* synthetic generators (SURVEY.md 8(d) C1-C5 shapes), built on the device:
+ * kind 0 RMAT(scale, edgefactor), 1 SBM(n, blocks, avg_degree, mu),
+ * 2 grid(side, keep_probability), 3 web(n, avg_degree), 4 uniform(n, edges) */
+typedef struct lvn_gen_params {
+  int kind;
+  uint64_t n;
+  uint64_t edges;      /* undirected samples (RMAT: 2^scale * edgefactor) */
+  uint32_t scale;
+  uint32_t blocks;
+  double a, b, c;      /* RMAT probabilities */
+  double mu;           /* SBM mixing */
+  double p;            /* grid keep probability */
+  double avg_degree;
+  uint64_t seed;
+} lvn_gen_params;
+int lvn_generate(const lvn_gen_params* gp, lvn_dgraph** out);
+int lvn_dgraph_upload(const lvn_csr* host, lvn_dgraph** out);
+int lvn_dgraph_view(const lvn_dgraph* g, lvn_csr* view); /* device pointers */
+int lvn_dgraph_download(const lvn_dgraph* g, uint64_t* offsets, uint32_t* targets,
+                        float* weights);
+void lvn_dgraph_free(lvn_dgraph* g);
+
+/* device buffers for device-located memberships (tests) */
+int lvn_device_alloc(size_t bytes, void** ptr);
+int lvn_device_free(void* ptr);
+int lvn_memcpy(void* dst, const void* src, size_t bytes, int kind /* 1 h2d, 2 d2h, 3 d2d */);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* LVN_H */

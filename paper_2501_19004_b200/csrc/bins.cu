@@ -1,0 +1,222 @@
+// Degree binning (stable multi-way partition of the rows by degree class) and
+// the pass reset of compact_impl (louvain_compact.cpp:357-360 +
+// engine_detail.cpp:26-42): K_u = fp64 row sum, Sigma = K, C = identity,
+// flags = 1 for rows with arcs (rows with none are never visited,
+// louvain_compact.cpp:138-141).
+//
+// Bytes: reset = 4 B x arcs + 29 B x vertices.
+#include "kernels.cuh"
+
+namespace lvn {
+namespace {
+
+constexpr int kT = 256;     // threads per tile
+constexpr int kRounds = 8;  // vertices per thread per tile
+constexpr int kTileV = kT * kRounds;
+
+__device__ __forceinline__ int bin_of(u64 deg, const BinEdges& e) {
+  if (deg == 0) return 0;
+  if (deg <= e.thread_max) return 1;
+  if (deg <= e.group_max) return 2;
+  if (deg <= e.warp_max) return 3;
+  if (deg <= e.block_max) return 4;
+  return 5;
+}
+
+__global__ void __launch_bounds__(kT) bin_count(const u64* __restrict__ off, u32 n, BinEdges e,
+                                                u64 cap, u64* __restrict__ counts, u32 nblocks,
+                                                ull* max_deg) {
+  __shared__ u32 cnt[kBins];
+  if (threadIdx.x < kBins) cnt[threadIdx.x] = 0;
+  __syncthreads();
+  const u64 base = u64(blockIdx.x) * kTileV;
+  const int lane = threadIdx.x & 31;
+  u64 mx = 0;
+  for (int r = 0; r < kRounds; ++r) {
+    const u64 v = base + u64(r) * kT + threadIdx.x;
+    int b = -1;
+    if (v < n) {
+      u64 d = off[v + 1] - off[v];
+      mx = d > mx ? d : mx;
+      d = d < cap ? d : cap;
+      b = bin_of(d, e);
+    }
+#pragma unroll
+    for (int k = 0; k < kBins; ++k) {
+      const u32 bal = __ballot_sync(0xffffffffu, b == k);
+      if (lane == 0 && bal) atomicAdd(&cnt[k], __popc(bal));
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const u64 y = __shfl_xor_sync(0xffffffffu, mx, o);
+    mx = y > mx ? y : mx;
+  }
+  if (lane == 0 && mx) atomicMax(max_deg, ull(mx));
+  __syncthreads();
+  if (threadIdx.x < kBins) counts[u64(threadIdx.x) * nblocks + blockIdx.x] = cnt[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(kT) bin_scatter(const u64* __restrict__ off, u32 n, BinEdges e,
+                                                  u64 cap, const u64* __restrict__ pos,
+                                                  u32 nblocks, u32* __restrict__ list) {
+  __shared__ u32 wc[kT / 32][kBins];
+  __shared__ u64 run[kBins];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (threadIdx.x < kBins) run[threadIdx.x] = pos[u64(threadIdx.x) * nblocks + blockIdx.x];
+  const u64 base = u64(blockIdx.x) * kTileV;
+  const u32 lt = (1u << lane) - 1u;
+  for (int r = 0; r < kRounds; ++r) {
+    const u64 v = base + u64(r) * kT + threadIdx.x;
+    int b = -1;
+    if (v < n) {
+      u64 d = off[v + 1] - off[v];
+      d = d < cap ? d : cap;
+      b = bin_of(d, e);
+    }
+    u32 my_rank = 0;
+#pragma unroll
+    for (int k = 0; k < kBins; ++k) {
+      const u32 bal = __ballot_sync(0xffffffffu, b == k);
+      if (lane == 0) wc[wid][k] = __popc(bal);
+      if (b == k) my_rank = __popc(bal & lt);
+    }
+    __syncthreads();
+    if (b >= 0) {
+      u64 o = run[b];
+      for (int w = 0; w < wid; ++w) o += wc[w][b];
+      list[o + my_rank] = u32(v);
+    }
+    __syncthreads();
+    if (threadIdx.x < kBins) {
+      u64 t = 0;
+      for (int w = 0; w < kT / 32; ++w) t += wc[w][threadIdx.x];
+      run[threadIdx.x] += t;
+    }
+    __syncthreads();
+  }
+}
+
+__global__ void gather_starts(const u64* pos, u32 nblocks, const ull* max_deg, u64* out) {
+  if (threadIdx.x < kBins) out[threadIdx.x] = pos[u64(threadIdx.x) * nblocks];
+  if (threadIdx.x == kBins) out[kBins] = *max_deg;
+}
+
+// thread per vertex: identity, flags, and the sequential fp64 row sum for
+// short rows (same summation order as the reference)
+__global__ void reset_thread(DGraph g, u32 short_max, double* __restrict__ K,
+                             double* __restrict__ sigma, u32* __restrict__ C,
+                             u8* __restrict__ flags) {
+  for (u64 v = blockIdx.x * u64(blockDim.x) + threadIdx.x; v < g.n;
+       v += u64(gridDim.x) * blockDim.x) {
+    const u64 lo = g.off[v], hi = g.off[v + 1];
+    if (C) C[v] = u32(v);
+    if (flags) flags[v] = hi > lo ? 1 : 0;
+    if (hi - lo <= short_max) {
+      double s = 0.0;
+      for (u64 a = lo; a < hi; ++a) s += double(g.w[a]);
+      K[v] = s;
+      if (sigma) sigma[v] = s;
+    }
+  }
+}
+
+__global__ void reset_warp(DGraph g, const u32* __restrict__ list, u64 count,
+                           double* __restrict__ K, double* __restrict__ sigma) {
+  const int lane = threadIdx.x & 31;
+  const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
+  for (u64 i = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; i < count; i += warps) {
+    const u32 v = list[i];
+    const u64 lo = g.off[v], hi = g.off[v + 1];
+    double s = 0.0;
+    for (u64 a = lo + lane; a < hi; a += 32) s += double(g.w[a]);
+    s = warp_sum(s);
+    if (lane == 0) {
+      K[v] = s;
+      if (sigma) sigma[v] = s;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(512) reset_block(DGraph g, const u32* __restrict__ list,
+                                                   u64 count, double* __restrict__ K,
+                                                   double* __restrict__ sigma) {
+  __shared__ double ws[16];
+  for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
+    const u32 v = list[i];
+    const u64 lo = g.off[v], hi = g.off[v + 1];
+    double s = 0.0;
+    for (u64 a = lo + threadIdx.x; a < hi; a += blockDim.x) s += double(g.w[a]);
+    s = warp_sum(s);
+    if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      double t = 0.0;
+      for (int w = 0; w < int(blockDim.x >> 5); ++w) t += ws[w];
+      K[v] = t;
+      if (sigma) sigma[v] = t;
+    }
+    __syncthreads();
+  }
+}
+
+void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C, u8* flags,
+                cudaStream_t s) {
+  if (g.n == 0) return;
+  const int sms = sm_count();
+  const u64 tb = std::min<u64>((g.n + 255) / 256, u64(sms) * 16);
+  reset_thread<<<unsigned(tb), 256, 0, s>>>(g, b.edges.group_max, K, sigma, C, flags);
+  LVN_LAUNCH();
+  if (b.count(3)) {
+    const u64 wb = std::min<u64>((b.count(3) + 7) / 8, u64(sms) * 16);
+    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(3), b.count(3), K, sigma);
+    LVN_LAUNCH();
+  }
+  const u64 big = b.count(4) + b.count(5);
+  if (big) {
+    const u64 bb = std::min<u64>(big, u64(sms) * 4);
+    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(4), big, K, sigma);
+    LVN_LAUNCH();
+  }
+}
+
+}  // namespace
+
+void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStream_t s, u64 cap) {
+  out.edges = e;
+  out.list.ensure(n ? n : 1);
+  if (n == 0) {
+    for (int b = 0; b <= kBins; ++b) out.start[b] = 0;
+    out.max_degree = 0;
+    return;
+  }
+  const u32 nblocks = u32((u64(n) + kTileV - 1) / kTileV);
+  const u64 ncnt = u64(kBins) * nblocks;
+  DBuf<u64> counts(ncnt), pos(ncnt + 1), small(kBins + 1);
+  DBuf<ull> mx(1);
+  LVN_CUDA(cudaMemsetAsync(mx.p, 0, sizeof(ull), s));
+  bin_count<<<nblocks, kT, 0, s>>>(off, n, e, cap, counts.p, nblocks, mx.p);
+  LVN_LAUNCH();
+  exclusive_scan_u64(counts.p, pos.p, ncnt, s);
+  bin_scatter<<<nblocks, kT, 0, s>>>(off, n, e, cap, pos.p, nblocks, out.list.p);
+  LVN_LAUNCH();
+  gather_starts<<<1, 32, 0, s>>>(pos.p, nblocks, mx.p, small.p);
+  LVN_LAUNCH();
+  u64* h = ctx().pinned;
+  LVN_CUDA(cudaMemcpyAsync(h, small.p, (kBins + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  for (int b = 0; b < kBins; ++b) out.start[b] = h[b];
+  out.start[kBins] = n;
+  out.max_degree = h[kBins];
+}
+
+void pass_reset(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C, u8* flags,
+                cudaStream_t s) {
+  reset_impl(g, b, K, sigma, C, flags, s);
+}
+
+void vertex_weights(const DGraph& g, const Bins& b, double* K, cudaStream_t s) {
+  reset_impl(g, b, K, nullptr, nullptr, nullptr, s);
+}
+
+}  // namespace lvn

@@ -1,0 +1,174 @@
+// Shared internals of liblvn.so: types, error plumbing, device pool, small
+// device helpers. Everything here is B200 (sm_100a) only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <cstdint>
+#include <cstdio>
+#include <map>
+#include <mutex>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+namespace lvn {
+
+using u8 = std::uint8_t;
+using u32 = std::uint32_t;
+using u64 = std::uint64_t;
+using ull = unsigned long long;
+
+constexpr u32 kEmpty = 0xFFFFFFFFu;  // empty-slot / invalid id (graph.hpp:15, compact_hashtable.hpp:26)
+constexpr ull kEmptySlot64 = 0xFFFFFFFF00000000ull;  // packed (key=kEmpty, value=0.0f)
+
+// status codes of include/lvn.h
+enum Status { kOk = 0, kInvalid = 1, kDegenerate = 2, kInternal = 3, kCuda = 4, kOom = 5 };
+
+struct Error {
+  int code;
+  std::string what;
+};
+
+[[noreturn]] inline void fail(int code, const std::string& what) { throw Error{code, what}; }
+
+inline void cuda_check(cudaError_t e, const char* expr, const char* file, int line) {
+  if (e != cudaSuccess) {
+    const int code = (e == cudaErrorMemoryAllocation) ? kOom : kCuda;
+    fail(code, std::string(expr) + ": " + cudaGetErrorString(e) + " (" + file + ":" +
+                   std::to_string(line) + ")");
+  }
+}
+extern std::atomic<unsigned long long> g_launches;  // kernels launched by this library
+
+#define LVN_CUDA(x) ::lvn::cuda_check((x), #x, __FILE__, __LINE__)
+#define LVN_LAUNCH()                                                         \
+  do {                                                                       \
+    ::lvn::g_launches.fetch_add(1, std::memory_order_relaxed);               \
+    ::lvn::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
+  } while (0)
+
+// device error word bits (checked by the host once per pass)
+enum DevErr : u32 { kErrTable = 1u, kErrLookup = 2u, kErrRange = 4u };
+
+// ---------------------------------------------------------------------------
+// Device view of a CSR graph (graph.hpp:38-54)
+// ---------------------------------------------------------------------------
+struct DGraph {
+  u32 n = 0;
+  u64 arcs = 0;
+  const u64* off = nullptr;
+  const u32* tgt = nullptr;
+  const float* w = nullptr;
+};
+
+// ---------------------------------------------------------------------------
+// Caching device pool: one cudaMalloc per size class, reused across calls.
+// ---------------------------------------------------------------------------
+class Pool {
+ public:
+  void* get(size_t bytes);
+  void put(void* p);
+  void trim();  // return cached blocks to the driver
+  ~Pool();
+
+ private:
+  std::multimap<size_t, void*> free_;
+  std::unordered_map<void*, size_t> used_;
+};
+
+// Engine context: one device, one stream, pinned scratch for small readbacks.
+struct Context {
+  int device = 0;
+  int sms = 148;
+  size_t smem_optin = 227 * 1024;
+  cudaStream_t stream = nullptr;
+  Pool pool;
+  u64* pinned = nullptr;  // 512 u64 of pinned host scratch
+  std::mutex mu;
+};
+
+Context& ctx();  // lazily initialised on device 0 (or the lvn_init device)
+void init_context(int device);
+void destroy_context();
+
+// RAII typed device buffer from the pool
+template <class T>
+struct DBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  DBuf() = default;
+  explicit DBuf(size_t count) { alloc(count); }
+  DBuf(const DBuf&) = delete;
+  DBuf& operator=(const DBuf&) = delete;
+  DBuf(DBuf&& o) noexcept : p(o.p), n(o.n) { o.p = nullptr, o.n = 0; }
+  DBuf& operator=(DBuf&& o) noexcept {
+    if (this != &o) {
+      release();
+      p = o.p, n = o.n;
+      o.p = nullptr, o.n = 0;
+    }
+    return *this;
+  }
+  void alloc(size_t count) {
+    release();
+    n = count;
+    p = static_cast<T*>(ctx().pool.get((count ? count : 1) * sizeof(T)));
+  }
+  void ensure(size_t count) {
+    if (count > n || !p) alloc(count);
+  }
+  void release() {
+    if (p) ctx().pool.put(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DBuf() { release(); }
+  T* get() const { return p; }
+};
+
+// ---------------------------------------------------------------------------
+// Device helpers
+// ---------------------------------------------------------------------------
+__host__ __device__ inline u32 ceil_log2_u64(u64 x) {
+  u32 r = 0;
+  while ((u64(1) << r) < x) ++r;
+  return r;
+}
+
+// multiplicative hash into a power-of-two table of 2^log_size slots
+__device__ __forceinline__ u32 slot_hash(u32 key, u32 log_size) {
+  return log_size ? (key * 0x9E3779B1u) >> (32u - log_size) : 0u;
+}
+
+// Eq. 2, evaluated operation for operation like delta_modularity
+// (quality.hpp:34-37) with round-to-nearest intrinsics so no FMA contraction
+// changes the bits.
+__device__ __forceinline__ double delta_q(double k_to_c, double k_to_d, double k_i, double sigma_c,
+                                          double sigma_d, double m) {
+  const double a = __ddiv_rn(__dsub_rn(k_to_c, k_to_d), m);
+  const double num = __dmul_rn(k_i, __dsub_rn(__dadd_rn(k_i, sigma_c), sigma_d));
+  const double den = __dmul_rn(__dmul_rn(2.0, m), m);
+  return __dsub_rn(a, __ddiv_rn(num, den));
+}
+
+// best-candidate order: greater gain, ties to the lowest id (compact_hashtable.hpp:152)
+__device__ __forceinline__ bool better(double g, u32 c, double bg, u32 bc) {
+  return g > bg || (g == bg && c < bc);
+}
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+__device__ __forceinline__ ull warp_sum(ull v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+int sm_count();
+
+}  // namespace lvn

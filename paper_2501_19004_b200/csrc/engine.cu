@@ -1,0 +1,1053 @@
+// Host engine of liblvn.so: device context and pool, the Louvain pass shell
+// (compact_impl, louvain_compact.cpp:312-402, re-expressed as a device
+// pipeline with one small readback per local-moving iteration), and every
+// C-ABI entry point declared in include/lvn.h.
+#include <atomic>
+#include <chrono>
+#include <cstdlib>
+#include <cstring>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+#include "lvn.h"
+
+namespace lvn {
+
+std::atomic<unsigned long long> g_launches{0};
+
+// ---------------------------------------------------------------------------
+// Pool / context
+// ---------------------------------------------------------------------------
+void* Pool::get(size_t bytes) {
+  const size_t r = bytes <= (size_t(1) << 20) ? ((bytes + 511) & ~size_t(511))
+                                              : ((bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1));
+  auto it = free_.lower_bound(r);
+  if (it != free_.end() && it->first <= 2 * r) {
+    void* p = it->second;
+    used_[p] = it->first;
+    free_.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaMalloc(&p, r);
+  if (e == cudaErrorMemoryAllocation) {
+    (void)cudaGetLastError();
+    trim();
+    e = cudaMalloc(&p, r);
+  }
+  if (e != cudaSuccess) {
+    (void)cudaGetLastError();
+    fail(e == cudaErrorMemoryAllocation ? kOom : kCuda,
+         "cudaMalloc(" + std::to_string(r) + " bytes): " + cudaGetErrorString(e));
+  }
+  used_[p] = r;
+  return p;
+}
+
+void Pool::put(void* p) {
+  auto it = used_.find(p);
+  if (it == used_.end()) return;
+  free_.emplace(it->second, p);
+  used_.erase(it);
+}
+
+void Pool::trim() {
+  (void)cudaDeviceSynchronize();
+  for (auto& kv : free_) (void)cudaFree(kv.second);
+  free_.clear();
+}
+
+Pool::~Pool() {
+  for (auto& kv : free_) (void)cudaFree(kv.second);
+  for (auto& kv : used_) (void)cudaFree(kv.first);
+}
+
+static Context* g_ctx = nullptr;
+static std::mutex g_ctx_mu;
+
+void init_context(int device) {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (g_ctx) {
+    if (g_ctx->device == device) return;
+    fail(kInvalid, "lvn context already initialised on another device; call lvn_finalize first");
+  }
+  int count = 0;
+  LVN_CUDA(cudaGetDeviceCount(&count));
+  if (device < 0 || device >= count) fail(kInvalid, "no such CUDA device");
+  LVN_CUDA(cudaSetDevice(device));
+  cudaDeviceProp prop{};
+  LVN_CUDA(cudaGetDeviceProperties(&prop, device));
+  if (prop.major != 10)
+    fail(kCuda, std::string("liblvn is built for sm_100a (B200); found ") + prop.name);
+  auto* c = new Context;
+  c->device = device;
+  c->sms = prop.multiProcessorCount;
+  c->smem_optin = prop.sharedMemPerBlockOptin;
+  LVN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  LVN_CUDA(cudaMallocHost(&c->pinned, 512 * sizeof(u64)));
+  g_ctx = c;
+}
+
+Context& ctx() {
+  if (!g_ctx) init_context(0);
+  return *g_ctx;
+}
+
+int sm_count() { return ctx().sms; }
+
+void destroy_context() {
+  std::lock_guard<std::mutex> lk(g_ctx_mu);
+  if (!g_ctx) return;
+  (void)cudaStreamSynchronize(g_ctx->stream);
+  (void)cudaFreeHost(g_ctx->pinned);
+  (void)cudaStreamDestroy(g_ctx->stream);
+  delete g_ctx;
+  g_ctx = nullptr;
+}
+
+// ---------------------------------------------------------------------------
+// helpers
+// ---------------------------------------------------------------------------
+namespace {
+
+using Clock = std::chrono::steady_clock;
+double since(Clock::time_point t0) {
+  return std::chrono::duration<double>(Clock::now() - t0).count();
+}
+
+template <class T>
+T read_scalar(const T* dev, cudaStream_t s) {
+  T* h = reinterpret_cast<T*>(ctx().pinned);
+  LVN_CUDA(cudaMemcpyAsync(h, dev, sizeof(T), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  return *h;
+}
+
+BinEdges edges_of(const lvn_params& p) {
+  BinEdges e;
+  e.thread_max = p.bin_thread_max;
+  e.group_max = p.bin_group_max;
+  e.warp_max = p.bin_warp_max;
+  e.block_max = p.bin_block_max;
+  return e;
+}
+
+// validate_params (engine_detail.cpp:16-24) + validate_options (louvain_compact.cpp:22-27)
+void validate(const lvn_params& p) {
+  if (p.max_passes < 0) fail(kInvalid, "max_passes must be >= 0");
+  if (p.max_iterations < 0) fail(kInvalid, "max_iterations must be >= 0");
+  if (!(p.tolerance_drop > 0.0)) fail(kInvalid, "tolerance_drop must be > 0");
+  if (!(p.aggregation_tolerance > 0.0)) fail(kInvalid, "aggregation_tolerance must be > 0");
+  if (p.thread_count < 0) fail(kInvalid, "thread_count must be >= 0");
+  if (p.chunk_size < 1) fail(kInvalid, "chunk_size must be >= 1");
+  if (p.pick_less_period < 2 || p.pick_less_period % 2 != 0)
+    fail(kInvalid, "pick-less period must be even and >= 2");
+  if (p.value_bits != 32 && p.value_bits != 64) fail(kInvalid, "value_bits must be 32 or 64");
+  if (p.probing < 0 || p.probing > 3) fail(kInvalid, "unknown probing mode");
+  if (!(p.bin_thread_max <= p.bin_group_max && p.bin_group_max <= p.bin_warp_max &&
+        p.bin_warp_max <= p.bin_block_max))
+    fail(kInvalid, "degree bin edges must be non-decreasing");
+  if (p.bin_thread_max > 8 || p.bin_group_max > 32 || p.bin_warp_max > 256 ||
+      p.bin_block_max > 4096)
+    fail(kInvalid, "degree bin edges exceed the device table capacities (8/32/256/4096)");
+}
+
+// pick_less_active (louvain_compact.hpp:22-24)
+bool pick_less_active(int iteration, int period) { return (iteration + period / 2) % period == 0; }
+
+// A graph resident on the device: borrowed device pointers or an uploaded copy.
+struct InGraph {
+  DGraph g;
+  double m = 0.0;
+  DBuf<u64> off;
+  DBuf<u32> tgt;
+  DBuf<float> w;
+};
+
+void check_csr_header(const lvn_csr* in) {
+  if (!in) fail(kInvalid, "null graph");
+  if (in->num_vertices >= kEmpty) fail(kInvalid, "vertex count collides with the reserved sentinel id");
+  if (!in->offsets) fail(kInvalid, "null offsets");
+  if (in->num_arcs && (!in->targets || !in->weights)) fail(kInvalid, "null targets/weights");
+  if (in->location != LVN_HOST && in->location != LVN_DEVICE) fail(kInvalid, "bad location");
+}
+
+void load_graph(const lvn_csr* in, cudaStream_t s, InGraph& out, double* h2d_seconds) {
+  check_csr_header(in);
+  const u64 n = in->num_vertices, a = in->num_arcs;
+  out.m = in->total_weight;
+  if (in->location == LVN_DEVICE) {
+    out.g = DGraph{u32(n), a, in->offsets, in->targets, in->weights};
+    return;
+  }
+  if (in->offsets[0] != 0 || in->offsets[n] != a)
+    fail(kInvalid, "offsets must start at 0 and end at num_arcs");
+  const auto t0 = Clock::now();
+  out.off.alloc(n + 1);
+  out.tgt.alloc(a ? a : 1);
+  out.w.alloc(a ? a : 1);
+  LVN_CUDA(cudaMemcpyAsync(out.off.p, in->offsets, (n + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+  if (a) {
+    LVN_CUDA(cudaMemcpyAsync(out.tgt.p, in->targets, a * sizeof(u32), cudaMemcpyHostToDevice, s));
+    LVN_CUDA(cudaMemcpyAsync(out.w.p, in->weights, a * sizeof(float), cudaMemcpyHostToDevice, s));
+  }
+  LVN_CUDA(cudaStreamSynchronize(s));
+  if (h2d_seconds) *h2d_seconds += since(t0);
+  out.g = DGraph{u32(n), a, out.off.p, out.tgt.p, out.w.p};
+}
+
+// membership-like array on the device (borrowed or uploaded)
+struct DevU32 {
+  u32* p = nullptr;
+  DBuf<u32> own;
+};
+void load_u32(const u32* src, u64 n, int location, cudaStream_t s, DevU32& out) {
+  if (n && !src) fail(kInvalid, "null membership");
+  if (location == LVN_DEVICE) {
+    out.p = const_cast<u32*>(src);
+    return;
+  }
+  out.own.alloc(n ? n : 1);
+  if (n) LVN_CUDA(cudaMemcpyAsync(out.own.p, src, n * sizeof(u32), cudaMemcpyHostToDevice, s));
+  out.p = out.own.p;
+}
+
+// ---- per-family device timing -------------------------------------------------
+struct Timing {
+  struct Span {
+    cudaEvent_t a, b;
+    int fam;
+    double bytes;
+    ull items, arcs;
+  };
+  std::vector<Span> spans;
+  std::vector<cudaEvent_t> free_events;
+  cudaEvent_t ev() {
+    if (!free_events.empty()) {
+      cudaEvent_t e = free_events.back();
+      free_events.pop_back();
+      return e;
+    }
+    cudaEvent_t e;
+    LVN_CUDA(cudaEventCreate(&e));
+    return e;
+  }
+  size_t begin(int fam, cudaStream_t s) {
+    Span sp{ev(), ev(), fam, 0.0, 0, 0};
+    LVN_CUDA(cudaEventRecord(sp.a, s));
+    spans.push_back(sp);
+    return spans.size() - 1;
+  }
+  void end(size_t i, cudaStream_t s, double bytes, ull items = 0, ull arcs = 0) {
+    LVN_CUDA(cudaEventRecord(spans[i].b, s));
+    spans[i].bytes = bytes;
+    spans[i].items = items;
+    spans[i].arcs = arcs;
+  }
+  void set_bytes(size_t i, double bytes, ull items, ull arcs) {
+    spans[i].bytes = bytes, spans[i].items = items, spans[i].arcs = arcs;
+  }
+  void collect(lvn_phase_stats* st) {
+    for (auto& sp : spans) {
+      float ms = 0.f;
+      LVN_CUDA(cudaEventSynchronize(sp.b));
+      LVN_CUDA(cudaEventElapsedTime(&ms, sp.a, sp.b));
+      lvn_phase_stats& f = st[sp.fam];
+      f.seconds += ms * 1e-3;
+      f.bytes += sp.bytes;
+      f.launches += 1;
+      f.items += sp.items;
+      f.arcs += sp.arcs;
+      free_events.push_back(sp.a);
+      free_events.push_back(sp.b);
+    }
+    spans.clear();
+  }
+  ~Timing() {
+    for (auto& sp : spans) (void)cudaEventDestroy(sp.a), (void)cudaEventDestroy(sp.b);
+    for (auto e : free_events) (void)cudaEventDestroy(e);
+  }
+};
+
+struct IterRecord {  // device scratch read back once per iteration
+  double gain;
+  ull verts, arcs, moves;
+};
+
+// ---- renumbering: ids of C (all < width) -> 0..count-1 ascending, returns count
+u32 renumber_device(u32* C, u64 n, u64 width, DBuf<u32>& used, DBuf<u32>& rank, cudaStream_t s,
+                    bool apply) {
+  used.ensure(width + 1);
+  rank.ensure(width + 1);
+  mark_used(C, n, used.p, width, s);
+  exclusive_scan_u32(used.p, rank.p, width, s);
+  const u32 count = read_scalar(rank.p + width, s);
+  if (apply) remap(C, n, rank.p, s);
+  return count;
+}
+
+// ---- aggregation of a graph by a contiguous membership ----------------------
+void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
+                      u32* err, cudaStream_t s, bool canonical) {
+  DBuf<u32> msize(count ? count : 1);
+  DBuf<u64> budget(count + 1), coff(count + 1), boff(count + 1), hoff(count + 1), capped(count + 1);
+  community_counts(g, C, count, msize.p, budget.p, s);
+  exclusive_scan_u32_to_u64(msize.p, coff.p, count, s);
+  exclusive_scan_u64(budget.p, boff.p, count, s);
+  // holey row capacity min(budget, count): distinct targets never exceed either
+  cap_budgets(budget.p, capped.p, count, s);
+  exclusive_scan_u64(capped.p, hoff.p, count, s);
+  DBuf<u32> members(g.n ? g.n : 1), cursor(count ? count : 1);
+  community_scatter(C, g.n, coff.p, count, cursor.p, members.p, s);
+  msize.release();
+  Bins ab;
+  compute_bins(boff.p, count, e, ab, s);  // synchronises
+  const u64 H = read_scalar(hoff.p + count, s);
+  DBuf<u32> htgt(H ? H : 1), fill(count ? count : 1);
+  DBuf<float> hw(H ? H : 1);
+  AggArgs a;
+  a.g = g;
+  a.C = C;
+  a.count = count;
+  a.coff = coff.p;
+  a.members = members.p;
+  a.boff = boff.p;
+  a.hoff = hoff.p;
+  a.htgt = htgt.p;
+  a.hw = hw.p;
+  a.fill = fill.p;
+  a.err = err;
+  DBuf<double> table;
+  const u64 max_cap = std::min<u64>(ab.max_degree, count);
+  const u64 slots = u64(1) << std::max<u32>(5, ceil_log2_u64(2 * (max_cap ? max_cap : 1)));
+  if (slots > (u64(1) << 13) && (ab.count(4) + ab.count(5))) {
+    int blocks = 0;
+    const size_t bytes = aggregate_table_bytes(slots, &blocks);
+    table.alloc(bytes / sizeof(double) + 1);
+    a.table = table.p;
+    a.table_slots = slots;
+  }
+  aggregate_rows(a, ab, s);
+  DBuf<u64> noff(count + 1);
+  exclusive_scan_u32_to_u64(fill.p, noff.p, count, s);
+  const u64 A = read_scalar(noff.p + count, s);
+  out.n = count;
+  out.arcs = A;
+  out.off = std::move(noff);
+  out.tgt.alloc(A ? A : 1);
+  out.w.alloc(A ? A : 1);
+  DBuf<double> tw(1);
+  compact_rows(hoff.p, htgt.p, hw.p, fill.p, out.off.p, count, out.tgt.p, out.w.p, tw.p, s);
+  if (canonical && A) {
+    DBuf<u32> mx(1);
+    reduce_max_u32(fill.p, count, mx.p, s);
+    const u32 max_row = read_scalar(mx.p, s);
+    segmented_sort_u32(out.tgt.p, out.w.p, out.off.p, count, max_row, s);
+  }
+  out.total_weight = read_scalar(tw.p, s) / 2.0;
+}
+
+double modularity_device(const DGraph& g, const Bins& b, const u32* C, u64 width, double m,
+                         cudaStream_t s) {
+  DBuf<double> tot(width ? width : 1), sums(2);
+  modularity_terms(g, b, C, tot.p, width, sums.p, s, 2.0 * m);
+  double* h = reinterpret_cast<double*>(ctx().pinned);
+  LVN_CUDA(cudaMemcpyAsync(h, sums.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  return h[0] / (2.0 * m) - h[1];
+}
+
+void check_err(const u32* err, cudaStream_t s) {
+  const u32 e = read_scalar(err, s);
+  if (e & kErrLookup) fail(kInternal, "dendrogram lookup index out of range");
+  if (e & kErrTable) fail(kInternal, "aggregation table exhausted; capacity invariant violated");
+  if (e) fail(kInternal, "device invariant violated");
+}
+
+// ---------------------------------------------------------------------------
+// Louvain pass shell
+// ---------------------------------------------------------------------------
+void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
+  const auto t_start = Clock::now();
+  Context& c = ctx();
+  cudaStream_t s = c.stream;
+  validate(p);
+  check_csr_header(in);
+  const double m = in->total_weight;
+  if (!(m > 0.0)) fail(kDegenerate, "cannot cluster a graph with zero total weight");
+  InGraph ig;
+  load_graph(in, s, ig, &r->h2d_seconds);
+  const u32 N = ig.g.n;
+  const BinEdges edges = edges_of(p);
+  Timing tm;
+
+  DBuf<u32> global(N ? N : 1), C(N ? N : 1), used, rank;
+  DBuf<double> K(N ? N : 1), S(N ? N : 1), table;
+  DBuf<u8> flags(N ? N : 1);
+  DBuf<IterRecord> rec(1);
+  DBuf<u32> err(1);
+  LVN_CUDA(cudaMemsetAsync(err.p, 0, sizeof(u32), s));
+  iota_u32(global.p, N, s);
+
+  Bins in_bins, bins;
+  bool have_in_bins = false;
+  OwnedCsr owned[2];
+  DGraph cur = ig.g;
+  double tolerance = p.initial_tolerance;
+  double t_move = 0.0, t_aggregate = 0.0;
+  std::vector<int> its;
+  std::vector<double> tols, pass_secs;
+  std::vector<u32> vpp;
+  std::vector<u64> app;
+  int passes = 0, aggregations = 0;
+
+  for (int pass = 0; pass < p.max_passes; ++pass) {
+    const auto t_pass = Clock::now();
+    const u32 nv = cur.n;
+    Bins& B = pass == 0 ? in_bins : bins;
+    compute_bins(cur.off, nv, edges, B, s);
+    if (pass == 0) have_in_bins = true;
+    size_t sp = tm.begin(LVN_STAT_RESET, s);
+    pass_reset(cur, B, K.p, S.p, C.p, flags.p, s);
+    tm.end(sp, s, 4.0 * double(cur.arcs) + 29.0 * nv);
+
+    MoveArgs a;
+    a.g = cur;
+    a.C = C.p;
+    a.K = K.p;
+    a.sigma = S.p;
+    a.flags = flags.p;
+    a.m = m;
+    a.prune = p.prune;
+    a.gain_acc = &rec.p->gain;
+    a.counters = &rec.p->verts;
+    a.err = err.p;
+    if (B.count(5)) {
+      int blocks = 0;
+      const size_t bytes = move_table_bytes(B.max_degree, p.value_bits, &blocks);
+      table.ensure(bytes / sizeof(double) + 1);
+      a.table = table.p;
+      a.table_slots = u64(1) << ceil_log2_u64(2 * B.max_degree);
+    }
+    const auto t0 = Clock::now();
+    int iterations = 0;
+    for (int it = 0; it < p.max_iterations; ++it) {
+      a.pickless = pick_less_active(it, p.pick_less_period);
+      LVN_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(IterRecord), s));
+      sp = tm.begin(LVN_STAT_MOVE, s);
+      move_sweep(a, B, p.value_bits, s);
+      tm.end(sp, s, 0.0);
+      IterRecord* h = reinterpret_cast<IterRecord*>(c.pinned);
+      LVN_CUDA(cudaMemcpyAsync(h, rec.p, sizeof(IterRecord), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaStreamSynchronize(s));
+      tm.set_bytes(sp, 12.0 * double(h->arcs) + 32.0 * double(h->verts), h->verts, h->arcs);
+      ++iterations;
+      if (h->gain <= tolerance) break;  // louvain_compact.cpp:209
+    }
+    t_move += since(t0);
+    ++passes;
+    its.push_back(iterations);
+    tols.push_back(tolerance);
+    vpp.push_back(nv);
+    app.push_back(cur.arcs);
+
+    if (iterations <= 1) {  // no effective movement (louvain_compact.cpp:370-374)
+      sp = tm.begin(LVN_STAT_RENUMBER, s);
+      lookup(global.p, N, C.p, nv, err.p, s);
+      tm.end(sp, s, 12.0 * N);
+      pass_secs.push_back(since(t_pass));
+      break;
+    }
+    sp = tm.begin(LVN_STAT_RENUMBER, s);
+    const u32 count = renumber_device(C.p, nv, nv, used, rank, s, false);
+    tm.end(sp, s, 12.0 * nv);
+    if (double(count) / nv > p.aggregation_tolerance) {  // low shrink (louvain_compact.cpp:375-380)
+      sp = tm.begin(LVN_STAT_RENUMBER, s);
+      lookup(global.p, N, C.p, nv, err.p, s);
+      tm.end(sp, s, 12.0 * N);
+      pass_secs.push_back(since(t_pass));
+      break;
+    }
+    sp = tm.begin(LVN_STAT_RENUMBER, s);
+    remap(C.p, nv, rank.p, s);                  // renumber_communities (louvain_compact.cpp:382)
+    lookup(global.p, N, C.p, nv, err.p, s);     // lookup_dendrogram (louvain_compact.cpp:383)
+    tm.end(sp, s, 12.0 * nv + 12.0 * N);
+    const auto t1 = Clock::now();
+    OwnedCsr& next = owned[pass & 1];
+    sp = tm.begin(LVN_STAT_AGGREGATE, s);
+    aggregate_device(cur, C.p, count, edges, next, err.p, s, false);
+    tm.end(sp, s, 12.0 * double(cur.arcs) + 16.0 * nv + 8.0 * double(next.arcs) + 8.0 * (count + 1.0),
+           nv, cur.arcs);
+    t_aggregate += since(t1);
+    cur = next.view();
+    ++aggregations;
+    tolerance /= p.tolerance_drop;
+    pass_secs.push_back(since(t_pass));
+    // the other ping-pong buffer is free for the pass after this one
+    owned[(pass + 1) & 1] = OwnedCsr();
+  }
+  check_err(err.p, s);
+
+  // final renumber (louvain_compact.cpp:394) and modularity on the input graph (:396)
+  size_t sp = tm.begin(LVN_STAT_RENUMBER, s);
+  const u32 count = renumber_device(global.p, N, N, used, rank, s, true);
+  tm.end(sp, s, 24.0 * N);
+  if (!have_in_bins) compute_bins(ig.g.off, N, edges, in_bins, s);
+  sp = tm.begin(LVN_STAT_MODULARITY, s);
+  const double q = modularity_device(ig.g, in_bins, global.p, count, m, s);
+  tm.end(sp, s, 12.0 * double(ig.g.arcs) + 12.0 * N, N, ig.g.arcs);
+
+  r->num_vertices = N;
+  r->num_communities = count;
+  r->modularity = q;
+  r->passes = passes;
+  r->aggregations = aggregations;
+  const size_t k = size_t(passes);
+  r->iterations_per_pass = static_cast<int*>(std::calloc(k + 1, sizeof(int)));
+  r->tolerance_per_pass = static_cast<double*>(std::calloc(k + 1, sizeof(double)));
+  r->pass_seconds = static_cast<double*>(std::calloc(k + 1, sizeof(double)));
+  r->vertices_per_pass = static_cast<u32*>(std::calloc(k + 1, sizeof(u32)));
+  r->arcs_per_pass = static_cast<u64*>(std::calloc(k + 1, sizeof(u64)));
+  for (size_t i = 0; i < k; ++i) {
+    r->iterations_per_pass[i] = its[i];
+    r->tolerance_per_pass[i] = tols[i];
+    r->pass_seconds[i] = i < pass_secs.size() ? pass_secs[i] : 0.0;
+    r->vertices_per_pass[i] = vpp[i];
+    r->arcs_per_pass[i] = app[i];
+  }
+  const auto t_d2h = Clock::now();
+  if (p.membership_on_device) {
+    r->membership = global.p;  // ownership moves to the result (released by lvn_result_free)
+    global.p = nullptr;
+    global.n = 0;
+    r->membership_on_device = 1;
+  } else {
+    r->membership = static_cast<u32*>(std::malloc(size_t(N ? N : 1) * sizeof(u32)));
+    if (!r->membership) fail(kOom, "host allocation of the membership failed");
+    if (N) LVN_CUDA(cudaMemcpyAsync(r->membership, global.p, size_t(N) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    r->membership_on_device = 0;
+  }
+  r->d2h_seconds = since(t_d2h);
+  tm.collect(r->stats);
+  r->wall_seconds = since(t_start);
+  r->local_moving = t_move;
+  r->aggregation = t_aggregate;
+  r->other = r->wall_seconds - t_move - t_aggregate;
+}
+
+thread_local std::string t_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    Context& c = ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    LVN_CUDA(cudaSetDevice(c.device));
+    f(c);
+    return kOk;
+  } catch (const Error& e) {
+    t_err = e.what;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    t_err = "host allocation failed";
+    return kOom;
+  } catch (const std::exception& e) {
+    t_err = e.what();
+    return kInternal;
+  }
+}
+
+struct DGraphHandle {
+  OwnedCsr g;
+};
+
+}  // namespace
+}  // namespace lvn
+
+// holey-row capacity kernel (used by aggregate_device)
+namespace lvn {
+__global__ void cap_budgets_k(const u64* __restrict__ budget, u64* __restrict__ capped, u32 count) {
+  for (u64 c = blockIdx.x * u64(blockDim.x) + threadIdx.x; c < count;
+       c += u64(gridDim.x) * blockDim.x)
+    capped[c] = budget[c] < count ? budget[c] : u64(count);
+}
+void cap_budgets(const u64* budget, u64* capped, u32 count, cudaStream_t s) {
+  if (!count) return;
+  const u64 blocks = std::min<u64>((u64(count) + 255) / 256, u64(sm_count()) * 8);
+  cap_budgets_k<<<unsigned(blocks), 256, 0, s>>>(budget, capped, count);
+  LVN_LAUNCH();
+}
+}  // namespace lvn
+
+// ===========================================================================
+// C-ABI
+// ===========================================================================
+using namespace lvn;
+
+extern "C" {
+
+const char* lvn_version(void) { return "lvn 0.1 (sm_100a)"; }
+const char* lvn_last_error(void) { return t_err.c_str(); }
+unsigned long long lvn_launch_count(void) { return g_launches.load(); }
+
+void lvn_params_default(lvn_params* p) {
+  if (!p) return;
+  std::memset(p, 0, sizeof(*p));
+  p->max_passes = 10;
+  p->max_iterations = 20;
+  p->initial_tolerance = 0.01;
+  p->tolerance_drop = 10.0;
+  p->aggregation_tolerance = 0.8;
+  p->thread_count = 0;
+  p->chunk_size = 2048;
+  p->prune = 1;
+  p->pick_less_period = 4;
+  p->switch_move = 64;
+  p->switch_aggregate = 128;
+  p->probing = LVN_QUADRATIC_DOUBLE;
+  p->value_bits = 32;
+  p->bin_thread_max = 4;
+  p->bin_group_max = 32;
+  p->bin_warp_max = 256;
+  p->bin_block_max = 4096;
+  p->membership_on_device = 0;
+}
+
+int lvn_init(int num_gpus, const int* devices) {
+  try {
+    if (num_gpus < 0) fail(kInvalid, "num_gpus must be >= 0");
+    if (num_gpus > 1) fail(kInvalid, "one device per process: shard across ranks (one process per GPU)");
+    init_context(num_gpus == 1 && devices ? devices[0] : 0);
+    return kOk;
+  } catch (const Error& e) {
+    t_err = e.what;
+    return e.code;
+  }
+}
+
+int lvn_finalize(void) {
+  destroy_context();
+  return kOk;
+}
+
+void lvn_result_free(lvn_result* r) {
+  if (!r) return;
+  if (r->membership) {
+    if (r->membership_on_device) {
+      try {
+        ctx().pool.put(r->membership);
+      } catch (...) {
+      }
+    } else {
+      std::free(r->membership);
+    }
+  }
+  std::free(r->iterations_per_pass);
+  std::free(r->tolerance_per_pass);
+  std::free(r->pass_seconds);
+  std::free(r->vertices_per_pass);
+  std::free(r->arcs_per_pass);
+  delete r;
+}
+
+void lvn_graph_free(lvn_graph_out* g) {
+  if (!g) return;
+  std::free(g->offsets);
+  std::free(g->targets);
+  std::free(g->weights);
+  delete g;
+}
+
+int lvn_louvain(const lvn_csr* g, const lvn_params* p, lvn_result** out) {
+  if (!out) {
+    t_err = "null output";
+    return kInvalid;
+  }
+  *out = nullptr;
+  lvn_params def;
+  lvn_params_default(&def);
+  auto* r = new lvn_result;
+  std::memset(r, 0, sizeof(*r));
+  const int rc = guard([&](Context&) { run_louvain(g, p ? *p : def, r); });
+  if (rc) {
+    lvn_result_free(r);
+    return rc;
+  }
+  *out = r;
+  return kOk;
+}
+
+int lvn_modularity(const lvn_csr* g, const uint32_t* membership, int membership_location, double* q) {
+  return guard([&](Context& c) {
+    if (!q) fail(kInvalid, "null output");
+    check_csr_header(g);
+    if (!(g->total_weight > 0.0))
+      fail(kDegenerate, "modularity is undefined when the total edge weight is zero");
+    cudaStream_t s = c.stream;
+    InGraph ig;
+    load_graph(g, s, ig, nullptr);
+    DevU32 memb;
+    load_u32(membership, ig.g.n, membership_location, s, memb);
+    DBuf<u32> mx(1);
+    reduce_max_u32(memb.p, ig.g.n, mx.p, s);
+    const u64 width = ig.g.n ? u64(read_scalar(mx.p, s)) + 1 : 0;
+    lvn_params d;
+    lvn_params_default(&d);
+    Bins b;
+    compute_bins(ig.g.off, ig.g.n, edges_of(d), b, s);
+    *q = modularity_device(ig.g, b, memb.p, width, g->total_weight, s);
+  });
+}
+
+int lvn_vertex_weights(const lvn_csr* g, double* out_host) {
+  return guard([&](Context& c) {
+    if (!out_host) fail(kInvalid, "null output");
+    cudaStream_t s = c.stream;
+    InGraph ig;
+    load_graph(g, s, ig, nullptr);
+    lvn_params d;
+    lvn_params_default(&d);
+    Bins b;
+    compute_bins(ig.g.off, ig.g.n, edges_of(d), b, s);
+    DBuf<double> K(ig.g.n ? ig.g.n : 1);
+    vertex_weights(ig.g, b, K.p, s);
+    if (ig.g.n) LVN_CUDA(cudaMemcpyAsync(out_host, K.p, ig.g.n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int lvn_count_communities(const uint32_t* membership, uint64_t n, int location, uint32_t* count) {
+  return guard([&](Context& c) {
+    if (!count) fail(kInvalid, "null output");
+    cudaStream_t s = c.stream;
+    if (n == 0) {
+      *count = 0;
+      return;
+    }
+    DevU32 m;
+    load_u32(membership, n, location, s, m);
+    DBuf<u32> mx(1), used, rank;
+    reduce_max_u32(m.p, n, mx.p, s);
+    const u64 width = u64(read_scalar(mx.p, s)) + 1;
+    *count = renumber_device(m.p, n, width, used, rank, s, false);
+  });
+}
+
+int lvn_renumber(uint32_t* membership, uint64_t n, int location, uint32_t* count) {
+  return guard([&](Context& c) {
+    cudaStream_t s = c.stream;
+    u32 k = 0;
+    if (n) {
+      DevU32 m;
+      load_u32(membership, n, location, s, m);
+      DBuf<u32> mx(1), used, rank;
+      reduce_max_u32(m.p, n, mx.p, s);
+      const u64 width = u64(read_scalar(mx.p, s)) + 1;
+      k = renumber_device(m.p, n, width, used, rank, s, true);
+      if (location == LVN_HOST)
+        LVN_CUDA(cudaMemcpyAsync(membership, m.p, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaStreamSynchronize(s));
+    }
+    if (count) *count = k;
+  });
+}
+
+int lvn_lookup_dendrogram(uint32_t* membership, uint64_t n, const uint32_t* level, uint64_t nl,
+                          int location) {
+  return guard([&](Context& c) {
+    cudaStream_t s = c.stream;
+    if (!n) return;
+    DevU32 m, l;
+    load_u32(membership, n, location, s, m);
+    load_u32(level, nl, location, s, l);
+    DBuf<u32> err(1);
+    LVN_CUDA(cudaMemsetAsync(err.p, 0, sizeof(u32), s));
+    lookup(m.p, n, l.p, nl, err.p, s);
+    check_err(err.p, s);
+    if (location == LVN_HOST)
+      LVN_CUDA(cudaMemcpyAsync(membership, m.p, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int lvn_community_csr(const uint32_t* membership, uint32_t n, uint32_t count, int location,
+                      uint64_t* offsets, uint32_t* members) {
+  return guard([&](Context& c) {
+    if (!offsets || (n && !members)) fail(kInvalid, "null output");
+    cudaStream_t s = c.stream;
+    DevU32 m;
+    load_u32(membership, n, location, s, m);
+    if (n) {
+      DBuf<u32> mx(1);
+      reduce_max_u32(m.p, n, mx.p, s);
+      if (read_scalar(mx.p, s) >= count) fail(kInvalid, "membership id out of range");
+    }
+    DBuf<u32> msize(count ? count : 1), cursor(count ? count : 1), mem(n ? n : 1);
+    DBuf<u64> budget(count + 1), coff(count + 1);
+    DGraph none;
+    none.n = n;
+    community_counts(none, m.p, count, msize.p, budget.p, s);
+    exclusive_scan_u32_to_u64(msize.p, coff.p, count, s);
+    community_scatter(m.p, n, coff.p, count, cursor.p, mem.p, s);
+    if (count) {
+      DBuf<u32> mx(1);
+      reduce_max_u32(msize.p, count, mx.p, s);
+      segmented_sort_u32(mem.p, nullptr, coff.p, count, read_scalar(mx.p, s), s);
+    }
+    LVN_CUDA(cudaMemcpyAsync(offsets, coff.p, (u64(count) + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    if (n) LVN_CUDA(cudaMemcpyAsync(members, mem.p, u64(n) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+int lvn_aggregate(const lvn_csr* g, const uint32_t* membership, int membership_location,
+                  int canonical, const lvn_params* p, lvn_graph_out** out) {
+  if (!out) {
+    t_err = "null output";
+    return kInvalid;
+  }
+  *out = nullptr;
+  lvn_graph_out* res = nullptr;
+  const int rc = guard([&](Context& c) {
+    lvn_params def;
+    lvn_params_default(&def);
+    const lvn_params& pp = p ? *p : def;
+    validate(pp);
+    cudaStream_t s = c.stream;
+    InGraph ig;
+    load_graph(g, s, ig, nullptr);
+    DevU32 m;
+    load_u32(membership, ig.g.n, membership_location, s, m);
+    // contiguity check (louvain_mc.cpp:106-112): max id + 1 == distinct count
+    u32 count = 0;
+    if (ig.g.n) {
+      DBuf<u32> mx(1), used, rank;
+      reduce_max_u32(m.p, ig.g.n, mx.p, s);
+      const u64 width = u64(read_scalar(mx.p, s)) + 1;
+      count = renumber_device(m.p, ig.g.n, width, used, rank, s, false);
+      if (count != width) fail(kInvalid, "membership ids must be contiguous");
+    }
+    DBuf<u32> err(1);
+    LVN_CUDA(cudaMemsetAsync(err.p, 0, sizeof(u32), s));
+    OwnedCsr o;
+    aggregate_device(ig.g, m.p, count, edges_of(pp), o, err.p, s, canonical != 0);
+    check_err(err.p, s);
+    res = new lvn_graph_out;
+    res->num_vertices = o.n;
+    res->num_arcs = o.arcs;
+    res->total_weight = o.total_weight;
+    res->offsets = static_cast<u64*>(std::malloc((u64(o.n) + 1) * sizeof(u64)));
+    res->targets = static_cast<u32*>(std::malloc((o.arcs ? o.arcs : 1) * sizeof(u32)));
+    res->weights = static_cast<float*>(std::malloc((o.arcs ? o.arcs : 1) * sizeof(float)));
+    if (!res->offsets || !res->targets || !res->weights) fail(kOom, "host allocation failed");
+    LVN_CUDA(cudaMemcpyAsync(res->offsets, o.off.p, (u64(o.n) + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    if (o.arcs) {
+      LVN_CUDA(cudaMemcpyAsync(res->targets, o.tgt.p, o.arcs * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaMemcpyAsync(res->weights, o.w.p, o.arcs * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    LVN_CUDA(cudaStreamSynchronize(s));
+  });
+  if (rc) {
+    lvn_graph_free(res);
+    return rc;
+  }
+  *out = res;
+  return kOk;
+}
+
+int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
+                       const double* community_w, double m, const lvn_params* p, int force_kernel,
+                       uint32_t* to, double* gain) {
+  return guard([&](Context& c) {
+    lvn_params def;
+    lvn_params_default(&def);
+    const lvn_params& pp = p ? *p : def;
+    validate(pp);
+    if (!to || !gain || !vertex_w || !community_w) fail(kInvalid, "null argument");
+    if (!(m > 0.0)) fail(kDegenerate, "m must be > 0");
+    cudaStream_t s = c.stream;
+    InGraph ig;
+    load_graph(g, s, ig, nullptr);
+    const u32 n = ig.g.n;
+    DevU32 mb;
+    load_u32(membership, n, LVN_HOST, s, mb);
+    DBuf<double> K(n ? n : 1), S(n ? n : 1), og(n ? n : 1), table;
+    DBuf<u32> ot(n ? n : 1);
+    if (n) {
+      LVN_CUDA(cudaMemcpyAsync(K.p, vertex_w, n * sizeof(double), cudaMemcpyHostToDevice, s));
+      LVN_CUDA(cudaMemcpyAsync(S.p, community_w, n * sizeof(double), cudaMemcpyHostToDevice, s));
+    }
+    BinEdges e = edges_of(pp);
+    if (force_kernel >= 1) e.thread_max = 0;
+    if (force_kernel >= 2) e.group_max = 0;
+    if (force_kernel >= 3) e.warp_max = 0;
+    if (force_kernel >= 4) e.block_max = 0;
+    Bins b;
+    compute_bins(ig.g.off, n, e, b, s);
+    // isolated vertices stay (louvain_compact.cpp:424)
+    if (n) {
+      LVN_CUDA(cudaMemcpyAsync(ot.p, mb.p, n * sizeof(u32), cudaMemcpyDeviceToDevice, s));
+      LVN_CUDA(cudaMemsetAsync(og.p, 0, n * sizeof(double), s));
+    }
+    DBuf<IterRecord> rec(1);
+    DBuf<u32> err(1);
+    LVN_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(IterRecord), s));
+    LVN_CUDA(cudaMemsetAsync(err.p, 0, sizeof(u32), s));
+    MoveArgs a;
+    a.g = ig.g;
+    a.C = mb.p;
+    a.K = K.p;
+    a.sigma = S.p;
+    a.m = m;
+    a.dry = 1;
+    a.out_to = ot.p;
+    a.out_gain = og.p;
+    a.gain_acc = &rec.p->gain;
+    a.counters = &rec.p->verts;
+    a.err = err.p;
+    if (b.count(5)) {
+      int blocks = 0;
+      const size_t bytes = move_table_bytes(b.max_degree, pp.value_bits, &blocks);
+      table.alloc(bytes / sizeof(double) + 1);
+      a.table = table.p;
+      a.table_slots = u64(1) << ceil_log2_u64(2 * b.max_degree);
+    }
+    move_sweep(a, b, pp.value_bits, s);
+    if (n) {
+      LVN_CUDA(cudaMemcpyAsync(to, ot.p, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaMemcpyAsync(gain, og.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));
+    }
+    LVN_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+// ---- device-resident graphs ----------------------------------------------------
+struct lvn_dgraph {
+  lvn::OwnedCsr g;
+};
+
+int lvn_generate(const lvn_gen_params* gp, lvn_dgraph** out) {
+  if (!out || !gp) {
+    t_err = "null argument";
+    return kInvalid;
+  }
+  *out = nullptr;
+  auto* h = new lvn_dgraph;
+  const int rc = guard([&](Context& c) {
+    GenSpec sp;
+    sp.kind = gp->kind;
+    sp.n = gp->n;
+    sp.edges = gp->edges;
+    sp.scale = gp->scale;
+    sp.blocks = gp->blocks;
+    sp.a = gp->a;
+    sp.b = gp->b;
+    sp.c = gp->c;
+    sp.mu = gp->mu;
+    sp.p = gp->p;
+    sp.avg_degree = gp->avg_degree;
+    sp.seed = gp->seed;
+    generate(sp, h->g, c.stream);
+  });
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return kOk;
+}
+
+int lvn_dgraph_upload(const lvn_csr* host, lvn_dgraph** out) {
+  if (!out) {
+    t_err = "null output";
+    return kInvalid;
+  }
+  *out = nullptr;
+  auto* h = new lvn_dgraph;
+  const int rc = guard([&](Context& c) {
+    if (!host || host->location != LVN_HOST) fail(kInvalid, "host graph expected");
+    InGraph ig;
+    load_graph(host, c.stream, ig, nullptr);
+    h->g.n = ig.g.n;
+    h->g.arcs = ig.g.arcs;
+    h->g.off = std::move(ig.off);
+    h->g.tgt = std::move(ig.tgt);
+    h->g.w = std::move(ig.w);
+    h->g.total_weight = host->total_weight;
+  });
+  if (rc) {
+    delete h;
+    return rc;
+  }
+  *out = h;
+  return kOk;
+}
+
+int lvn_dgraph_view(const lvn_dgraph* g, lvn_csr* view) {
+  if (!g || !view) {
+    t_err = "null argument";
+    return kInvalid;
+  }
+  view->num_vertices = g->g.n;
+  view->num_arcs = g->g.arcs;
+  view->offsets = g->g.off.p;
+  view->targets = g->g.tgt.p;
+  view->weights = g->g.w.p;
+  view->total_weight = g->g.total_weight;
+  view->location = LVN_DEVICE;
+  return kOk;
+}
+
+int lvn_dgraph_download(const lvn_dgraph* g, uint64_t* offsets, uint32_t* targets, float* weights) {
+  return guard([&](Context& c) {
+    if (!g) fail(kInvalid, "null graph");
+    cudaStream_t s = c.stream;
+    if (offsets)
+      LVN_CUDA(cudaMemcpyAsync(offsets, g->g.off.p, (u64(g->g.n) + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    if (targets && g->g.arcs)
+      LVN_CUDA(cudaMemcpyAsync(targets, g->g.tgt.p, g->g.arcs * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    if (weights && g->g.arcs)
+      LVN_CUDA(cudaMemcpyAsync(weights, g->g.w.p, g->g.arcs * sizeof(float), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+  });
+}
+
+void lvn_dgraph_free(lvn_dgraph* g) {
+  if (!g) return;
+  try {
+    Context& c = ctx();
+    std::lock_guard<std::mutex> lk(c.mu);
+    (void)cudaStreamSynchronize(c.stream);
+    delete g;
+  } catch (...) {
+  }
+}
+
+int lvn_device_alloc(size_t bytes, void** ptr) {
+  return guard([&](Context&) {
+    if (!ptr) fail(kInvalid, "null output");
+    LVN_CUDA(cudaMalloc(ptr, bytes ? bytes : 1));
+  });
+}
+
+int lvn_device_free(void* ptr) {
+  return guard([&](Context& c) {
+    LVN_CUDA(cudaStreamSynchronize(c.stream));
+    LVN_CUDA(cudaFree(ptr));
+  });
+}
+
+int lvn_memcpy(void* dst, const void* src, size_t bytes, int kind) {
+  return guard([&](Context& c) {
+    const cudaMemcpyKind k = kind == 1 ? cudaMemcpyHostToDevice
+                             : kind == 2 ? cudaMemcpyDeviceToHost
+                                         : cudaMemcpyDeviceToDevice;
+    LVN_CUDA(cudaMemcpyAsync(dst, src, bytes, k, c.stream));
+    LVN_CUDA(cudaStreamSynchronize(c.stream));
+  });
+}
+
+}  // extern "C"

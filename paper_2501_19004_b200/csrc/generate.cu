@@ -1,0 +1,304 @@
+// Device-side synthetic graph construction (SURVEY 8(d) C1-C5 shapes; the
+// device replacement of build_csr, graph.cpp:15-87, for unit-weight inputs):
+// sample undirected edges with a counter-based hash RNG, emit both arcs as
+// 64-bit (source<<32 | target) keys, drop self-loops, sort, deduplicate, and
+// build the CSR (rows sorted by target, unit weights, m = arcs / 2).
+//
+// This is input plumbing, not the timed hot path; the key sort uses CUB's
+// radix sort (library code, like cuBLAS for a plain GEMM).
+#include <cub/device/device_radix_sort.cuh>
+
+#include <cmath>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace lvn {
+
+namespace {
+
+constexpr ull kDrop = ~0ull;
+
+__device__ __forceinline__ u64 mix64(u64 z) {
+  z += 0x9E3779B97F4A7C15ull;
+  z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+  z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+  return z ^ (z >> 31);
+}
+__device__ __forceinline__ double unit(u64 x) { return double(x >> 11) * (1.0 / 9007199254740992.0); }
+__device__ __forceinline__ u64 below(u64 x, u64 n) {  // uniform in [0, n) from 64 random bits
+  return u64((unsigned __int128)x * n >> 64);
+}
+
+__device__ __forceinline__ void emit(ull* keys, u64 e, u32 u, u32 v) {
+  if (u == v) {
+    keys[2 * e] = kDrop;
+    keys[2 * e + 1] = kDrop;
+  } else {
+    keys[2 * e] = (ull(u) << 32) | v;
+    keys[2 * e + 1] = (ull(v) << 32) | u;
+  }
+}
+
+// Graph500 R-MAT: 2^scale vertices, quadrant (a, b, c, d) per level
+__global__ void gen_rmat(ull* keys, u64 edges, u32 scale, double a, double b, double c, u64 seed) {
+  for (u64 e = blockIdx.x * u64(blockDim.x) + threadIdx.x; e < edges;
+       e += u64(gridDim.x) * blockDim.x) {
+    u32 u = 0, v = 0;
+    const u64 base = mix64(seed ^ mix64(e));
+    for (u32 l = 0; l < scale; ++l) {
+      const double r = unit(mix64(base + l));
+      u32 bu = 0, bv = 0;
+      if (r < a) {
+      } else if (r < a + b) {
+        bv = 1;
+      } else if (r < a + b + c) {
+        bu = 1;
+      } else {
+        bu = 1, bv = 1;
+      }
+      u = (u << 1) | bu;
+      v = (v << 1) | bv;
+    }
+    emit(keys, e, u, v);
+  }
+}
+
+// planted partition: u ~ U(n); v ~ U(block(u)) with probability 1 - mu, else U(n)
+__global__ void gen_sbm(ull* keys, u64 edges, u64 n, u64 blocks, double mu, u64 seed) {
+  const u64 bsize = n / blocks;
+  for (u64 e = blockIdx.x * u64(blockDim.x) + threadIdx.x; e < edges;
+       e += u64(gridDim.x) * blockDim.x) {
+    const u64 r0 = mix64(seed ^ mix64(3 * e)), r1 = mix64(seed ^ mix64(3 * e + 1)),
+              r2 = mix64(seed ^ mix64(3 * e + 2));
+    const u64 u = below(r0, n);
+    u64 v;
+    if (unit(r1) < mu) {
+      v = below(r2, n);
+    } else {
+      u64 blk = u / bsize;
+      if (blk >= blocks) blk = blocks - 1;
+      const u64 lo = blk * bsize, hi = (blk == blocks - 1) ? n : lo + bsize;
+      v = lo + below(r2, hi - lo);
+    }
+    emit(keys, e, u32(u), u32(v));
+  }
+}
+
+// 2-D lattice side x side, each lattice edge kept with probability p
+__global__ void gen_grid(ull* keys, u64 side, double p, u64 seed) {
+  const u64 horiz = side * (side - 1);
+  const u64 edges = 2 * horiz;
+  for (u64 e = blockIdx.x * u64(blockDim.x) + threadIdx.x; e < edges;
+       e += u64(gridDim.x) * blockDim.x) {
+    u64 u, v;
+    if (e < horiz) {  // (r, c) - (r, c+1)
+      const u64 r = e / (side - 1), c = e % (side - 1);
+      u = r * side + c;
+      v = u + 1;
+    } else {  // (r, c) - (r+1, c)
+      const u64 k = e - horiz;
+      u = k;
+      v = k + side;
+    }
+    if (unit(mix64(seed ^ mix64(e))) < p)
+      emit(keys, e, u32(u), u32(v));
+    else
+      keys[2 * e] = keys[2 * e + 1] = kDrop;
+  }
+}
+
+__global__ void gen_uniform(ull* keys, u64 edges, u64 n, u64 seed) {
+  for (u64 e = blockIdx.x * u64(blockDim.x) + threadIdx.x; e < edges;
+       e += u64(gridDim.x) * blockDim.x) {
+    const u64 u = below(mix64(seed ^ mix64(2 * e)), n), v = below(mix64(seed ^ mix64(2 * e + 1)), n);
+    emit(keys, e, u32(u), u32(v));
+  }
+}
+
+// Web-crawl shape: hosts are contiguous id ranges; vertex u emits deg(u)
+// (truncated power law) edges, most inside its host within a locality
+// window, the rest to global preferential-attachment targets (low ids).
+__global__ void gen_web(ull* keys, const u64* __restrict__ eoff, u64 n, const u32* __restrict__ host_lo,
+                        const u32* __restrict__ host_hi, double p_local, u64 window, u64 seed) {
+  for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n;
+       u += u64(gridDim.x) * blockDim.x) {
+    const u64 e0 = eoff[u], e1 = eoff[u + 1];
+    const u64 lo = host_lo[u], hi = host_hi[u];
+    for (u64 e = e0; e < e1; ++e) {
+      const u64 r0 = mix64(seed ^ mix64(2 * e)), r1 = mix64(seed ^ mix64(2 * e + 1));
+      u64 v;
+      if (unit(r0) < p_local) {
+        const u64 a = u > lo + window ? u - window : lo;
+        const u64 b = u + window + 1 < hi ? u + window + 1 : hi;
+        v = a + below(r1, b - a);
+      } else {
+        // preferential attachment: P(v) ~ v^(-0.8) over the id space
+        const double x = unit(r1);
+        v = u64(double(n) * pow(x, 5.0));
+        if (v >= n) v = n - 1;
+      }
+      emit(keys, e, u32(u), u32(v));
+    }
+  }
+}
+
+__global__ void web_degrees(u64* __restrict__ deg, u64 n, double alpha, double dmin, double dmax,
+                            double scale, u64 seed) {
+  for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n;
+       u += u64(gridDim.x) * blockDim.x) {
+    // inverse-CDF sample of a power law truncated to [dmin, dmax]
+    const double x = unit(mix64(seed ^ mix64(u)));
+    const double a1 = 1.0 - alpha;
+    const double lo = pow(dmin, a1), hi = pow(dmax, a1);
+    const double d = pow(lo + x * (hi - lo), 1.0 / a1) * scale;
+    deg[u] = u64(d < 1.0 ? 1.0 : d);
+  }
+}
+
+__global__ void keep_flags(const ull* __restrict__ keys, u64 m, u32* __restrict__ keep) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < m;
+       i += u64(gridDim.x) * blockDim.x)
+    keep[i] = keys[i] != kDrop && (i == 0 || keys[i] != keys[i - 1]);
+}
+
+__global__ void place(const ull* __restrict__ keys, u64 m, const u32* __restrict__ keep,
+                      const u64* __restrict__ pos, u32* __restrict__ tgt, u32* __restrict__ deg) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < m;
+       i += u64(gridDim.x) * blockDim.x) {
+    if (!keep[i]) continue;
+    const ull k = keys[i];
+    tgt[pos[i]] = u32(k);
+    atomicAdd(&deg[u32(k >> 32)], 1u);
+  }
+}
+
+__global__ void fill_ones(float* w, u64 n) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+    w[i] = 1.0f;
+}
+
+unsigned grid(u64 n) {
+  return unsigned(std::max<u64>(1, std::min<u64>((n + 255) / 256, u64(sm_count()) * 32)));
+}
+
+}  // namespace
+
+// keys: 2 * edges arc keys (some kDrop) -> CSR over n vertices
+void keys_to_csr(DBuf<ull>& keys, u64 nkeys, u64 n, OwnedCsr& out, cudaStream_t s) {
+  DBuf<ull> sorted(nkeys);
+  const int end_bit = 32 + int(ceil_log2_u64(n ? n : 1));
+  size_t tmp_bytes = 0;
+  // valid keys have no bits at or above end_bit; the drop marker has all bits
+  // set, so it still sorts last
+  LVN_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, tmp_bytes, keys.p, sorted.p, nkeys, 0, end_bit, s));
+  {
+    DBuf<unsigned char> tmp(tmp_bytes);
+    LVN_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, tmp_bytes, keys.p, sorted.p, nkeys, 0, end_bit, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+  }
+  keys.release();
+  DBuf<u32> keep(nkeys);
+  keep_flags<<<grid(nkeys), 256, 0, s>>>(sorted.p, nkeys, keep.p);
+  LVN_LAUNCH();
+  DBuf<u64> pos(nkeys + 1);
+  exclusive_scan_u32_to_u64(keep.p, pos.p, nkeys, s);
+  u64 arcs = 0;
+  LVN_CUDA(cudaMemcpyAsync(&arcs, pos.p + nkeys, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  out.n = u32(n);
+  out.arcs = arcs;
+  out.tgt.alloc(arcs ? arcs : 1);
+  out.w.alloc(arcs ? arcs : 1);
+  out.off.alloc(n + 1);
+  DBuf<u32> deg(n ? n : 1);
+  LVN_CUDA(cudaMemsetAsync(deg.p, 0, (n ? n : 1) * sizeof(u32), s));
+  place<<<grid(nkeys), 256, 0, s>>>(sorted.p, nkeys, keep.p, pos.p, out.tgt.p, deg.p);
+  LVN_LAUNCH();
+  exclusive_scan_u32_to_u64(deg.p, out.off.p, n, s);
+  fill_ones<<<grid(arcs), 256, 0, s>>>(out.w.p, arcs);
+  LVN_LAUNCH();
+  out.total_weight = double(arcs) / 2.0;
+  LVN_CUDA(cudaStreamSynchronize(s));
+}
+
+void generate(const GenSpec& g, OwnedCsr& out, cudaStream_t s) {
+  u64 n = g.n, edges = g.edges;
+  DBuf<ull> keys;
+  switch (g.kind) {
+    case 0: {  // RMAT
+      if (g.scale == 0 || g.scale > 31) fail(kInvalid, "rmat scale must be in 1..31");
+      n = u64(1) << g.scale;
+      keys.alloc(2 * edges);
+      gen_rmat<<<grid(edges), 256, 0, s>>>(keys.p, edges, g.scale, g.a, g.b, g.c, g.seed);
+      break;
+    }
+    case 1: {  // SBM
+      if (!n || !g.blocks || g.blocks > n) fail(kInvalid, "sbm needs 1 <= blocks <= n");
+      keys.alloc(2 * edges);
+      gen_sbm<<<grid(edges), 256, 0, s>>>(keys.p, edges, n, g.blocks, g.mu, g.seed);
+      break;
+    }
+    case 2: {  // grid
+      const u64 side = g.n;
+      if (side < 2) fail(kInvalid, "grid side must be >= 2");
+      n = side * side;
+      edges = 2 * side * (side - 1);
+      keys.alloc(2 * edges);
+      gen_grid<<<grid(edges), 256, 0, s>>>(keys.p, side, g.p, g.seed);
+      break;
+    }
+    case 3: {  // web
+      if (n < 16) fail(kInvalid, "web graph needs n >= 16");
+      // host side: Zipf host sizes in [10, 1e6]
+      std::vector<u32> hlo(n), hhi(n);
+      u64 state = g.seed * 0x2545F4914F6CDD1Dull + 1;
+      auto rnd = [&]() {
+        state ^= state >> 12, state ^= state << 25, state ^= state >> 27;
+        return double((state * 0x2545F4914F6CDD1Dull) >> 11) * (1.0 / 9007199254740992.0);
+      };
+      for (u64 v = 0; v < n;) {
+        // P(size >= x) ~ x^-1 truncated to [10, 1e6]
+        const double x = rnd();
+        u64 size = u64(10.0 / (1.0 - x * (1.0 - 10.0 / 1e6)));
+        if (size > n - v) size = n - v;
+        for (u64 k = v; k < v + size; ++k) hlo[k] = u32(v), hhi[k] = u32(v + size);
+        v += size;
+      }
+      DBuf<u32> dlo(n), dhi(n);
+      LVN_CUDA(cudaMemcpyAsync(dlo.p, hlo.data(), n * 4, cudaMemcpyHostToDevice, s));
+      LVN_CUDA(cudaMemcpyAsync(dhi.p, hhi.data(), n * 4, cudaMemcpyHostToDevice, s));
+      DBuf<u64> deg(n), eoff(n + 1);
+      // out-degree power law (exponent 2.1) scaled to the requested mean
+      const double alpha = 2.1, dmin = 1.0, dmax = 1e5;
+      const double a1 = 1.0 - alpha, a2 = 2.0 - alpha;
+      const double mean_raw = (a1 / a2) * (std::pow(dmax, a2) - std::pow(dmin, a2)) /
+                              (std::pow(dmax, a1) - std::pow(dmin, a1));
+      const double target = g.avg_degree / 2.0 * 1.06;  // undirected samples per vertex
+      web_degrees<<<grid(n), 256, 0, s>>>(deg.p, n, alpha, dmin, dmax, target / mean_raw,
+                                          g.seed + 7);
+      LVN_LAUNCH();
+      exclusive_scan_u64(deg.p, eoff.p, n, s);
+      LVN_CUDA(cudaMemcpyAsync(&edges, eoff.p + n, sizeof(u64), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaStreamSynchronize(s));
+      keys.alloc(2 * edges);
+      gen_web<<<grid(n), 256, 0, s>>>(keys.p, eoff.p, n, dlo.p, dhi.p, 0.92, 64, g.seed);
+      LVN_LAUNCH();
+      LVN_CUDA(cudaStreamSynchronize(s));
+      break;
+    }
+    case 4: {  // uniform
+      if (n < 2) fail(kInvalid, "uniform graph needs n >= 2");
+      keys.alloc(2 * edges);
+      gen_uniform<<<grid(edges), 256, 0, s>>>(keys.p, edges, n, g.seed);
+      break;
+    }
+    default:
+      fail(kInvalid, "unknown generator kind");
+  }
+  LVN_LAUNCH();
+  if (n >= kEmpty) fail(kInvalid, "vertex count collides with the reserved sentinel id");
+  keys_to_csr(keys, 2 * edges, n, out, s);
+}
+
+}  // namespace lvn

@@ -1,0 +1,131 @@
+// Host-side launchers of the device kernels (one .cu per family). All run on
+// the context stream; none synchronises unless it says so.
+#pragma once
+
+#include "common.cuh"
+
+namespace lvn {
+
+// ---- scan.cu: exclusive prefix sums, out has n+1 entries (prefix_sum.hpp:12-23)
+void exclusive_scan_u32(const u32* in, u32* out, u64 n, cudaStream_t s);
+void exclusive_scan_u64(const u64* in, u64* out, u64 n, cudaStream_t s);
+void exclusive_scan_u32_to_u64(const u32* in, u64* out, u64 n, cudaStream_t s);
+// max-reduction of a u32 array into *out (device)
+void reduce_max_u32(const u32* in, u64 n, u32* out, cudaStream_t s);
+
+// ---- bins.cu: degree bins + pass reset ------------------------------------
+constexpr int kBins = 6;  // 0 isolated, 1 thread, 2 group8, 3 warp, 4 block, 5 global table
+struct BinEdges {
+  u32 thread_max = 4, group_max = 32, warp_max = 256, block_max = 4096;
+};
+struct Bins {
+  DBuf<u32> list;       // vertex ids grouped by bin, ascending within a bin
+  u64 start[kBins + 1]; // host copy of the bin boundaries in `list`
+  u64 max_degree = 0;
+  BinEdges edges;
+  u64 count(int b) const { return start[b + 1] - start[b]; }
+  const u32* of(int b) const { return list.p + start[b]; }
+};
+// bin of row v by min(off[v+1]-off[v], cap): rows of a CSR, or community
+// budgets during aggregation. Synchronises (reads the bin sizes).
+void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStream_t s,
+                  u64 cap = ~u64(0));
+// K_u = row sums (fp64), Sigma = K, C = identity, flags = deg > 0
+void pass_reset(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C, u8* flags,
+                cudaStream_t s);
+void vertex_weights(const DGraph& g, const Bins& b, double* K, cudaStream_t s);
+
+// ---- move.cu: local-moving sweep ------------------------------------------
+struct MoveArgs {
+  DGraph g;
+  u32* C = nullptr;
+  const double* K = nullptr;
+  double* sigma = nullptr;
+  u8* flags = nullptr;
+  double m = 1.0;
+  int pickless = 0;
+  int prune = 1;
+  int dry = 0;              // evaluate only: write out_to / out_gain, apply nothing
+  u32* out_to = nullptr;
+  double* out_gain = nullptr;
+  double* gain_acc = nullptr;  // summed gain of applied moves
+  ull* counters = nullptr;     // [0] vertices processed, [1] arcs scanned, [2] moves
+  u32* err = nullptr;
+  double* table = nullptr;     // global-table scratch for bin 5 (see move_table_bytes)
+  u64 table_slots = 0;         // slots per block
+};
+// one sweep over bins 1..5 (thread, group8, warp, block, global); the
+// force_kernel >= 0 variant routes every vertex to at least that class.
+void move_sweep(const MoveArgs& a, const Bins& bins, int value_bits, cudaStream_t s);
+size_t move_table_bytes(u64 max_degree, int value_bits, int* blocks);
+
+// ---- community.cu -----------------------------------------------------------
+// used[c] = 1 for every c in C (used zeroed here), sized n
+void mark_used(const u32* C, u64 n, u32* used, u64 width, cudaStream_t s);
+// C[v] = rank[C[v]]
+void remap(u32* C, u64 n, const u32* rank, cudaStream_t s);
+// global[i] = level[global[i]], range-checked into *err
+void lookup(u32* global, u64 n, const u32* level, u64 nl, u32* err, cudaStream_t s);
+// per-community member counts (u32) and arc budgets (u64), zeroed here
+void community_counts(const DGraph& g, const u32* C, u32 count, u32* members, u64* budget,
+                      cudaStream_t s);
+// members[coff[c] + cursor[c]++] = v (cursor zeroed here)
+void community_scatter(const u32* C, u32 n, const u64* coff, u32 count, u32* cursor, u32* members,
+                       cudaStream_t s);
+// sort every segment [off[i], off[i+1]) of keys ascending (vals permuted alongside)
+void segmented_sort_u32(u32* keys, float* vals, const u64* off, u32 nseg, u64 max_seg,
+                        cudaStream_t s);
+void iota_u32(u32* p, u64 n, cudaStream_t s);
+
+// ---- aggregate.cu -----------------------------------------------------------
+struct AggArgs {
+  DGraph g;
+  const u32* C = nullptr;        // contiguous ids < count
+  u32 count = 0;
+  const u64* coff = nullptr;     // community -> member offsets
+  const u32* members = nullptr;
+  const u64* boff = nullptr;     // scanned total member degrees (work per community)
+  const u64* hoff = nullptr;     // holey row offsets (scanned min(budget, count))
+  u32* htgt = nullptr;           // holey targets / weights
+  float* hw = nullptr;
+  u32* fill = nullptr;           // entries written per row
+  u32* err = nullptr;
+  double* table = nullptr;       // global-table scratch
+  u64 table_slots = 0;
+};
+void aggregate_rows(const AggArgs& a, const Bins& bins, cudaStream_t s);
+// capped[c] = min(budget[c], count): holey row capacity
+void cap_budgets(const u64* budget, u64* capped, u32 count, cudaStream_t s);
+size_t aggregate_table_bytes(u64 max_slots, int* blocks);
+// out rows = holey rows compacted (noff = scan of fill), total weight (fp64) into *tw
+void compact_rows(const u64* hoff, const u32* htgt, const float* hw, const u32* fill,
+                  const u64* noff, u32 count, u32* otgt, float* ow, double* tw,
+                  cudaStream_t s);
+
+// ---- modularity.cu ----------------------------------------------------------
+// sums: [0] internal arc weight, [1] sum_c Sigma_c^2 ; tot (width entries) zeroed here
+void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width,
+                      double* sums, cudaStream_t s, double two_m);
+
+// ---- generate.cu: device-built synthetic inputs --------------------------------
+struct OwnedCsr {
+  u32 n = 0;
+  u64 arcs = 0;
+  DBuf<u64> off;
+  DBuf<u32> tgt;
+  DBuf<float> w;
+  double total_weight = 0.0;
+  DGraph view() const { return DGraph{n, arcs, off.p, tgt.p, w.p}; }
+};
+struct GenSpec {
+  int kind = 0;
+  u64 n = 0, edges = 0;
+  u32 scale = 0, blocks = 0;
+  double a = 0.57, b = 0.19, c = 0.19, mu = 0.1, p = 0.6, avg_degree = 16.0;
+  u64 seed = 1;
+};
+void generate(const GenSpec& g, OwnedCsr& out, cudaStream_t s);
+// sorted arc keys (source<<32 | target, ~0 = dropped) -> deduplicated unit-weight CSR
+void keys_to_csr(DBuf<ull>& keys, u64 nkeys, u64 n, OwnedCsr& out, cudaStream_t s);
+
+}  // namespace lvn

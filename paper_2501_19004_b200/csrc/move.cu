@@ -1,0 +1,392 @@
+// Local-moving phase: one sweep of compact_move (louvain_compact.cpp:116-212)
+// over the active vertices, degree-binned:
+//
+//   bin 1  deg <= thread_max (<= 8)   thread per vertex, candidates in registers
+//   bin 2  deg <= group_max  (<= 32)  8-lane group per vertex, 64-slot smem table
+//   bin 3  deg <= warp_max   (<= 256) warp per vertex, 512-slot smem table
+//   bin 4  deg <= block_max  (<= 4096) block per vertex, <= 8192-slot smem table
+//   bin 5  larger                      block per vertex, table in global memory
+//
+// Per vertex u (scan_serial + decide_serial, louvain_compact.cpp:37-68):
+// K_{u->c} is accumulated over the non-self arcs into an open-addressing table
+// keyed by community (the weight to u's own community is kept privately per
+// lane, which removes the one heavily contended key); every live entry c !=
+// C[u] is scored with Eq. 2 in fp64 (delta_q, bit-for-bit the reference
+// formula) and the best one (ties to the lowest id) is taken if its gain is
+// positive and Pick-Less allows it (louvain_compact.cpp:151-152). A move
+// updates Sigma with fp64 L2 reductions and marks every arc target of u for
+// the next iteration (louvain_compact.cpp:154-161). Stale reads of C and
+// Sigma are benign, exactly as in the reference (louvain_mc.hpp:80-86).
+//
+// Table values: value_bits 32 -> fp32 accumulated in a packed 64-bit slot
+// (key<<32 | float) updated by one CAS; value_bits 64 -> u32 key + fp64 value.
+// (Shared-memory float/double atomicAdd are CAS loops on sm_100a anyway.)
+//
+// Algorithmic bytes: 12 B per scanned arc + 32 B per processed
+// vertex; the kernels count both on the device.
+#include <cooperative_groups.h>
+#include <cooperative_groups/reduce.h>
+
+#include <cmath>
+
+#include "kernels.cuh"
+#include "tables.cuh"
+
+namespace cg = cooperative_groups;
+
+namespace lvn {
+namespace {
+
+constexpr int kThreadMaxD = 8;
+constexpr int kGroupCapLog = 6;    // 64 slots  (group_max <= 32)
+constexpr int kWarpCapLog = 9;     // 512 slots (warp_max <= 256)
+constexpr int kBlockCapLog = 13;   // 8192 slots (block_max <= 4096)
+constexpr int kBlockThreads = 512;
+
+// ---- per-thread accounting, flushed once per thread at kernel exit ----------
+struct Tally {
+  double gain = 0.0;
+  ull verts = 0, arcs = 0, moves = 0;
+  __device__ void flush(const MoveArgs& x) {
+    const double g = warp_sum(gain);
+    const ull v = warp_sum(verts), a = warp_sum(arcs), m = warp_sum(moves);
+    if ((threadIdx.x & 31) == 0) {
+      if (g != 0.0) atomicAdd(x.gain_acc, g);
+      if (v) atomicAdd(&x.counters[0], v);
+      if (a) atomicAdd(&x.counters[1], a);
+      if (m) atomicAdd(&x.counters[2], m);
+    }
+  }
+};
+
+// Move decision shared by every kernel; called by exactly one thread per vertex.
+template <bool DRY>
+__device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, double ku, u32 bc,
+                                       double bg, Tally& t) {
+  bool mv = bc != kEmpty && bg > 0.0;  // bc != from by construction
+  if (DRY) {
+    x.out_to[u] = mv ? bc : from;
+    x.out_gain[u] = mv ? bg : 0.0;
+    return false;
+  }
+  if (mv && x.pickless && bc > from) mv = false;
+  if (mv) {
+    atomicAdd(&x.sigma[from], -ku);
+    atomicAdd(&x.sigma[bc], ku);
+    x.C[u] = bc;
+    t.gain += bg;
+    ++t.moves;
+  }
+  return mv;
+}
+
+// ---- bin 1: thread per vertex --------------------------------------------------
+template <class V, bool DRY>
+__global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restrict__ list,
+                                                 u64 count) {
+  Tally tl;
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < count;
+       i += u64(gridDim.x) * blockDim.x) {
+    const u32 u = list[i];
+    if (!DRY) {
+      if (x.prune && !x.flags[u]) continue;
+      x.flags[u] = 0;
+    }
+    const u64 lo = x.g.off[u];
+    const int d = int(x.g.off[u + 1] - lo);
+    const u32 from = x.C[u];
+    u32 t[kThreadMaxD], c[kThreadMaxD];
+    V wv[kThreadMaxD];
+#pragma unroll
+    for (int k = 0; k < kThreadMaxD; ++k) {
+      t[k] = kEmpty;
+      c[k] = kEmpty;
+      wv[k] = V(0);
+      if (k < d) {
+        t[k] = x.g.tgt[lo + k];
+        wv[k] = V(x.g.w[lo + k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < kThreadMaxD; ++k)
+      if (k < d && t[k] != u) c[k] = x.C[t[k]];
+    V own = V(0);
+#pragma unroll
+    for (int k = 0; k < kThreadMaxD; ++k)
+      if (c[k] == from) own += wv[k];
+    const double ku = x.K[u], sf = x.sigma[from];
+    double bg = -INFINITY;
+    u32 bc = kEmpty;
+#pragma unroll
+    for (int k = 0; k < kThreadMaxD; ++k) {
+      const u32 ck = c[k];
+      bool first = ck != kEmpty && ck != from;
+#pragma unroll
+      for (int j = 0; j < k; ++j) first = first && c[j] != ck;
+      if (first) {
+        V sum = V(0);  // row order, like the reference's serial scan
+#pragma unroll
+        for (int j = k; j < kThreadMaxD; ++j)
+          if (c[j] == ck) sum += wv[j];
+        const double g = delta_q(double(sum), double(own), ku, x.sigma[ck], sf, x.m);
+        if (better(g, ck, bg, bc)) bg = g, bc = ck;
+      }
+    }
+    ++tl.verts;
+    tl.arcs += d;
+    if (decide<DRY>(x, u, from, ku, bc, bg, tl) && x.prune) {
+#pragma unroll
+      for (int k = 0; k < kThreadMaxD; ++k)
+        if (k < d) x.flags[t[k]] = 1;
+    }
+  }
+  tl.flush(x);
+}
+
+// ---- bins 2 and 3: G lanes per vertex, smem table per group ---------------------
+template <class Tab, int G, int CAPLOG, int THREADS, bool DRY>
+__global__ void __launch_bounds__(THREADS) lm_group(MoveArgs x, const u32* __restrict__ list,
+                                                    u64 count) {
+  using V = typename Tab::V;
+  constexpr int GPB = THREADS / G;
+  constexpr u32 CAP = 1u << CAPLOG;
+  constexpr u32 MINLOG = G == 8 ? 3 : 5;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const auto tile = cg::tiled_partition<G>(cg::this_thread_block());
+  const int gi = threadIdx.x / G;
+  const u32 lane = tile.thread_rank();
+  const Tab tab(smem + size_t(gi) * CAP * Tab::kSlotBytes, CAP);
+  Tally tl;
+  for (u64 i = blockIdx.x * u64(GPB) + gi; i < count; i += u64(gridDim.x) * GPB) {
+    const u32 u = list[i];
+    if (!DRY) {
+      u32 act = 0;
+      if (lane == 0) {
+        act = !x.prune || x.flags[u];
+        if (act) x.flags[u] = 0;
+      }
+      if (!tile.shfl(act, 0)) continue;
+    }
+    const u64 lo = x.g.off[u];
+    const u64 d = x.g.off[u + 1] - lo;
+    const u32 from = x.C[u];
+    const u32 lg = table_log(d, MINLOG);
+    const u32 S = 1u << lg;
+    for (u32 s = lane; s < S; s += G) tab.clear(s);
+    tile.sync();
+    V own = V(0);
+    for (u64 a = lo + lane; a < lo + d; a += G) {
+      const u32 t = x.g.tgt[a];
+      if (t == u) continue;
+      const V w = V(x.g.w[a]);
+      const u32 c = x.C[t];
+      if (c == from)
+        own += w;
+      else
+        tab.insert(lg, c, w);
+    }
+    own = cg::reduce(tile, own, cg::plus<V>());
+    tile.sync();
+    const double ku = x.K[u], sf = x.sigma[from];
+    double bg = -INFINITY;
+    u32 bc = kEmpty;
+    for (u32 s = lane; s < S; s += G) {
+      u32 key;
+      double val;
+      if (tab.read(s, key, val)) {
+        const double g = delta_q(val, double(own), ku, x.sigma[key], sf, x.m);
+        if (better(g, key, bg, bc)) bg = g, bc = key;
+      }
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const double og = tile.shfl_xor(bg, o);
+      const u32 oc = tile.shfl_xor(bc, o);
+      if (better(og, oc, bg, bc)) bg = og, bc = oc;
+    }
+    u32 moved = 0;
+    if (lane == 0) {
+      ++tl.verts;
+      tl.arcs += d;
+      moved = decide<DRY>(x, u, from, ku, bc, bg, tl);
+    }
+    if (!DRY && tile.shfl(moved, 0) && x.prune)
+      for (u64 a = lo + lane; a < lo + d; a += G) x.flags[x.g.tgt[a]] = 1;
+    tile.sync();
+  }
+  tl.flush(x);
+}
+
+// ---- bins 4 and 5: block per vertex, table in smem (4) or global memory (5) -----
+template <class Tab, bool GLOBAL, bool DRY>
+__global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32* __restrict__ list,
+                                                          u64 count) {
+  using V = typename Tab::V;
+  constexpr int W = kBlockThreads / 32;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ V red_v[W];
+  __shared__ double red_g[W];
+  __shared__ u32 red_c[W];
+  __shared__ u32 bcast;
+  const Tab tab = GLOBAL ? Tab(x.table + blockIdx.x * x.table_slots * Tab::kSlotBytes / 8,
+                               x.table_slots)
+                         : Tab(smem, u64(1) << kBlockCapLog);
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Tally tl;
+  for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
+    const u32 u = list[i];
+    if (!DRY) {
+      if (threadIdx.x == 0) {
+        const u32 act = !x.prune || x.flags[u];
+        if (act) x.flags[u] = 0;
+        bcast = act;
+      }
+      __syncthreads();
+      const u32 act = bcast;
+      __syncthreads();
+      if (!act) continue;
+    }
+    const u64 lo = x.g.off[u];
+    const u64 d = x.g.off[u + 1] - lo;
+    const u32 from = x.C[u];
+    const u32 lg = table_log(d, 5);
+    const u32 S = 1u << lg;
+    for (u32 s = threadIdx.x; s < S; s += kBlockThreads) tab.clear(s);
+    __syncthreads();
+    V own = V(0);
+    for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) {
+      const u32 t = x.g.tgt[a];
+      if (t == u) continue;
+      const V w = V(x.g.w[a]);
+      const u32 c = x.C[t];
+      if (c == from)
+        own += w;
+      else
+        tab.insert(lg, c, w);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
+    if (lane == 0) red_v[wid] = own;
+    if (GLOBAL) __threadfence();
+    __syncthreads();
+    V own_all = V(0);
+#pragma unroll
+    for (int k = 0; k < W; ++k) own_all += red_v[k];
+    const double ku = x.K[u], sf = x.sigma[from];
+    double bg = -INFINITY;
+    u32 bc = kEmpty;
+    for (u32 s = threadIdx.x; s < S; s += kBlockThreads) {
+      u32 key;
+      double val;
+      if (tab.read(s, key, val)) {
+        const double g = delta_q(val, double(own_all), ku, x.sigma[key], sf, x.m);
+        if (better(g, key, bg, bc)) bg = g, bc = key;
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+      const u32 oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      if (better(og, oc, bg, bc)) bg = og, bc = oc;
+    }
+    if (lane == 0) red_g[wid] = bg, red_c[wid] = bc;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int k = 1; k < W; ++k)
+        if (better(red_g[k], red_c[k], bg, bc)) bg = red_g[k], bc = red_c[k];
+      ++tl.verts;
+      tl.arcs += d;
+      bcast = decide<DRY>(x, u, from, ku, bc, bg, tl);
+    }
+    __syncthreads();
+    if (!DRY && bcast && x.prune)
+      for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) x.flags[x.g.tgt[a]] = 1;
+    __syncthreads();
+  }
+  tl.flush(x);
+}
+
+// ---- launch plumbing ----------------------------------------------------------
+template <class K>
+int occupancy(K kernel, int threads, size_t smem) {
+  int b = 0;
+  LVN_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&b, kernel, threads, smem));
+  return b > 0 ? b : 1;
+}
+
+template <class K>
+void set_smem(K kernel, size_t smem) {
+  if (smem > 48 * 1024)
+    LVN_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+}
+
+template <class Tab, bool DRY>
+void sweep(const MoveArgs& a, const Bins& b, cudaStream_t s) {
+  using V = typename Tab::V;
+  const int sms = sm_count();
+  if (b.count(1)) {
+    auto k = lm_thread<V, DRY>;
+    static const int occ = occupancy(k, 256, 0);
+    const u64 blocks = std::min<u64>((b.count(1) + 255) / 256, u64(sms) * occ);
+    k<<<unsigned(blocks), 256, 0, s>>>(a, b.of(1), b.count(1));
+    LVN_LAUNCH();
+  }
+  if (b.count(2)) {
+    constexpr int T = 256;
+    auto k = lm_group<Tab, 8, kGroupCapLog, T, DRY>;
+    const size_t smem = size_t(T / 8) * (1u << kGroupCapLog) * Tab::kSlotBytes;
+    static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
+    const u64 blocks = std::min<u64>((b.count(2) + T / 8 - 1) / (T / 8), u64(sms) * occ);
+    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(2), b.count(2));
+    LVN_LAUNCH();
+  }
+  if (b.count(3)) {
+    constexpr int T = 256;
+    auto k = lm_group<Tab, 32, kWarpCapLog, T, DRY>;
+    const size_t smem = size_t(T / 32) * (1u << kWarpCapLog) * Tab::kSlotBytes;
+    static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
+    const u64 blocks = std::min<u64>((b.count(3) + T / 32 - 1) / (T / 32), u64(sms) * occ);
+    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(3), b.count(3));
+    LVN_LAUNCH();
+  }
+  if (b.count(4)) {
+    auto k = lm_block<Tab, false, DRY>;
+    const size_t smem = (size_t(1) << kBlockCapLog) * Tab::kSlotBytes;
+    static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
+    const u64 blocks = std::min<u64>(b.count(4), u64(sms) * occ);
+    k<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(4), b.count(4));
+    LVN_LAUNCH();
+  }
+  if (b.count(5)) {
+    if (!a.table || !a.table_slots) fail(kInternal, "global move table not provisioned");
+    auto k = lm_block<Tab, true, DRY>;
+    int blocks = 0;
+    move_table_bytes(b.max_degree, sizeof(V) == 4 ? 32 : 64, &blocks);
+    blocks = int(std::min<u64>(b.count(5), u64(blocks)));
+    k<<<unsigned(blocks), kBlockThreads, 0, s>>>(a, b.of(5), b.count(5));
+    LVN_LAUNCH();
+  }
+}
+
+}  // namespace
+
+size_t move_table_bytes(u64 max_degree, int value_bits, int* blocks) {
+  const u64 slots = u64(1) << ceil_log2_u64(2 * (max_degree ? max_degree : 1));
+  if (blocks) *blocks = sm_count();
+  const size_t per = slots * (value_bits == 64 ? SplitF64::kSlotBytes : PackedF32::kSlotBytes);
+  return per * size_t(sm_count());
+}
+
+void move_sweep(const MoveArgs& a, const Bins& b, int value_bits, cudaStream_t s) {
+  if (b.edges.thread_max > kThreadMaxD || b.edges.group_max > (1u << (kGroupCapLog - 1)) ||
+      b.edges.warp_max > (1u << (kWarpCapLog - 1)) ||
+      b.edges.block_max > (1u << (kBlockCapLog - 1)))
+    fail(kInvalid, "degree bin edges exceed the device table capacities");
+  if (value_bits == 64) {
+    a.dry ? sweep<SplitF64, true>(a, b, s) : sweep<SplitF64, false>(a, b, s);
+  } else {
+    a.dry ? sweep<PackedF32, true>(a, b, s) : sweep<PackedF32, false>(a, b, s);
+  }
+}
+
+}  // namespace lvn

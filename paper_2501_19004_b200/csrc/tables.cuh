@@ -1,0 +1,82 @@
+// Open-addressing community tables over shared or global memory (the device
+// counterpart of the reference's slab tables, compact_hashtable.hpp:28-122):
+// power-of-two capacity, multiplicative hash, linear probing, empty key
+// 0xFFFFFFFF. Capacity is always >= 2x the distinct keys that can arrive,
+// so probing terminates.
+#pragma once
+
+#include "common.cuh"
+
+namespace lvn {
+
+__device__ __forceinline__ u32 table_log(u64 deg, u32 min_log) {
+  const u32 l = ceil_log2_u64(2 * deg);
+  return l > min_log ? l : min_log;
+}
+
+// ---- table flavours ---------------------------------------------------------
+struct PackedF32 {  // value_bits == 32
+  using V = float;
+  static constexpr size_t kSlotBytes = 8;
+  ull* s;
+  __device__ PackedF32(void* base, u64 slots) : s(static_cast<ull*>(base)) { (void)slots; }
+  __device__ __forceinline__ void clear(u32 i) const { s[i] = kEmptySlot64; }
+  __device__ __forceinline__ void insert(u32 log_size, u32 key, float w) const {
+    const u32 mask = (1u << log_size) - 1u;
+    u32 h = slot_hash(key, log_size);
+    while (true) {
+      const ull cur = reinterpret_cast<volatile ull*>(s)[h];
+      const u32 k = u32(cur >> 32);
+      if (k == key || k == kEmpty) {
+        const float nv = __uint_as_float(u32(cur)) + w;
+        const ull want = (ull(key) << 32) | __float_as_uint(nv);
+        if (atomicCAS(&s[h], cur, want) == cur) return;
+      } else {
+        h = (h + 1) & mask;
+      }
+    }
+  }
+  __device__ __forceinline__ bool read(u32 i, u32& key, double& val) const {
+    const ull x = s[i];
+    key = u32(x >> 32);
+    val = double(__uint_as_float(u32(x)));
+    return key != kEmpty;
+  }
+};
+
+struct SplitF64 {  // value_bits == 64
+  using V = double;
+  static constexpr size_t kSlotBytes = 12;
+  u32* k;
+  double* v;
+  __device__ SplitF64(void* base, u64 slots)
+      : k(reinterpret_cast<u32*>(static_cast<double*>(base) + slots)),
+        v(static_cast<double*>(base)) {}
+  __device__ __forceinline__ void clear(u32 i) const {
+    k[i] = kEmpty;
+    v[i] = 0.0;
+  }
+  __device__ __forceinline__ void insert(u32 log_size, u32 key, double w) const {
+    const u32 mask = (1u << log_size) - 1u;
+    u32 h = slot_hash(key, log_size);
+    while (true) {
+      u32 cur = reinterpret_cast<volatile u32*>(k)[h];
+      if (cur == kEmpty) {
+        cur = atomicCAS(&k[h], kEmpty, key);
+        if (cur == kEmpty) cur = key;
+      }
+      if (cur == key) {
+        atomicAdd(&v[h], w);
+        return;
+      }
+      h = (h + 1) & mask;
+    }
+  }
+  __device__ __forceinline__ bool read(u32 i, u32& key, double& val) const {
+    key = k[i];
+    val = v[i];
+    return key != kEmpty;
+  }
+};
+
+}  // namespace lvn

@@ -1,0 +1,323 @@
+"""Parity of the CUDA path (through the C-ABI) against the oracle on the same
+inputs. Bars (BASELINE.json north_star): renumbering, community CSR and
+canonical aggregation bit-exact (integer weights); modularity within 1e-9
+relative; per-vertex decisions bit-exact on a fixed snapshot (integer weights
+make fp32/fp64 accumulation exact); end-to-end modularity within 0.005 of the
+reference's."""
+
+import numpy as np
+import pytest
+
+import golden_data as G
+from graphs import (BARBELL, LOW_SHRINK, SINGLE_EDGE, SWAP_GADGET, TRIANGLE, TWO_TRIANGLES, canonical_rows,
+                    from_triples, planted, random_graph, random_membership, rmat)
+
+pytestmark = pytest.mark.gpu
+
+MOD_RTOL = 1e-9
+Q_TOL = 0.005
+
+
+@pytest.fixture(scope="module")
+def lvn():
+    import torch
+
+    if not torch.cuda.is_available():
+        pytest.skip("needs a B200")
+    import paper_2501_19004_b200 as m
+
+    return m
+
+
+def G_(g, lvn):
+    return lvn.CsrGraph(g.offsets, g.targets, g.weights, g.total_weight)
+
+
+def assert_q(a, b):
+    assert abs(a - b) <= MOD_RTOL * max(1.0, abs(b)), (a, b)
+
+
+def star(n_leaves):
+    """hub 0 joined to every leaf: a row longer than every smem table"""
+    src = np.zeros(n_leaves, np.uint32)
+    dst = np.arange(1, n_leaves + 1, dtype=np.uint32)
+    from oracle import port
+
+    return port.build_csr(n_leaves + 1, src, dst, np.ones(n_leaves))
+
+
+# ---------------------------------------------------------------- modularity
+def test_modularity_anchors(lvn):
+    assert abs(lvn.modularity(G_(from_triples((3, [(0, 1, 1.0), (1, 2, 2.0), (2, 2, 4.0)])), lvn), [0, 0, 0])) <= 1e-12
+    assert_q(lvn.modularity(G_(from_triples(TRIANGLE), lvn), [0, 1, 2]), -1 / 3)
+    assert_q(lvn.modularity(G_(from_triples(BARBELL), lvn), [0, 0, 0, 1, 1, 1]), 5 / 14)
+    assert_q(lvn.modularity(G_(from_triples(SINGLE_EDGE), lvn), [0, 1]), -0.5)
+    with pytest.raises(lvn.DegenerateGraphError):
+        lvn.modularity(G_(from_triples((2, [])), lvn), [0, 1])
+
+
+@pytest.mark.parametrize("t", range(12))
+def test_modularity_golden(lvn, t):
+    p = f"rnd{t}_"
+    g = G.graph(p)
+    assert_q(lvn.modularity(G_(g, lvn), G.field(p, "membership")), float(G.field(p, "modularity")))
+    assert np.allclose(lvn.vertex_weights(G_(g, lvn)), G.field(p, "vertex_weights"), rtol=1e-12, atol=0)
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_modularity_random_labels(lvn, port, seed):
+    g = random_graph(3000, 20000, seed, 0.25, 7.5, True, False)
+    memb = np.random.default_rng(seed).integers(0, 1 + 97 * seed, g.n).astype(np.uint32) * 7 + 1000
+    assert_q(lvn.modularity(G_(g, lvn), memb), port.modularity(g, memb))
+
+
+def test_modularity_hub_rows(lvn, port):
+    g = star(20000)
+    memb = random_membership(g.n, 50, 3)
+    assert_q(lvn.modularity(G_(g, lvn), memb), port.modularity(g, memb))
+
+
+def test_modularity_rmat16(lvn, port):
+    g = rmat(16, 16, 1)
+    memb = random_membership(g.n, 1000, 1)
+    assert_q(lvn.modularity(G_(g, lvn), memb), port.modularity(g, memb))
+
+
+# ------------------------------------------------------- renumber / lookup / CSR
+def test_renumber_lookup_golden(lvn):
+    m = np.array([5, 5, 2, 9], np.uint32)
+    assert lvn.renumber_communities(m) == 3 and list(m) == [1, 1, 0, 2]
+    m = np.array([0, 1, 1, 2], np.uint32)
+    lvn.lookup_dendrogram(m, [2, 0, 1])
+    assert list(m) == [2, 0, 0, 1]
+    with pytest.raises(lvn.InternalError):
+        lvn.lookup_dendrogram(np.array([0, 5], np.uint32), [2, 0, 1])
+    assert lvn.count_communities([5, 5, 2, 9]) == 3
+    assert lvn.count_communities(np.array([], np.uint32)) == 0
+
+
+@pytest.mark.parametrize("n,k", [(1, 1), (1000, 7), (100000, 5000), (2_000_000, 300_000)])
+def test_renumber_bit_exact(lvn, port, n, k):
+    rng = np.random.default_rng(n)
+    m = (rng.integers(0, k, n) * 3 + 11).astype(np.uint32)
+    want, wc = port.renumber(m)
+    got = m.copy()
+    assert lvn.renumber_communities(got) == wc
+    assert (got == want).all()
+    assert lvn.count_communities(m) == port.count_communities(m)
+    level = rng.permutation(wc).astype(np.uint32)
+    a = want.copy()
+    lvn.lookup_dendrogram(a, level)
+    assert (a == port.lookup(want, level)).all()
+
+
+@pytest.mark.parametrize("n,k", [(10, 3), (50000, 40), (300000, 30000), (20000, 1)])
+def test_community_csr_bit_exact(lvn, port, n, k):
+    m = random_membership(n, k, n + k)
+    count = port.count_communities(m)
+    off, mem = lvn.build_community_csr(m, count)
+    woff, wmem = port.community_csr(m, count)
+    assert (off == woff).all() and (mem == wmem).all()
+
+
+# ---------------------------------------------------------------- aggregation
+def agg_equal(a, want):
+    assert (a.offsets == want.offsets).all()
+    ra, ta, wa = canonical_rows(a)
+    rb, tb, wb = canonical_rows(want)
+    assert (ta == tb).all() and (wa == wb).all()
+    assert (a.targets == ta).all(), "rows must come out canonically sorted"
+    assert a.total_weight == want.total_weight
+
+
+def test_aggregate_barbell_golden(lvn):
+    a = lvn.compact_aggregate(G_(from_triples(BARBELL), lvn), [0, 0, 0, 1, 1, 1])
+    assert list(a.offsets) == [0, 2, 4] and list(a.targets) == [0, 1, 0, 1]
+    assert list(a.weights) == [6.0, 1.0, 1.0, 6.0] and a.total_weight == 7.0
+    with pytest.raises(ValueError):
+        lvn.compact_aggregate(G_(from_triples(TRIANGLE), lvn), [0, 2, 2])
+
+
+@pytest.mark.parametrize("t", range(12))
+def test_aggregate_golden(lvn, t):
+    p = f"rnd{t}_"
+    a = lvn.compact_aggregate(G_(G.graph(p), lvn), G.field(p, "membership"))
+    assert (a.offsets == G.field(p, "agg_offsets")).all()
+    assert (a.targets == G.field(p, "agg_targets")).all()
+    assert (a.weights == G.field(p, "agg_weights")).all()
+    assert a.total_weight == float(G.field(p, "agg_total_weight"))
+
+
+@pytest.mark.parametrize("n,edges,k", [(2000, 8000, 3), (5000, 40000, 50), (20000, 100000, 2000),
+                                       (100000, 400000, 30000), (4000, 200000, 9)])
+def test_aggregate_bit_exact_random(lvn, port, n, edges, k):
+    g = random_graph(n, edges, n + k)
+    m = random_membership(n, k, k)
+    agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
+
+
+def test_aggregate_global_table_path(lvn, port):
+    g = star(12000)  # community of the hub has 12000 distinct neighbours > smem table
+    m = np.arange(g.n, dtype=np.uint32)
+    agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
+    m2 = random_membership(g.n, 9000, 5)
+    agg_equal(lvn.compact_aggregate(G_(g, lvn), m2), port.aggregate(g, m2))
+
+
+def test_aggregate_planted(lvn, port):
+    g = planted(50000, 100, 32, 0.1, 9)
+    m = (np.arange(g.n) // 500).astype(np.uint32)
+    agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
+
+
+# ------------------------------------------------------------ move decisions
+def decisions_equal(lvn, port, g, memb, force=-1, value_bits=64):
+    kw = port.vertex_weights(g)
+    cw = np.zeros(g.n)
+    np.add.at(cw, memb, kw)
+    opts = lvn.CompactOptions(value_bits=value_bits)
+    to, gain = lvn.evaluate_moves(G_(g, lvn), memb, kw, cw, g.total_weight, opts, force)
+    for u in range(g.n):
+        want = port.evaluate_move(g, memb, kw, cw, g.total_weight, u, 64)
+        assert (int(to[u]), float(gain[u])) == want, (u, g.offsets[u + 1] - g.offsets[u])
+
+
+@pytest.mark.parametrize("t", range(12))
+def test_decisions_golden(lvn, t):
+    p = f"rnd{t}_"
+    g = G.graph(p)
+    memb = G.field(p, "membership")
+    kw = G.field(p, "vertex_weights")
+    cw = np.zeros(g.n)
+    np.add.at(cw, memb, kw)
+    to, gain = lvn.evaluate_moves(G_(g, lvn), memb, kw, cw, g.total_weight)
+    assert (to == G.field(p, "move_to")).all() and (gain == G.field(p, "move_gain")).all()
+
+
+@pytest.mark.parametrize("force", [-1, 1, 2, 3, 4])
+@pytest.mark.parametrize("value_bits", [32, 64])
+def test_decisions_every_kernel_class(lvn, port, force, value_bits):
+    # integer weights keep fp32 and fp64 accumulation exact, so every kernel
+    # class must decide bit-identically (test_compact.cpp:114-144)
+    g = random_graph(600, 6000, 11 + force, 1.0, 6.0, True, True)
+    memb = random_membership(g.n, 40, 3)
+    decisions_equal(lvn, port, g, memb, force, value_bits)
+
+
+def test_decisions_hub(lvn, port):
+    g = star(9000)
+    memb = random_membership(g.n, 700, 8)
+    decisions_equal(lvn, port, g, memb)
+
+
+# ------------------------------------------------------------ engine end to end
+def test_engine_fixture_optima(lvn):
+    r = lvn.louvain_compact(G_(from_triples(TWO_TRIANGLES), lvn))
+    assert abs(r.modularity - 0.5) <= 1e-9 and r.num_communities == 2
+    r = lvn.louvain_compact(G_(from_triples(BARBELL), lvn))
+    assert abs(r.modularity - 5 / 14) <= 1e-9 and r.num_communities == 2
+    r = lvn.louvain_compact(G_(from_triples(SINGLE_EDGE), lvn))
+    assert r.num_communities == 1 and abs(r.modularity) <= 1e-12
+    r = lvn.louvain_compact(G_(from_triples(TRIANGLE), lvn))
+    assert r.num_communities == 1
+
+
+def test_engine_params_and_errors(lvn):
+    g = G_(from_triples(BARBELL), lvn)
+    r = lvn.louvain_compact(g, lvn.LouvainParams(max_passes=0))
+    assert r.passes == 0 and r.num_communities == 6 and list(r.membership) == list(range(6))
+    r = lvn.louvain_compact(g, lvn.LouvainParams(max_iterations=0))
+    assert r.passes == 1 and r.num_communities == 6
+    for bad in (lvn.LouvainParams(max_passes=-1), lvn.LouvainParams(tolerance_drop=0.0),
+                lvn.LouvainParams(aggregation_tolerance=0.0), lvn.LouvainParams(chunk_size=0)):
+        with pytest.raises(ValueError):
+            lvn.louvain_compact(g, bad)
+    with pytest.raises(ValueError):
+        lvn.louvain_compact(g, None, lvn.CompactOptions(pick_less=lvn.PickLessSchedule(3)))
+    with pytest.raises(ValueError):
+        lvn.louvain_compact(g, None, lvn.CompactOptions(value_bits=16))
+    with pytest.raises(lvn.DegenerateGraphError):
+        lvn.louvain_compact(G_(from_triples((3, [])), lvn))
+
+
+def test_engine_low_shrink(lvn):
+    r = lvn.louvain_compact(G_(from_triples(LOW_SHRINK), lvn))
+    assert r.aggregations == 0 and r.passes == 1 and r.num_communities == 9
+    assert r.membership[8] == r.membership[9]
+
+
+def test_engine_swap_gadget(lvn, port):
+    g = from_triples(SWAP_GADGET)
+    r = lvn.louvain_compact(G_(g, lvn))
+    assert r.membership[3] == r.membership[5]
+    assert_q(r.modularity, port.modularity(g, r.membership))
+
+
+def test_engine_tolerance_schedule_and_bookkeeping(lvn, port):
+    g = planted(3000, 30, 24, 0.05, 77)
+    r = lvn.louvain_compact(G_(g, lvn))
+    assert r.passes >= 2 and r.aggregations <= r.passes
+    for p, t in enumerate(r.tolerance_per_pass):
+        assert t == pytest.approx(0.01 / 10**p, rel=1e-12)
+    assert len(r.pass_seconds) == r.passes and len(r.iterations_per_pass) == r.passes
+    assert r.phase.total() == pytest.approx(r.wall_seconds, rel=1e-9)
+    m = r.membership.copy()
+    assert port.count_communities(m) == r.num_communities == int(m.max()) + 1
+    assert_q(r.modularity, port.modularity(g, r.membership))
+
+
+@pytest.mark.parametrize("t", range(4))
+def test_engine_quality_vs_reference_planted(lvn, t):
+    p = f"pp{t}_"
+    g = G.graph(p)
+    r = lvn.louvain_compact(G_(g, lvn))
+    assert r.modularity >= float(G.field(p, "seq_modularity")) - Q_TOL
+    assert r.modularity >= float(G.field(p, "mc_modularity")) - Q_TOL
+
+
+@pytest.mark.parametrize("value_bits", [32, 64])
+def test_engine_quality_rmat16_c1(lvn, port, value_bits):
+    # config C1: RMAT scale 16, edge factor 16, dedupe, default parameters
+    g = rmat(16, 16, 1)
+    want = port.sequential_louvain(g).modularity
+    r = lvn.louvain_compact(G_(g, lvn), None, lvn.CompactOptions(value_bits=value_bits))
+    assert_q(r.modularity, port.modularity(g, r.membership))
+    assert r.modularity >= want - Q_TOL, (r.modularity, want)
+
+
+def test_engine_quality_planted_large(lvn, port):
+    g = planted(200000, 200, 32, 0.1, 5)
+    truth = (np.arange(g.n) // (g.n // 200)).astype(np.uint32)
+    r = lvn.louvain_compact(G_(g, lvn))
+    assert_q(r.modularity, port.modularity(g, r.membership))
+    assert r.modularity >= port.modularity(g, truth) - Q_TOL
+
+
+def test_engine_device_resident_input(lvn, port):
+    g = rmat(14, 16, 2)
+    dg = lvn.DeviceGraph.upload(G_(g, lvn))
+    r = lvn.louvain_compact(dg)
+    assert_q(r.modularity, port.modularity(g, r.membership))
+    r2 = lvn.louvain_compact(dg, membership_on_device=True)
+    assert r2.membership_device_ptr and r2.num_communities > 0
+
+
+# ----------------------------------------------------------------- generators
+@pytest.mark.parametrize("kind,kw", [("rmat", dict(scale=12, edgefactor=16)),
+                                     ("sbm", dict(n=20000, blocks=20, avg_degree=16, mu=0.1)),
+                                     ("grid", dict(side=60, p=0.6)),
+                                     ("uniform", dict(n=5000, edges=20000)),
+                                     ("web", dict(n=20000, avg_degree=20))])
+def test_generators_produce_valid_csr(lvn, kind, kw):
+    dg = lvn.generate(kind, seed=3, **kw)
+    g = dg.download()
+    n = g.num_vertices()
+    rows = np.repeat(np.arange(n), np.diff(g.offsets.astype(np.int64)))
+    assert (np.diff(g.offsets.astype(np.int64)) >= 0).all()
+    assert (g.targets < n).all() and (g.weights == 1.0).all()
+    assert not (rows == g.targets).any(), "self-loops"
+    key = rows.astype(np.uint64) << np.uint64(32) | g.targets.astype(np.uint64)
+    assert (np.diff(key.astype(np.int64)) > 0).all(), "rows sorted and deduplicated"
+    rev = g.targets.astype(np.uint64) << np.uint64(32) | rows.astype(np.uint64)
+    assert np.array_equal(np.sort(rev), key), "symmetric"
+    assert g.total_weight == g.num_arcs() / 2
