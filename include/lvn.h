@@ -95,7 +95,11 @@ typedef struct lvn_params {
   uint32_t bin_warp_max;        /* 256 */
   uint32_t bin_block_max;       /* 4096 */
   int membership_on_device;     /* result membership stays in device memory */
-  int reserved[7];
+  /* at most this many vertices of a degree bin are decided by one launch of a
+   * sweep (launches run in vertex order, later ones see earlier moves);
+   * 0 = automatic (scaled to the graph), UINT32_MAX = one launch per bin */
+  uint32_t sweep_chunk;
+  int reserved[6];
 } lvn_params;
 
 /* Per-kernel-family device accounting (CUDA events on the engine stream). */

@@ -61,7 +61,8 @@ class lvn_params(C.Structure):
         ("bin_warp_max", C.c_uint32),
         ("bin_block_max", C.c_uint32),
         ("membership_on_device", C.c_int),
-        ("reserved", C.c_int * 7),
+        ("sweep_chunk", C.c_uint32),
+        ("reserved", C.c_int * 6),
     ]
 
 

@@ -157,6 +157,14 @@ void validate(const lvn_params& p) {
 // pick_less_active (louvain_compact.hpp:22-24)
 bool pick_less_active(int iteration, int period) { return (iteration + period / 2) % period == 0; }
 
+// vertices of one degree bin decided per launch (lvn_params.sweep_chunk)
+u64 sweep_chunk(const lvn_params& p, u32 nv) {
+  if (p.sweep_chunk == 0xFFFFFFFFu) return ~u64(0);
+  if (p.sweep_chunk) return p.sweep_chunk;
+  (void)nv;
+  return ~u64(0);  // automatic policy: set from the quality/throughput study
+}
+
 // A graph resident on the device: borrowed device pointers or an uploaded copy.
 struct InGraph {
   DGraph g;
@@ -424,6 +432,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
     a.gain_acc = &rec.p->gain;
     a.counters = &rec.p->verts;
     a.err = err.p;
+    a.chunk = sweep_chunk(p, nv);
     if (B.count(5)) {
       int blocks = 0;
       const size_t bytes = move_table_bytes(B.max_degree, p.value_bits, &blocks);
@@ -614,6 +623,7 @@ void lvn_params_default(lvn_params* p) {
   p->bin_warp_max = 256;
   p->bin_block_max = 4096;
   p->membership_on_device = 0;
+  p->sweep_chunk = 0;
 }
 
 int lvn_init(int num_gpus, const int* devices) {

@@ -53,6 +53,7 @@ struct MoveArgs {
   u32* err = nullptr;
   double* table = nullptr;     // global-table scratch for bin 5 (see move_table_bytes)
   u64 table_slots = 0;         // slots per block
+  u64 chunk = ~u64(0);         // max vertices of one bin decided per launch
 };
 // one sweep over bins 1..5 (thread, group8, warp, block, global); the
 // force_kernel >= 0 variant routes every vertex to at least that class.

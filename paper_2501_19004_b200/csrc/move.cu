@@ -320,6 +320,22 @@ void set_smem(K kernel, size_t smem) {
     LVN_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
 }
 
+// Launch `kernel` over list[0, count) in chunks of at most a.chunk vertices;
+// chunks run in vertex order on the stream, so a later chunk sees the moves
+// of the earlier ones (bounded concurrency keeps small graphs from taking
+// fully synchronous, oscillation-prone sweeps).
+template <class K>
+void launch_chunks(K kernel, const MoveArgs& a, const u32* list, u64 count, int threads, u64 per_block,
+                   u64 max_blocks, size_t smem, cudaStream_t s) {
+  const u64 chunk = a.chunk ? a.chunk : count;
+  for (u64 off = 0; off < count; off += chunk) {
+    const u64 c = std::min<u64>(chunk, count - off);
+    const u64 blocks = std::max<u64>(1, std::min<u64>((c + per_block - 1) / per_block, max_blocks));
+    kernel<<<unsigned(blocks), threads, smem, s>>>(a, list + off, c);
+    LVN_LAUNCH();
+  }
+}
+
 template <class Tab, bool DRY>
 void sweep(const MoveArgs& a, const Bins& b, cudaStream_t s) {
   using V = typename Tab::V;
@@ -327,44 +343,33 @@ void sweep(const MoveArgs& a, const Bins& b, cudaStream_t s) {
   if (b.count(1)) {
     auto k = lm_thread<V, DRY>;
     static const int occ = occupancy(k, 256, 0);
-    const u64 blocks = std::min<u64>((b.count(1) + 255) / 256, u64(sms) * occ);
-    k<<<unsigned(blocks), 256, 0, s>>>(a, b.of(1), b.count(1));
-    LVN_LAUNCH();
+    launch_chunks(k, a, b.of(1), b.count(1), 256, 256, u64(sms) * occ, 0, s);
   }
   if (b.count(2)) {
     constexpr int T = 256;
     auto k = lm_group<Tab, 8, kGroupCapLog, T, DRY>;
     const size_t smem = size_t(T / 8) * (1u << kGroupCapLog) * Tab::kSlotBytes;
     static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
-    const u64 blocks = std::min<u64>((b.count(2) + T / 8 - 1) / (T / 8), u64(sms) * occ);
-    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(2), b.count(2));
-    LVN_LAUNCH();
+    launch_chunks(k, a, b.of(2), b.count(2), T, T / 8, u64(sms) * occ, smem, s);
   }
   if (b.count(3)) {
     constexpr int T = 256;
     auto k = lm_group<Tab, 32, kWarpCapLog, T, DRY>;
     const size_t smem = size_t(T / 32) * (1u << kWarpCapLog) * Tab::kSlotBytes;
     static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
-    const u64 blocks = std::min<u64>((b.count(3) + T / 32 - 1) / (T / 32), u64(sms) * occ);
-    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(3), b.count(3));
-    LVN_LAUNCH();
+    launch_chunks(k, a, b.of(3), b.count(3), T, T / 32, u64(sms) * occ, smem, s);
   }
   if (b.count(4)) {
     auto k = lm_block<Tab, false, DRY>;
     const size_t smem = (size_t(1) << kBlockCapLog) * Tab::kSlotBytes;
     static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
-    const u64 blocks = std::min<u64>(b.count(4), u64(sms) * occ);
-    k<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(4), b.count(4));
-    LVN_LAUNCH();
+    launch_chunks(k, a, b.of(4), b.count(4), kBlockThreads, 1, u64(sms) * occ, smem, s);
   }
   if (b.count(5)) {
     if (!a.table || !a.table_slots) fail(kInternal, "global move table not provisioned");
-    auto k = lm_block<Tab, true, DRY>;
     int blocks = 0;
     move_table_bytes(b.max_degree, sizeof(V) == 4 ? 32 : 64, &blocks);
-    blocks = int(std::min<u64>(b.count(5), u64(blocks)));
-    k<<<unsigned(blocks), kBlockThreads, 0, s>>>(a, b.of(5), b.count(5));
-    LVN_LAUNCH();
+    launch_chunks(lm_block<Tab, true, DRY>, a, b.of(5), b.count(5), kBlockThreads, 1, u64(blocks), 0, s);
   }
 }
 

@@ -123,6 +123,7 @@ class CompactOptions:  # louvain_compact.hpp:35-40
     probing: Probing = Probing.quadratic_double
     value_bits: int = 32
     bins: DeviceBins = field(default_factory=DeviceBins)
+    sweep_chunk: int = 0  # vertices per launch of a sweep; 0 automatic, 2**32-1 unbounded
 
 
 @dataclass
@@ -302,6 +303,7 @@ def _params(params: LouvainParams | None, options: CompactOptions | None, on_dev
     p.bin_warp_max = options.bins.warp_max
     p.bin_block_max = options.bins.block_max
     p.membership_on_device = int(on_device)
+    p.sweep_chunk = options.sweep_chunk
     return p
 
 
