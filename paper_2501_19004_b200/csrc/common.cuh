@@ -42,12 +42,11 @@ inline void cuda_check(cudaError_t e, const char* expr, const char* file, int li
 }
 extern std::atomic<unsigned long long> g_launches;  // kernels launched by this library
 
+// LVN_SYNC_DEBUG=1: synchronise after every launch and name the launch site
+void launch_check(const char* file, int line);
+
 #define LVN_CUDA(x) ::lvn::cuda_check((x), #x, __FILE__, __LINE__)
-#define LVN_LAUNCH()                                                         \
-  do {                                                                       \
-    ::lvn::g_launches.fetch_add(1, std::memory_order_relaxed);               \
-    ::lvn::cuda_check(cudaGetLastError(), "kernel launch", __FILE__, __LINE__); \
-  } while (0)
+#define LVN_LAUNCH() ::lvn::launch_check(__FILE__, __LINE__)
 
 // device error word bits (checked by the host once per pass)
 enum DevErr : u32 { kErrTable = 1u, kErrLookup = 2u, kErrRange = 4u };

@@ -17,6 +17,16 @@ namespace lvn {
 
 std::atomic<unsigned long long> g_launches{0};
 
+void launch_check(const char* file, int line) {
+  static const bool debug = [] {
+    const char* e = std::getenv("LVN_SYNC_DEBUG");
+    return e && *e && *e != '0';
+  }();
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  cuda_check(cudaGetLastError(), "kernel launch", file, line);
+  if (debug) cuda_check(cudaDeviceSynchronize(), "kernel execution (LVN_SYNC_DEBUG)", file, line);
+}
+
 // ---------------------------------------------------------------------------
 // Pool / context
 // ---------------------------------------------------------------------------
@@ -296,6 +306,8 @@ u32 renumber_device(u32* C, u64 n, u64 width, DBuf<u32>& used, DBuf<u32>& rank, 
   return count;
 }
 
+bool check_mode();
+
 // ---- aggregation of a graph by a contiguous membership ----------------------
 void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
                       u32* err, cudaStream_t s, bool canonical) {
@@ -315,6 +327,8 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   const u64 H = read_scalar(hoff.p + count, s);
   DBuf<u32> htgt(H ? H : 1), fill(count ? count : 1);
   DBuf<float> hw(H ? H : 1);
+  // communities whose members have no arcs (bin 0) emit nothing and are never visited
+  LVN_CUDA(cudaMemsetAsync(fill.p, 0, size_t(count ? count : 1) * sizeof(u32), s));
   AggArgs a;
   a.g = g;
   a.C = C;
@@ -338,6 +352,38 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
     a.table_slots = slots;
   }
   aggregate_rows(a, ab, s);
+  if (check_mode()) {
+    std::vector<u64> h_coff(count + 1), h_boff(count + 1), h_hoff(count + 1), h_off(u64(g.n) + 1);
+    std::vector<u32> h_mem(g.n), h_fill(count), h_C(g.n);
+    LVN_CUDA(cudaMemcpyAsync(h_coff.data(), coff.p, (count + 1) * 8, cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(h_boff.data(), boff.p, (count + 1) * 8, cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(h_hoff.data(), hoff.p, (count + 1) * 8, cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(h_off.data(), g.off, (u64(g.n) + 1) * 8, cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(h_mem.data(), members.p, u64(g.n) * 4, cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(h_fill.data(), fill.p, u64(count) * 4, cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(h_C.data(), C, u64(g.n) * 4, cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    std::vector<u8> seen(g.n, 0);
+    for (u32 c = 0; c < count; ++c) {
+      u64 deg = 0;
+      for (u64 k = h_coff[c]; k < h_coff[c + 1]; ++k) {
+        const u32 v = h_mem[k];
+        if (v >= g.n || seen[v] || h_C[v] != c)
+          fail(kInternal, "LVN_CHECK: community CSR broken at community " + std::to_string(c));
+        seen[v] = 1;
+        deg += h_off[v + 1] - h_off[v];
+      }
+      if (deg != h_boff[c + 1] - h_boff[c])
+        fail(kInternal, "LVN_CHECK: budget of community " + std::to_string(c) + " is " +
+                            std::to_string(h_boff[c + 1] - h_boff[c]) + ", member degrees sum to " +
+                            std::to_string(deg));
+      if (h_fill[c] > h_hoff[c + 1] - h_hoff[c])
+        fail(kInternal, "LVN_CHECK: row " + std::to_string(c) + " emitted " + std::to_string(h_fill[c]) +
+                            " entries into capacity " + std::to_string(h_hoff[c + 1] - h_hoff[c]) +
+                            " (budget " + std::to_string(deg) + ", members " +
+                            std::to_string(h_coff[c + 1] - h_coff[c]) + ")");
+    }
+  }
   DBuf<u64> noff(count + 1);
   exclusive_scan_u32_to_u64(fill.p, noff.p, count, s);
   const u64 A = read_scalar(noff.p + count, s);
@@ -367,10 +413,53 @@ double modularity_device(const DGraph& g, const Bins& b, const u32* C, u64 width
   return h[0] / (2.0 * m) - h[1];
 }
 
+// LVN_CHECK=1: validate device state between phases (debugging aid; copies
+// state to the host, so it is never enabled in measured runs)
+bool check_mode() {
+  static const bool on = [] {
+    const char* e = std::getenv("LVN_CHECK");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
+void check_membership(const char* what, const u32* C, u64 n, u64 bound, cudaStream_t s) {
+  if (!check_mode()) return;
+  std::vector<u32> h(n);
+  if (n) LVN_CUDA(cudaMemcpyAsync(h.data(), C, n * 4, cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  for (u64 i = 0; i < n; ++i)
+    if (h[i] >= bound)
+      fail(kInternal, std::string("LVN_CHECK ") + what + ": id " + std::to_string(h[i]) + " at " +
+                          std::to_string(i) + " >= " + std::to_string(bound));
+}
+
+void check_graph(const char* what, const DGraph& g, cudaStream_t s) {
+  if (!check_mode()) return;
+  std::vector<u64> off(u64(g.n) + 1);
+  std::vector<u32> tgt(g.arcs);
+  std::vector<float> w(g.arcs);
+  LVN_CUDA(cudaMemcpyAsync(off.data(), g.off, off.size() * 8, cudaMemcpyDeviceToHost, s));
+  if (g.arcs) {
+    LVN_CUDA(cudaMemcpyAsync(tgt.data(), g.tgt, g.arcs * 4, cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(w.data(), g.w, g.arcs * 4, cudaMemcpyDeviceToHost, s));
+  }
+  LVN_CUDA(cudaStreamSynchronize(s));
+  auto bad = [&](const std::string& m) { fail(kInternal, std::string("LVN_CHECK ") + what + ": " + m); };
+  if (off[0] != 0 || off[g.n] != g.arcs) bad("offsets do not span the arcs");
+  for (u64 v = 0; v < g.n; ++v)
+    if (off[v + 1] < off[v]) bad("offsets decrease at row " + std::to_string(v));
+  for (u64 a = 0; a < g.arcs; ++a) {
+    if (tgt[a] >= g.n) bad("target " + std::to_string(tgt[a]) + " out of range at arc " + std::to_string(a));
+    if (!(w[a] >= 0.0f)) bad("bad weight at arc " + std::to_string(a));
+  }
+}
+
 void check_err(const u32* err, cudaStream_t s) {
   const u32 e = read_scalar(err, s);
   if (e & kErrLookup) fail(kInternal, "dendrogram lookup index out of range");
-  if (e & kErrTable) fail(kInternal, "aggregation table exhausted; capacity invariant violated");
+  if (e & kErrTable) fail(kInternal, "scan table exhausted; capacity invariant violated");
+  if (e & kErrRange) fail(kInternal, "community id out of range in a local-moving table");
   if (e) fail(kInternal, "device invariant violated");
 }
 
@@ -456,6 +545,8 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
       if (h->gain <= tolerance) break;  // louvain_compact.cpp:209
     }
     t_move += since(t0);
+    check_err(err.p, s);
+    check_membership("after local moving", C.p, nv, nv, s);
     ++passes;
     its.push_back(iterations);
     tols.push_back(tolerance);
@@ -491,6 +582,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
            nv, cur.arcs);
     t_aggregate += since(t1);
     cur = next.view();
+    check_graph("aggregated graph", cur, s);
     ++aggregations;
     tolerance /= p.tolerance_drop;
     pass_secs.push_back(since(t_pass));

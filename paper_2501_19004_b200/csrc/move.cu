@@ -59,10 +59,31 @@ struct Tally {
   }
 };
 
+// community ids read back from a table must be vertex ids of this graph
+__device__ __forceinline__ bool key_ok(const MoveArgs& x, u32 key) {
+  if (key < x.g.n) return true;
+  atomicOr(x.err, u32(kErrRange));
+  return false;
+}
+
 // Move decision shared by every kernel; called by exactly one thread per vertex.
+// bk = K_{u->bc}, own = K_{u->from}.
+//
+// Applying a move validates it against the true Sigma at the instant it
+// lands: the join is one fp64 atomicAdd that returns Sigma_bc as it stood
+// (all earlier joiners included), the gain is re-scored with that value and
+// the current Sigma_from, and the join is undone if it is no longer positive.
+// This is the reference's asynchronous semantics (every decision sees the
+// moves applied before it, louvain_mc.hpp:80-86) kept under massive
+// concurrency, where thousands of deciders would otherwise read the same
+// stale Sigma and herd into one community.
 template <bool DRY>
 __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, double ku, u32 bc,
-                                       double bg, Tally& t) {
+                                       double bg, double bk, double own, Tally& t) {
+  if (from >= x.g.n) {
+    atomicOr(x.err, u32(kErrRange));
+    return false;
+  }
   bool mv = bc != kEmpty && bg > 0.0;  // bc != from by construction
   if (DRY) {
     x.out_to[u] = mv ? bc : from;
@@ -71,11 +92,18 @@ __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, doubl
   }
   if (mv && x.pickless && bc > from) mv = false;
   if (mv) {
-    atomicAdd(&x.sigma[from], -ku);
-    atomicAdd(&x.sigma[bc], ku);
-    x.C[u] = bc;
-    t.gain += bg;
-    ++t.moves;
+    const double sigma_c = atomicAdd(&x.sigma[bc], ku);
+    const double sigma_d = *reinterpret_cast<volatile double*>(&x.sigma[from]);
+    const double g = delta_q(bk, own, ku, sigma_c, sigma_d, x.m);
+    if (g > 0.0) {
+      atomicAdd(&x.sigma[from], -ku);
+      x.C[u] = bc;
+      t.gain += g;
+      ++t.moves;
+    } else {
+      atomicAdd(&x.sigma[bc], -ku);
+      mv = false;
+    }
   }
   return mv;
 }
@@ -115,12 +143,12 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
     for (int k = 0; k < kThreadMaxD; ++k)
       if (c[k] == from) own += wv[k];
     const double ku = x.K[u], sf = x.sigma[from];
-    double bg = -INFINITY;
+    double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
 #pragma unroll
     for (int k = 0; k < kThreadMaxD; ++k) {
       const u32 ck = c[k];
-      bool first = ck != kEmpty && ck != from;
+      bool first = ck != kEmpty && ck != from && key_ok(x, ck);
 #pragma unroll
       for (int j = 0; j < k; ++j) first = first && c[j] != ck;
       if (first) {
@@ -129,12 +157,12 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
         for (int j = k; j < kThreadMaxD; ++j)
           if (c[j] == ck) sum += wv[j];
         const double g = delta_q(double(sum), double(own), ku, x.sigma[ck], sf, x.m);
-        if (better(g, ck, bg, bc)) bg = g, bc = ck;
+        if (better(g, ck, bg, bc)) bg = g, bc = ck, bk = double(sum);
       }
     }
     ++tl.verts;
     tl.arcs += d;
-    if (decide<DRY>(x, u, from, ku, bc, bg, tl) && x.prune) {
+    if (decide<DRY>(x, u, from, ku, bc, bg, bk, double(own), tl) && x.prune) {
 #pragma unroll
       for (int k = 0; k < kThreadMaxD; ++k)
         if (k < d) x.flags[t[k]] = 1;
@@ -172,6 +200,10 @@ __global__ void __launch_bounds__(THREADS) lm_group(MoveArgs x, const u32* __res
     const u32 from = x.C[u];
     const u32 lg = table_log(d, MINLOG);
     const u32 S = 1u << lg;
+    if (S > CAP) {  // bin / table-capacity invariant
+      if (lane == 0) atomicOr(x.err, u32(kErrTable));
+      continue;
+    }
     for (u32 s = lane; s < S; s += G) tab.clear(s);
     tile.sync();
     V own = V(0);
@@ -188,27 +220,28 @@ __global__ void __launch_bounds__(THREADS) lm_group(MoveArgs x, const u32* __res
     own = cg::reduce(tile, own, cg::plus<V>());
     tile.sync();
     const double ku = x.K[u], sf = x.sigma[from];
-    double bg = -INFINITY;
+    double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
     for (u32 s = lane; s < S; s += G) {
       u32 key;
       double val;
-      if (tab.read(s, key, val)) {
+      if (tab.read(s, key, val) && key_ok(x, key)) {
         const double g = delta_q(val, double(own), ku, x.sigma[key], sf, x.m);
-        if (better(g, key, bg, bc)) bg = g, bc = key;
+        if (better(g, key, bg, bc)) bg = g, bc = key, bk = val;
       }
     }
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) {
       const double og = tile.shfl_xor(bg, o);
       const u32 oc = tile.shfl_xor(bc, o);
-      if (better(og, oc, bg, bc)) bg = og, bc = oc;
+      const double ok = tile.shfl_xor(bk, o);
+      if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
     }
     u32 moved = 0;
     if (lane == 0) {
       ++tl.verts;
       tl.arcs += d;
-      moved = decide<DRY>(x, u, from, ku, bc, bg, tl);
+      moved = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own), tl);
     }
     if (!DRY && tile.shfl(moved, 0) && x.prune)
       for (u64 a = lo + lane; a < lo + d; a += G) x.flags[x.g.tgt[a]] = 1;
@@ -225,7 +258,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
   constexpr int W = kBlockThreads / 32;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ V red_v[W];
-  __shared__ double red_g[W];
+  __shared__ double red_g[W], red_k[W];
   __shared__ u32 red_c[W];
   __shared__ u32 bcast;
   const Tab tab = GLOBAL ? Tab(x.table + blockIdx.x * x.table_slots * Tab::kSlotBytes / 8,
@@ -251,6 +284,10 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
     const u32 from = x.C[u];
     const u32 lg = table_log(d, 5);
     const u32 S = 1u << lg;
+    if (GLOBAL ? u64(S) > x.table_slots : S > (1u << kBlockCapLog)) {  // capacity invariant
+      if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
+      continue;
+    }
     for (u32 s = threadIdx.x; s < S; s += kBlockThreads) tab.clear(s);
     __syncthreads();
     V own = V(0);
@@ -273,30 +310,31 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
 #pragma unroll
     for (int k = 0; k < W; ++k) own_all += red_v[k];
     const double ku = x.K[u], sf = x.sigma[from];
-    double bg = -INFINITY;
+    double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
     for (u32 s = threadIdx.x; s < S; s += kBlockThreads) {
       u32 key;
       double val;
-      if (tab.read(s, key, val)) {
+      if (tab.read(s, key, val) && key_ok(x, key)) {
         const double g = delta_q(val, double(own_all), ku, x.sigma[key], sf, x.m);
-        if (better(g, key, bg, bc)) bg = g, bc = key;
+        if (better(g, key, bg, bc)) bg = g, bc = key, bk = val;
       }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double og = __shfl_xor_sync(0xffffffffu, bg, o);
       const u32 oc = __shfl_xor_sync(0xffffffffu, bc, o);
-      if (better(og, oc, bg, bc)) bg = og, bc = oc;
+      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
     }
-    if (lane == 0) red_g[wid] = bg, red_c[wid] = bc;
+    if (lane == 0) red_g[wid] = bg, red_c[wid] = bc, red_k[wid] = bk;
     __syncthreads();
     if (threadIdx.x == 0) {
       for (int k = 1; k < W; ++k)
-        if (better(red_g[k], red_c[k], bg, bc)) bg = red_g[k], bc = red_c[k];
+        if (better(red_g[k], red_c[k], bg, bc)) bg = red_g[k], bc = red_c[k], bk = red_k[k];
       ++tl.verts;
       tl.arcs += d;
-      bcast = decide<DRY>(x, u, from, ku, bc, bg, tl);
+      bcast = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own_all), tl);
     }
     __syncthreads();
     if (!DRY && bcast && x.prune)
