@@ -1,0 +1,12 @@
+"""Profiling driver (run under ncu on the GPU box): one warm-up and N runs of a config."""
+import sys
+sys.path.insert(0, '.')
+import paper_2501_19004_b200 as lvn
+from bench import CONFIGS
+cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
+runs = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+c = CONFIGS[cfg]
+dg = lvn.generate(c["kind"], **{k: v for k, v in c.items() if k not in ("kind", "desc")})
+for i in range(runs):
+    r = lvn.louvain_compact(dg, membership_on_device=True)
+    print(cfg, r.modularity, r.passes, r.iterations_per_pass, {k: round(s.seconds * 1e3, 2) for k, s in r.stats.items()}, flush=True)
