@@ -526,8 +526,9 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
       int blocks = 0;
       const size_t bytes = move_table_bytes(B.max_degree, p.value_bits, &blocks);
       table.ensure(bytes / sizeof(double) + 1);
+      move_table_init(table.p, B.max_degree, p.value_bits, s);
       a.table = table.p;
-      a.table_slots = u64(1) << ceil_log2_u64(2 * B.max_degree);
+      a.table_slots = move_table_slots(B.max_degree);
     }
     const auto t0 = Clock::now();
     int iterations = 0;
@@ -1014,8 +1015,9 @@ int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const doubl
       int blocks = 0;
       const size_t bytes = move_table_bytes(b.max_degree, pp.value_bits, &blocks);
       table.alloc(bytes / sizeof(double) + 1);
+      move_table_init(table.p, b.max_degree, pp.value_bits, s);
       a.table = table.p;
-      a.table_slots = u64(1) << ceil_log2_u64(2 * b.max_degree);
+      a.table_slots = move_table_slots(b.max_degree);
     }
     move_sweep(a, b, pp.value_bits, s);
     if (n) {

@@ -54,11 +54,15 @@ struct MoveArgs {
   double* table = nullptr;     // global-table scratch for bin 5 (see move_table_bytes)
   u64 table_slots = 0;         // slots per block
   u64 chunk = ~u64(0);         // max vertices of one bin decided per launch
+  double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
 };
 // one sweep over bins 1..5 (thread, group8, warp, block, global); the
 // force_kernel >= 0 variant routes every vertex to at least that class.
 void move_sweep(const MoveArgs& a, const Bins& bins, int value_bits, cudaStream_t s);
 size_t move_table_bytes(u64 max_degree, int value_bits, int* blocks);
+u64 move_table_slots(u64 max_degree);
+// mark every slot of the bin-5 tables empty (done whenever they are allocated)
+void move_table_init(void* table, u64 max_degree, int value_bits, cudaStream_t s);
 
 // ---- community.cu -----------------------------------------------------------
 // used[c] = 1 for every c in C (used zeroed here), sized n

@@ -10,13 +10,20 @@
 // Per vertex u (scan_serial + decide_serial, louvain_compact.cpp:37-68):
 // K_{u->c} is accumulated over the non-self arcs into an open-addressing table
 // keyed by community (the weight to u's own community is kept privately per
-// lane, which removes the one heavily contended key); every live entry c !=
-// C[u] is scored with Eq. 2 in fp64 (delta_q, bit-for-bit the reference
-// formula) and the best one (ties to the lowest id) is taken if its gain is
-// positive and Pick-Less allows it (louvain_compact.cpp:151-152). A move
-// updates Sigma with fp64 L2 reductions and marks every arc target of u for
-// the next iteration (louvain_compact.cpp:154-161). Stale reads of C and
-// Sigma are benign, exactly as in the reference (louvain_mc.hpp:80-86).
+// lane, which removes the one heavily contended key). Every slot a vertex
+// claims is appended to a per-group live list, so ranking scans only live
+// entries and the table is restored to empty by clearing just those slots.
+// Each live entry c != C[u] is ranked by Eq. 2; ties go to the lowest id.
+// The move is applied if its gain is positive and Pick-Less allows it
+// (louvain_compact.cpp:151-152); applying it validates the gain against the
+// Sigma values current at that instant (see decide()), updates Sigma with fp64
+// L2 atomics and marks every arc target of u (louvain_compact.cpp:154-161).
+//
+// Ranking: the dry-run evaluation (lvn_evaluate_moves, the parity path) scores
+// every candidate with the reference formula operation for operation
+// (delta_q); the engine ranks with the same formula using precomputed 1/m and
+// 1/(2m^2) (differences only at the last ulp) and decides with the exact
+// formula.
 //
 // Table values: value_bits 32 -> fp32 accumulated in a packed 64-bit slot
 // (key<<32 | float) updated by one CAS; value_bits 64 -> u32 key + fp64 value.
@@ -66,17 +73,25 @@ __device__ __forceinline__ bool key_ok(const MoveArgs& x, u32 key) {
   return false;
 }
 
+// Eq. 2 for ranking: exact (reference operation order) or with reciprocals
+template <bool EXACT>
+__device__ __forceinline__ double score(const MoveArgs& x, double k_to_c, double own, double ku,
+                                        double sigma_c, double sigma_d) {
+  if (EXACT) return delta_q(k_to_c, own, ku, sigma_c, sigma_d, x.m);
+  return (k_to_c - own) * x.inv_m - ku * (ku + sigma_c - sigma_d) * x.inv_2m2;
+}
+
 // Move decision shared by every kernel; called by exactly one thread per vertex.
 // bk = K_{u->bc}, own = K_{u->from}.
 //
 // Applying a move validates it against the true Sigma at the instant it
 // lands: the join is one fp64 atomicAdd that returns Sigma_bc as it stood
-// (all earlier joiners included), the gain is re-scored with that value and
-// the current Sigma_from, and the join is undone if it is no longer positive.
-// This is the reference's asynchronous semantics (every decision sees the
-// moves applied before it, louvain_mc.hpp:80-86) kept under massive
-// concurrency, where thousands of deciders would otherwise read the same
-// stale Sigma and herd into one community.
+// (all earlier joiners included), the gain is re-scored exactly with that
+// value and the current Sigma_from, and the join is undone if it is no
+// longer positive. This is the reference's asynchronous semantics (every
+// decision sees the moves applied before it, louvain_mc.hpp:80-86) kept under
+// massive concurrency, where thousands of deciders would otherwise read the
+// same stale Sigma and herd into one community.
 template <bool DRY>
 __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, double ku, u32 bc,
                                        double bg, double bk, double own, Tally& t) {
@@ -156,7 +171,7 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
 #pragma unroll
         for (int j = k; j < kThreadMaxD; ++j)
           if (c[j] == ck) sum += wv[j];
-        const double g = delta_q(double(sum), double(own), ku, x.sigma[ck], sf, x.m);
+        const double g = score<DRY>(x, double(sum), double(own), ku, x.sigma[ck], sf);
         if (better(g, ck, bg, bc)) bg = g, bc = ck, bk = double(sum);
       }
     }
@@ -171,19 +186,30 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
   tl.flush(x);
 }
 
-// ---- bins 2 and 3: G lanes per vertex, smem table per group ---------------------
+// ---- bins 2 and 3: G lanes per vertex, smem table + live list per group ---------
+template <class Tab, int G, int CAPLOG, int THREADS>
+constexpr size_t group_smem() {
+  return size_t(THREADS / G) * ((size_t(1) << CAPLOG) * Tab::kSlotBytes + (size_t(1) << (CAPLOG - 1)) * 4 + 16);
+}
+
 template <class Tab, int G, int CAPLOG, int THREADS, bool DRY>
-__global__ void __launch_bounds__(THREADS) lm_group(MoveArgs x, const u32* __restrict__ list,
-                                                    u64 count) {
+__global__ void __launch_bounds__(THREADS, 4) lm_group(MoveArgs x, const u32* __restrict__ list,
+                                                       u64 count) {
   using V = typename Tab::V;
   constexpr int GPB = THREADS / G;
   constexpr u32 CAP = 1u << CAPLOG;
+  constexpr u32 LCAP = CAP / 2;
   constexpr u32 MINLOG = G == 8 ? 3 : 5;
   extern __shared__ __align__(16) unsigned char smem[];
   const auto tile = cg::tiled_partition<G>(cg::this_thread_block());
   const int gi = threadIdx.x / G;
   const u32 lane = tile.thread_rank();
   const Tab tab(smem + size_t(gi) * CAP * Tab::kSlotBytes, CAP);
+  u32* live = reinterpret_cast<u32*>(smem + size_t(GPB) * CAP * Tab::kSlotBytes) + size_t(gi) * LCAP;
+  u32* nlive = reinterpret_cast<u32*>(smem + size_t(GPB) * (CAP * Tab::kSlotBytes + LCAP * 4)) + gi;
+  for (u32 s = lane; s < CAP; s += G) tab.clear(s);
+  if (lane == 0) *nlive = 0;
+  tile.sync();
   Tally tl;
   for (u64 i = blockIdx.x * u64(GPB) + gi; i < count; i += u64(gridDim.x) * GPB) {
     const u32 u = list[i];
@@ -199,34 +225,34 @@ __global__ void __launch_bounds__(THREADS) lm_group(MoveArgs x, const u32* __res
     const u64 d = x.g.off[u + 1] - lo;
     const u32 from = x.C[u];
     const u32 lg = table_log(d, MINLOG);
-    const u32 S = 1u << lg;
-    if (S > CAP) {  // bin / table-capacity invariant
+    if ((1u << lg) > CAP) {  // bin / table-capacity invariant
       if (lane == 0) atomicOr(x.err, u32(kErrTable));
       continue;
     }
-    for (u32 s = lane; s < S; s += G) tab.clear(s);
-    tile.sync();
     V own = V(0);
     for (u64 a = lo + lane; a < lo + d; a += G) {
       const u32 t = x.g.tgt[a];
       if (t == u) continue;
       const V w = V(x.g.w[a]);
       const u32 c = x.C[t];
-      if (c == from)
+      if (c == from) {
         own += w;
-      else
-        tab.insert(lg, c, w);
+      } else {
+        const int slot = tab.insert(lg, c, w);
+        if (slot >= 0) live[atomicAdd(nlive, 1u)] = u32(slot);
+      }
     }
     own = cg::reduce(tile, own, cg::plus<V>());
     tile.sync();
+    const u32 n = *reinterpret_cast<volatile u32*>(nlive);
     const double ku = x.K[u], sf = x.sigma[from];
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
-    for (u32 s = lane; s < S; s += G) {
+    for (u32 j = lane; j < n; j += G) {
       u32 key;
       double val;
-      if (tab.read(s, key, val) && key_ok(x, key)) {
-        const double g = delta_q(val, double(own), ku, x.sigma[key], sf, x.m);
+      if (tab.read(live[j], key, val) && key_ok(x, key)) {
+        const double g = score<DRY>(x, val, double(own), ku, x.sigma[key], sf);
         if (better(g, key, bg, bc)) bg = g, bc = key, bk = val;
       }
     }
@@ -237,8 +263,10 @@ __global__ void __launch_bounds__(THREADS) lm_group(MoveArgs x, const u32* __res
       const double ok = tile.shfl_xor(bk, o);
       if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
     }
+    for (u32 j = lane; j < n; j += G) tab.clear(live[j]);
     u32 moved = 0;
     if (lane == 0) {
+      *nlive = 0;
       ++tl.verts;
       tl.arcs += d;
       moved = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own), tl);
@@ -251,6 +279,11 @@ __global__ void __launch_bounds__(THREADS) lm_group(MoveArgs x, const u32* __res
 }
 
 // ---- bins 4 and 5: block per vertex, table in smem (4) or global memory (5) -----
+template <class Tab>
+constexpr size_t block_smem() {
+  return (size_t(1) << kBlockCapLog) * Tab::kSlotBytes + (size_t(1) << (kBlockCapLog - 1)) * 4;
+}
+
 template <class Tab, bool GLOBAL, bool DRY>
 __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32* __restrict__ list,
                                                           u64 count) {
@@ -260,11 +293,18 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
   __shared__ V red_v[W];
   __shared__ double red_g[W], red_k[W];
   __shared__ u32 red_c[W];
-  __shared__ u32 bcast;
-  const Tab tab = GLOBAL ? Tab(x.table + blockIdx.x * x.table_slots * Tab::kSlotBytes / 8,
-                               x.table_slots)
-                         : Tab(smem, u64(1) << kBlockCapLog);
+  __shared__ u32 bcast, nlive;
+  // global tables: per-block region of table_slots slots followed by table_slots/2 live entries
+  const size_t gstride = x.table_slots * Tab::kSlotBytes + x.table_slots / 2 * 4;
+  unsigned char* gbase = reinterpret_cast<unsigned char*>(x.table) + blockIdx.x * gstride;
+  const Tab tab = GLOBAL ? Tab(gbase, x.table_slots) : Tab(smem, u64(1) << kBlockCapLog);
+  u32* live = GLOBAL ? reinterpret_cast<u32*>(gbase + x.table_slots * Tab::kSlotBytes)
+                     : reinterpret_cast<u32*>(smem + (size_t(1) << kBlockCapLog) * Tab::kSlotBytes);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  if (!GLOBAL)  // smem starts dirty; the global table is kept empty between vertices and launches
+    for (u32 s = threadIdx.x; s < (1u << kBlockCapLog); s += kBlockThreads) tab.clear(s);
+  if (threadIdx.x == 0) nlive = 0;
+  __syncthreads();
   Tally tl;
   for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
     const u32 u = list[i];
@@ -283,40 +323,39 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
     const u64 d = x.g.off[u + 1] - lo;
     const u32 from = x.C[u];
     const u32 lg = table_log(d, 5);
-    const u32 S = 1u << lg;
-    if (GLOBAL ? u64(S) > x.table_slots : S > (1u << kBlockCapLog)) {  // capacity invariant
+    if (GLOBAL ? (u64(1) << lg) > x.table_slots : lg > u32(kBlockCapLog)) {  // capacity invariant
       if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
       continue;
     }
-    for (u32 s = threadIdx.x; s < S; s += kBlockThreads) tab.clear(s);
-    __syncthreads();
     V own = V(0);
     for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) {
       const u32 t = x.g.tgt[a];
       if (t == u) continue;
       const V w = V(x.g.w[a]);
       const u32 c = x.C[t];
-      if (c == from)
+      if (c == from) {
         own += w;
-      else
-        tab.insert(lg, c, w);
+      } else {
+        const int slot = tab.insert(lg, c, w);
+        if (slot >= 0) live[atomicAdd(&nlive, 1u)] = u32(slot);
+      }
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
     if (lane == 0) red_v[wid] = own;
-    if (GLOBAL) __threadfence();
     __syncthreads();
     V own_all = V(0);
 #pragma unroll
     for (int k = 0; k < W; ++k) own_all += red_v[k];
+    const u32 n = nlive;
     const double ku = x.K[u], sf = x.sigma[from];
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
-    for (u32 s = threadIdx.x; s < S; s += kBlockThreads) {
+    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) {
       u32 key;
       double val;
-      if (tab.read(s, key, val) && key_ok(x, key)) {
-        const double g = delta_q(val, double(own_all), ku, x.sigma[key], sf, x.m);
+      if (tab.read(live[j], key, val) && key_ok(x, key)) {
+        const double g = score<DRY>(x, val, double(own_all), ku, x.sigma[key], sf);
         if (better(g, key, bg, bc)) bg = g, bc = key, bk = val;
       }
     }
@@ -329,9 +368,11 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
     }
     if (lane == 0) red_g[wid] = bg, red_c[wid] = bc, red_k[wid] = bk;
     __syncthreads();
+    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) tab.clear(live[j]);
     if (threadIdx.x == 0) {
       for (int k = 1; k < W; ++k)
         if (better(red_g[k], red_c[k], bg, bc)) bg = red_g[k], bc = red_c[k], bk = red_k[k];
+      nlive = 0;
       ++tl.verts;
       tl.arcs += d;
       bcast = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own_all), tl);
@@ -342,6 +383,11 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
     __syncthreads();
   }
   tl.flush(x);
+}
+
+__global__ void fill_u64(ull* p, u64 n, ull v) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+    p[i] = v;
 }
 
 // ---- launch plumbing ----------------------------------------------------------
@@ -360,8 +406,7 @@ void set_smem(K kernel, size_t smem) {
 
 // Launch `kernel` over list[0, count) in chunks of at most a.chunk vertices;
 // chunks run in vertex order on the stream, so a later chunk sees the moves
-// of the earlier ones (bounded concurrency keeps small graphs from taking
-// fully synchronous, oscillation-prone sweeps).
+// of the earlier ones.
 template <class K>
 void launch_chunks(K kernel, const MoveArgs& a, const u32* list, u64 count, int threads, u64 per_block,
                    u64 max_blocks, size_t smem, cudaStream_t s) {
@@ -386,20 +431,20 @@ void sweep(const MoveArgs& a, const Bins& b, cudaStream_t s) {
   if (b.count(2)) {
     constexpr int T = 256;
     auto k = lm_group<Tab, 8, kGroupCapLog, T, DRY>;
-    const size_t smem = size_t(T / 8) * (1u << kGroupCapLog) * Tab::kSlotBytes;
+    constexpr size_t smem = group_smem<Tab, 8, kGroupCapLog, T>();
     static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
     launch_chunks(k, a, b.of(2), b.count(2), T, T / 8, u64(sms) * occ, smem, s);
   }
   if (b.count(3)) {
     constexpr int T = 256;
     auto k = lm_group<Tab, 32, kWarpCapLog, T, DRY>;
-    const size_t smem = size_t(T / 32) * (1u << kWarpCapLog) * Tab::kSlotBytes;
+    constexpr size_t smem = group_smem<Tab, 32, kWarpCapLog, T>();
     static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
     launch_chunks(k, a, b.of(3), b.count(3), T, T / 32, u64(sms) * occ, smem, s);
   }
   if (b.count(4)) {
     auto k = lm_block<Tab, false, DRY>;
-    const size_t smem = (size_t(1) << kBlockCapLog) * Tab::kSlotBytes;
+    constexpr size_t smem = block_smem<Tab>();
     static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
     launch_chunks(k, a, b.of(4), b.count(4), kBlockThreads, 1, u64(sms) * occ, smem, s);
   }
@@ -414,17 +459,42 @@ void sweep(const MoveArgs& a, const Bins& b, cudaStream_t s) {
 }  // namespace
 
 size_t move_table_bytes(u64 max_degree, int value_bits, int* blocks) {
-  const u64 slots = u64(1) << ceil_log2_u64(2 * (max_degree ? max_degree : 1));
+  const u64 slots = u64(1) << std::max<u32>(5, ceil_log2_u64(2 * (max_degree ? max_degree : 1)));
   if (blocks) *blocks = sm_count();
-  const size_t per = slots * (value_bits == 64 ? SplitF64::kSlotBytes : PackedF32::kSlotBytes);
+  const size_t per = slots * (value_bits == 64 ? SplitF64::kSlotBytes : PackedF32::kSlotBytes) + slots / 2 * 4;
   return per * size_t(sm_count());
 }
 
-void move_sweep(const MoveArgs& a, const Bins& b, int value_bits, cudaStream_t s) {
+u64 move_table_slots(u64 max_degree) {
+  return u64(1) << std::max<u32>(5, ceil_log2_u64(2 * (max_degree ? max_degree : 1)));
+}
+
+// every slot of every per-block region empty (the kernels keep it that way)
+void move_table_init(void* table, u64 max_degree, int value_bits, cudaStream_t s) {
+  const u64 slots = move_table_slots(max_degree);
+  const int blocks = sm_count();
+  const size_t stride = slots * (value_bits == 64 ? SplitF64::kSlotBytes : PackedF32::kSlotBytes) + slots / 2 * 4;
+  for (int b = 0; b < blocks; ++b) {
+    unsigned char* base = static_cast<unsigned char*>(table) + size_t(b) * stride;
+    if (value_bits == 64) {
+      LVN_CUDA(cudaMemsetAsync(base, 0, slots * 8, s));                // values
+      LVN_CUDA(cudaMemsetAsync(base + slots * 8, 0xFF, slots * 4, s));  // keys
+    } else {
+      fill_u64<<<unsigned(std::min<u64>((slots + 255) / 256, 1024)), 256, 0, s>>>(
+          reinterpret_cast<ull*>(base), slots, kEmptySlot64);
+      LVN_LAUNCH();
+    }
+  }
+}
+
+void move_sweep(const MoveArgs& a0, const Bins& b, int value_bits, cudaStream_t s) {
   if (b.edges.thread_max > kThreadMaxD || b.edges.group_max > (1u << (kGroupCapLog - 1)) ||
       b.edges.warp_max > (1u << (kWarpCapLog - 1)) ||
       b.edges.block_max > (1u << (kBlockCapLog - 1)))
     fail(kInvalid, "degree bin edges exceed the device table capacities");
+  MoveArgs a = a0;
+  a.inv_m = 1.0 / a.m;
+  a.inv_2m2 = 1.0 / (2.0 * a.m * a.m);
   if (value_bits == 64) {
     a.dry ? sweep<SplitF64, true>(a, b, s) : sweep<SplitF64, false>(a, b, s);
   } else {

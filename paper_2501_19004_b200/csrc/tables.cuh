@@ -2,7 +2,9 @@
 // counterpart of the reference's slab tables, compact_hashtable.hpp:28-122):
 // power-of-two capacity, multiplicative hash, linear probing, empty key
 // 0xFFFFFFFF. Capacity is always >= 2x the distinct keys that can arrive,
-// so probing terminates.
+// so probing terminates. insert() returns the slot it claimed for a new key
+// (-1 when the key was already present), so callers can keep a list of live
+// slots: scans then touch only live entries and clearing touches only them.
 #pragma once
 
 #include "common.cuh"
@@ -15,13 +17,13 @@ __device__ __forceinline__ u32 table_log(u64 deg, u32 min_log) {
 }
 
 // ---- table flavours ---------------------------------------------------------
-struct PackedF32 {  // value_bits == 32
+struct PackedF32 {  // value_bits == 32: one 64-bit slot (key << 32 | float bits), one CAS per update
   using V = float;
   static constexpr size_t kSlotBytes = 8;
   ull* s;
   __device__ PackedF32(void* base, u64 slots) : s(static_cast<ull*>(base)) { (void)slots; }
   __device__ __forceinline__ void clear(u32 i) const { s[i] = kEmptySlot64; }
-  __device__ __forceinline__ void insert(u32 log_size, u32 key, float w) const {
+  __device__ __forceinline__ int insert(u32 log_size, u32 key, float w) const {
     const u32 mask = (1u << log_size) - 1u;
     u32 h = slot_hash(key, log_size);
     while (true) {
@@ -30,7 +32,7 @@ struct PackedF32 {  // value_bits == 32
       if (k == key || k == kEmpty) {
         const float nv = __uint_as_float(u32(cur)) + w;
         const ull want = (ull(key) << 32) | __float_as_uint(nv);
-        if (atomicCAS(&s[h], cur, want) == cur) return;
+        if (atomicCAS(&s[h], cur, want) == cur) return k == kEmpty ? int(h) : -1;
       } else {
         h = (h + 1) & mask;
       }
@@ -44,7 +46,7 @@ struct PackedF32 {  // value_bits == 32
   }
 };
 
-struct SplitF64 {  // value_bits == 64
+struct SplitF64 {  // value_bits == 64: u32 key array + fp64 value array
   using V = double;
   static constexpr size_t kSlotBytes = 12;
   u32* k;
@@ -56,18 +58,19 @@ struct SplitF64 {  // value_bits == 64
     k[i] = kEmpty;
     v[i] = 0.0;
   }
-  __device__ __forceinline__ void insert(u32 log_size, u32 key, double w) const {
+  __device__ __forceinline__ int insert(u32 log_size, u32 key, double w) const {
     const u32 mask = (1u << log_size) - 1u;
     u32 h = slot_hash(key, log_size);
     while (true) {
       u32 cur = reinterpret_cast<volatile u32*>(k)[h];
+      int claimed = -1;
       if (cur == kEmpty) {
         cur = atomicCAS(&k[h], kEmpty, key);
-        if (cur == kEmpty) cur = key;
+        if (cur == kEmpty) cur = key, claimed = int(h);
       }
       if (cur == key) {
         atomicAdd(&v[h], w);
-        return;
+        return claimed;
       }
       h = (h + 1) & mask;
     }
