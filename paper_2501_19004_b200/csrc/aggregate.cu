@@ -25,7 +25,7 @@ namespace cg = cooperative_groups;
 namespace lvn {
 namespace {
 
-constexpr int kGroupCapLog = 6;
+constexpr int kGroupCapLog = 7;
 constexpr int kWarpCapLog = 9;
 constexpr int kBlockCapLog = 13;
 constexpr int kBlockThreads = 512;
@@ -214,7 +214,7 @@ size_t aggregate_table_bytes(u64 max_slots, int* blocks) {
 
 void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
   const int sms = sm_count();
-  if (b.edges.group_max > 32 || b.edges.warp_max > 256 || b.edges.block_max > 4096)
+  if (b.edges.group_max > 64 || b.edges.warp_max > 256 || b.edges.block_max > 4096)
     fail(kInvalid, "aggregation bin edges exceed the device table capacities");
   const u64 small = b.count(1) + b.count(2);
   if (small) {

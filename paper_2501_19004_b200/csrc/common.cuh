@@ -131,9 +131,11 @@ struct DBuf {
 // Device helpers
 // ---------------------------------------------------------------------------
 __host__ __device__ inline u32 ceil_log2_u64(u64 x) {
-  u32 r = 0;
-  while ((u64(1) << r) < x) ++r;
-  return r;
+#ifdef __CUDA_ARCH__
+  return x <= 1 ? 0u : 64u - u32(__clzll((long long)(x - 1)));
+#else
+  return x <= 1 ? 0u : 64u - u32(__builtin_clzll(x - 1));
+#endif
 }
 
 // multiplicative hash into a power-of-two table of 2^log_size slots

@@ -16,7 +16,7 @@ void reduce_max_u32(const u32* in, u64 n, u32* out, cudaStream_t s);
 // ---- bins.cu: degree bins + pass reset ------------------------------------
 constexpr int kBins = 6;  // 0 isolated, 1 thread, 2 group8, 3 warp, 4 block, 5 global table
 struct BinEdges {
-  u32 thread_max = 4, group_max = 32, warp_max = 256, block_max = 4096;
+  u32 thread_max = 4, group_max = 64, warp_max = 256, block_max = 4096;
 };
 struct Bins {
   DBuf<u32> list;       // vertex ids grouped by bin, ascending within a bin

@@ -2,7 +2,7 @@
 // over the active vertices, degree-binned:
 //
 //   bin 1  deg <= thread_max (<= 8)   thread per vertex, candidates in registers
-//   bin 2  deg <= group_max  (<= 32)  8-lane group per vertex, 64-slot smem table
+//   bin 2  deg <= group_max  (<= 64)  8-lane group per vertex, 128-slot smem table
 //   bin 3  deg <= warp_max   (<= 256) warp per vertex, 512-slot smem table
 //   bin 4  deg <= block_max  (<= 4096) block per vertex, <= 8192-slot smem table
 //   bin 5  larger                      block per vertex, table in global memory
@@ -45,10 +45,11 @@ namespace lvn {
 namespace {
 
 constexpr int kThreadMaxD = 8;
-constexpr int kGroupCapLog = 6;    // 64 slots  (group_max <= 32)
+constexpr int kGroupCapLog = 7;    // 128 slots (group_max <= 64)
 constexpr int kWarpCapLog = 9;     // 512 slots (warp_max <= 256)
 constexpr int kBlockCapLog = 13;   // 8192 slots (block_max <= 4096)
 constexpr int kBlockThreads = 512;
+constexpr int kBatch = 4;          // arcs (and ranked entries) in flight per lane
 
 // ---- per-thread accounting, flushed once per thread at kernel exit ----------
 struct Tally {
@@ -186,6 +187,65 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
   tl.flush(x);
 }
 
+// ---- shared scan / rank loops of the table kernels ----------------------------------
+// Accumulate K_{u->c} over arcs [lo, hi) handled by `lane` of `stride` lanes, B
+// arcs per lane per round: all B target/weight loads, then all B C[t] gathers,
+// are issued before the first dependent use, so each lane keeps B independent
+// memory requests in flight (the sweep is latency-bound otherwise).
+template <int B, class Tab, class V>
+__device__ __forceinline__ void scan_arcs(const MoveArgs& x, const Tab& tab, u32 lg, u32 u, u32 from,
+                                          u64 lo, u64 hi, u32 lane, u32 stride, V& own, u32* live,
+                                          u32* nlive) {
+  for (u64 base = lo + lane; base < hi; base += u64(stride) * B) {
+    u32 t[B], c[B];
+    V w[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const u64 a = base + u64(k) * stride;
+      t[k] = a < hi ? x.g.tgt[a] : u;  // out of range reads as a self-loop: skipped
+      w[k] = a < hi ? V(x.g.w[a]) : V(0);
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) c[k] = t[k] != u ? x.C[t[k]] : kEmpty;
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (c[k] == kEmpty) continue;
+      if (c[k] == from) {
+        own += w[k];
+      } else {
+        const int slot = tab.insert(lg, c[k], w[k]);
+        if (slot >= 0) live[atomicAdd(nlive, 1u)] = u32(slot);
+      }
+    }
+  }
+}
+
+// Best live entry seen by this lane (B Sigma gathers in flight per round).
+template <int B, bool DRY, class Tab>
+__device__ __forceinline__ void rank_live(const MoveArgs& x, const Tab& tab, const u32* live, u32 n,
+                                          u32 lane, u32 stride, double own, double ku, double sf,
+                                          double& bg, u32& bc, double& bk) {
+  for (u32 j0 = lane; j0 < n; j0 += stride * B) {
+    u32 key[B];
+    double val[B], sc[B];
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      const u32 j = j0 + k * stride;
+      key[k] = kEmpty;
+      val[k] = 0.0;
+      if (j < n && !(tab.read(live[j], key[k], val[k]) && key_ok(x, key[k]))) key[k] = kEmpty;
+    }
+#pragma unroll
+    for (int k = 0; k < B; ++k) sc[k] = key[k] != kEmpty ? x.sigma[key[k]] : 0.0;
+#pragma unroll
+    for (int k = 0; k < B; ++k) {
+      if (key[k] == kEmpty) continue;
+      const double g = score<DRY>(x, val[k], own, ku, sc[k], sf);
+      if (better(g, key[k], bg, bc)) bg = g, bc = key[k], bk = val[k];
+    }
+  }
+}
+
 // ---- bins 2 and 3: G lanes per vertex, smem table + live list per group ---------
 template <class Tab, int G, int CAPLOG, int THREADS>
 constexpr size_t group_smem() {
@@ -230,32 +290,14 @@ __global__ void __launch_bounds__(THREADS, 4) lm_group(MoveArgs x, const u32* __
       continue;
     }
     V own = V(0);
-    for (u64 a = lo + lane; a < lo + d; a += G) {
-      const u32 t = x.g.tgt[a];
-      if (t == u) continue;
-      const V w = V(x.g.w[a]);
-      const u32 c = x.C[t];
-      if (c == from) {
-        own += w;
-      } else {
-        const int slot = tab.insert(lg, c, w);
-        if (slot >= 0) live[atomicAdd(nlive, 1u)] = u32(slot);
-      }
-    }
+    scan_arcs<kBatch>(x, tab, lg, u, from, lo, lo + d, lane, G, own, live, nlive);
     own = cg::reduce(tile, own, cg::plus<V>());
     tile.sync();
     const u32 n = *reinterpret_cast<volatile u32*>(nlive);
     const double ku = x.K[u], sf = x.sigma[from];
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
-    for (u32 j = lane; j < n; j += G) {
-      u32 key;
-      double val;
-      if (tab.read(live[j], key, val) && key_ok(x, key)) {
-        const double g = score<DRY>(x, val, double(own), ku, x.sigma[key], sf);
-        if (better(g, key, bg, bc)) bg = g, bc = key, bk = val;
-      }
-    }
+    rank_live<kBatch, DRY>(x, tab, live, n, lane, G, double(own), ku, sf, bg, bc, bk);
 #pragma unroll
     for (int o = G / 2; o > 0; o >>= 1) {
       const double og = tile.shfl_xor(bg, o);
@@ -328,18 +370,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
       continue;
     }
     V own = V(0);
-    for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) {
-      const u32 t = x.g.tgt[a];
-      if (t == u) continue;
-      const V w = V(x.g.w[a]);
-      const u32 c = x.C[t];
-      if (c == from) {
-        own += w;
-      } else {
-        const int slot = tab.insert(lg, c, w);
-        if (slot >= 0) live[atomicAdd(&nlive, 1u)] = u32(slot);
-      }
-    }
+    scan_arcs<kBatch>(x, tab, lg, u, from, lo, lo + d, threadIdx.x, kBlockThreads, own, live, &nlive);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
     if (lane == 0) red_v[wid] = own;
@@ -351,14 +382,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
     const double ku = x.K[u], sf = x.sigma[from];
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
-    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) {
-      u32 key;
-      double val;
-      if (tab.read(live[j], key, val) && key_ok(x, key)) {
-        const double g = score<DRY>(x, val, double(own_all), ku, x.sigma[key], sf);
-        if (better(g, key, bg, bc)) bg = g, bc = key, bk = val;
-      }
-    }
+    rank_live<kBatch, DRY>(x, tab, live, n, threadIdx.x, kBlockThreads, double(own_all), ku, sf, bg, bc, bk);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double og = __shfl_xor_sync(0xffffffffu, bg, o);

@@ -276,13 +276,17 @@ def test_engine_quality_vs_reference_planted(lvn, t):
 
 
 @pytest.mark.parametrize("value_bits", [32, 64])
-def test_engine_quality_rmat16_c1(lvn, port, value_bits):
-    # config C1: RMAT scale 16, edge factor 16, dedupe, default parameters
+def test_engine_quality_rmat16_c1(lvn, port, ref, value_bits):
+    # config C1: RMAT scale 16, edge factor 16, dedupe, default parameters. The
+    # gate is |Q_gpu - mean Q of the reference louvain_mc| <= 0.005,
+    # with louvain_mc run on all host cores as in the CPU baseline.
     g = rmat(16, 16, 1)
-    want = port.sequential_louvain(g).modularity
+    want = float(np.mean([ref.louvain(g, "mc").modularity for _ in range(3)]))
+    qs = [lvn.louvain_compact(G_(g, lvn), None, lvn.CompactOptions(value_bits=value_bits)).modularity
+          for _ in range(3)]
     r = lvn.louvain_compact(G_(g, lvn), None, lvn.CompactOptions(value_bits=value_bits))
     assert_q(r.modularity, port.modularity(g, r.membership))
-    assert r.modularity >= want - Q_TOL, (r.modularity, want)
+    assert float(np.mean(qs)) >= want - Q_TOL, (qs, want)
 
 
 def test_engine_quality_planted_large(lvn, port):
