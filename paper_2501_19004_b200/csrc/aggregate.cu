@@ -216,31 +216,31 @@ void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
   const int sms = sm_count();
   if (b.edges.group_max > 64 || b.edges.warp_max > 256 || b.edges.block_max > 4096)
     fail(kInvalid, "aggregation bin edges exceed the device table capacities");
-  const u64 small = b.count(1) + b.count(2);
+  const u64 small = b.start[kBinWarp] - b.start[kBinThread];  // budgets <= group_max (<= 64)
   if (small) {
     constexpr int T = 256;
     auto k = ag_group<8, kGroupCapLog, T>;
     const size_t smem = size_t(T / 8) * (1u << kGroupCapLog) * Tab::kSlotBytes;
     static const int occ = occupancy(k, T, smem);
     const u64 blocks = std::min<u64>((small + T / 8 - 1) / (T / 8), u64(sms) * occ);
-    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(1), small);
+    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(kBinThread), small);
     LVN_LAUNCH();
   }
-  if (b.count(3)) {
+  if (b.count(kBinWarp)) {
     constexpr int T = 256;
     auto k = ag_group<32, kWarpCapLog, T>;
     const size_t smem = size_t(T / 32) * (1u << kWarpCapLog) * Tab::kSlotBytes;
     static const int occ = occupancy(k, T, smem);
-    const u64 blocks = std::min<u64>((b.count(3) + T / 32 - 1) / (T / 32), u64(sms) * occ);
-    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(3), b.count(3));
+    const u64 blocks = std::min<u64>((b.count(kBinWarp) + T / 32 - 1) / (T / 32), u64(sms) * occ);
+    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(kBinWarp), b.count(kBinWarp));
     LVN_LAUNCH();
   }
-  const u64 big = b.count(4) + b.count(5);
+  const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
   if (big) {
     const size_t smem = (size_t(1) << kBlockCapLog) * Tab::kSlotBytes;
     static const int occ = occupancy(ag_block, kBlockThreads, smem);
     const u64 blocks = std::min<u64>(big, u64(sms) * (a.table ? 1 : occ));
-    ag_block<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(4), big);
+    ag_block<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(kBinBlock), big);
     LVN_LAUNCH();
   }
 }

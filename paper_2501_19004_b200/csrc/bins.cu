@@ -15,12 +15,17 @@ constexpr int kRounds = 8;  // vertices per thread per tile
 constexpr int kTileV = kT * kRounds;
 
 __device__ __forceinline__ int bin_of(u64 deg, const BinEdges& e) {
-  if (deg == 0) return 0;
-  if (deg <= e.thread_max) return 1;
-  if (deg <= e.group_max) return 2;
-  if (deg <= e.warp_max) return 3;
-  if (deg <= e.block_max) return 4;
-  return 5;
+  if (deg == 0) return kBinIso;
+  if (deg <= e.thread_max) return kBinThread;
+  if (deg <= e.group_max) {
+    if (deg <= 8) return kBinSort8;
+    if (deg <= 16) return kBinSort16;
+    if (deg <= 32) return kBinSort32;
+    return kBinSort64;
+  }
+  if (deg <= e.warp_max) return kBinWarp;
+  if (deg <= e.block_max) return kBinBlock;
+  return kBinGlobal;
 }
 
 __global__ void __launch_bounds__(kT) bin_count(const u64* __restrict__ off, u32 n, BinEdges e,
@@ -167,20 +172,52 @@ void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C
   const u64 tb = std::min<u64>((g.n + 255) / 256, u64(sms) * 16);
   reset_thread<<<unsigned(tb), 256, 0, s>>>(g, b.edges.group_max, K, sigma, C, flags);
   LVN_LAUNCH();
-  if (b.count(3)) {
-    const u64 wb = std::min<u64>((b.count(3) + 7) / 8, u64(sms) * 16);
-    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(3), b.count(3), K, sigma);
+  if (b.count(kBinWarp)) {
+    const u64 wb = std::min<u64>((b.count(kBinWarp) + 7) / 8, u64(sms) * 16);
+    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinWarp), b.count(kBinWarp), K, sigma);
     LVN_LAUNCH();
   }
-  const u64 big = b.count(4) + b.count(5);
+  const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
   if (big) {
     const u64 bb = std::min<u64>(big, u64(sms) * 4);
-    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(4), big, K, sigma);
+    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(kBinBlock), big, K, sigma);
     LVN_LAUNCH();
   }
 }
 
+// active vertices of every bin segment, packed at the front of the segment
+__global__ void compact_active_k(const u32* __restrict__ list, u64 n, BinView v,
+                                 const u8* __restrict__ flags, u32* __restrict__ out,
+                                 ull* __restrict__ counts) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n;
+       i += u64(gridDim.x) * blockDim.x) {
+    const u32 u = list[i];
+    int b = kBins - 1;
+    while (b > 0 && i < v.off[b]) --b;
+    const bool on = b != kBinIso && flags[u];
+    const u32 act = __activemask();
+    const u32 key = on ? u32(b) : 0xFFFFFFFFu;
+    const u32 peers = __match_any_sync(act, key);
+    if (!on) continue;
+    const int lane = threadIdx.x & 31;
+    const int leader = __ffs(peers) - 1;
+    ull base = 0;
+    if (lane == leader) base = atomicAdd(&counts[b], ull(__popc(peers)));
+    base = __shfl_sync(peers, base, leader);
+    out[v.off[b] + base + __popc(peers & ((1u << lane) - 1u))] = u;
+  }
+}
+
 }  // namespace
+
+void compact_active(const Bins& b, const u8* flags, u32* out_list, ull* counts, cudaStream_t s) {
+  LVN_CUDA(cudaMemsetAsync(counts, 0, kBins * sizeof(ull), s));
+  const u64 n = b.start[kBins];
+  if (!n) return;
+  const u64 blocks = std::min<u64>((n + 255) / 256, u64(sm_count()) * 8);
+  compact_active_k<<<unsigned(blocks), 256, 0, s>>>(b.list.p, n, b.view(), flags, out_list, counts);
+  LVN_LAUNCH();
+}
 
 void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStream_t s, u64 cap) {
   out.edges = e;

@@ -292,6 +292,7 @@ struct Timing {
 struct IterRecord {  // device scratch read back once per iteration
   double gain;
   ull verts, arcs, moves;
+  ull active[kBins];  // per-bin sizes of the next iteration's active lists
 };
 
 // ---- renumbering: ids of C (all < width) -> 0..count-1 ascending, returns count
@@ -344,7 +345,7 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   DBuf<double> table;
   const u64 max_cap = std::min<u64>(ab.max_degree, count);
   const u64 slots = u64(1) << std::max<u32>(5, ceil_log2_u64(2 * (max_cap ? max_cap : 1)));
-  if (slots > (u64(1) << 13) && (ab.count(4) + ab.count(5))) {
+  if (slots > (u64(1) << 13) && (ab.count(kBinBlock) + ab.count(kBinGlobal))) {
     int blocks = 0;
     const size_t bytes = aggregate_table_bytes(slots, &blocks);
     table.alloc(bytes / sizeof(double) + 1);
@@ -480,7 +481,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
   const BinEdges edges = edges_of(p);
   Timing tm;
 
-  DBuf<u32> global(N ? N : 1), C(N ? N : 1), used, rank;
+  DBuf<u32> global(N ? N : 1), C(N ? N : 1), used, rank, active;
   DBuf<double> K(N ? N : 1), S(N ? N : 1), table;
   DBuf<u8> flags(N ? N : 1);
   DBuf<IterRecord> rec(1);
@@ -522,7 +523,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
     a.counters = &rec.p->verts;
     a.err = err.p;
     a.chunk = sweep_chunk(p, nv);
-    if (B.count(5)) {
+    if (B.count(kBinGlobal)) {
       int blocks = 0;
       const size_t bytes = move_table_bytes(B.max_degree, p.value_bits, &blocks);
       table.ensure(bytes / sizeof(double) + 1);
@@ -532,18 +533,27 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
     }
     const auto t0 = Clock::now();
     int iterations = 0;
+    // iteration 0 sweeps every row with arcs (all flagged); later iterations
+    // sweep the flagged rows only, compacted right after the previous sweep
+    BinView view = B.view();
+    active.ensure(nv ? nv : 1);
     for (int it = 0; it < p.max_iterations; ++it) {
       a.pickless = pick_less_active(it, p.pick_less_period);
       LVN_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(IterRecord), s));
       sp = tm.begin(LVN_STAT_MOVE, s);
-      move_sweep(a, B, p.value_bits, s);
+      move_sweep(a, view, p.value_bits, s);
       tm.end(sp, s, 0.0);
+      if (p.prune) compact_active(B, flags.p, active.p, rec.p->active, s);
       IterRecord* h = reinterpret_cast<IterRecord*>(c.pinned);
       LVN_CUDA(cudaMemcpyAsync(h, rec.p, sizeof(IterRecord), cudaMemcpyDeviceToHost, s));
       LVN_CUDA(cudaStreamSynchronize(s));
       tm.set_bytes(sp, 12.0 * double(h->arcs) + 32.0 * double(h->verts), h->verts, h->arcs);
       ++iterations;
       if (h->gain <= tolerance) break;  // louvain_compact.cpp:209
+      if (p.prune) {
+        view.list = active.p;
+        for (int b = 0; b < kBins; ++b) view.cnt[b] = h->active[b];
+      }
     }
     t_move += since(t0);
     check_err(err.p, s);
@@ -1011,7 +1021,7 @@ int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const doubl
     a.gain_acc = &rec.p->gain;
     a.counters = &rec.p->verts;
     a.err = err.p;
-    if (b.count(5)) {
+    if (b.count(kBinGlobal)) {
       int blocks = 0;
       const size_t bytes = move_table_bytes(b.max_degree, pp.value_bits, &blocks);
       table.alloc(bytes / sizeof(double) + 1);
@@ -1019,7 +1029,7 @@ int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const doubl
       a.table = table.p;
       a.table_slots = move_table_slots(b.max_degree);
     }
-    move_sweep(a, b, pp.value_bits, s);
+    move_sweep(a, b.view(), pp.value_bits, s);
     if (n) {
       LVN_CUDA(cudaMemcpyAsync(to, ot.p, n * sizeof(u32), cudaMemcpyDeviceToHost, s));
       LVN_CUDA(cudaMemcpyAsync(gain, og.p, n * sizeof(double), cudaMemcpyDeviceToHost, s));

@@ -14,9 +14,31 @@ void exclusive_scan_u32_to_u64(const u32* in, u64* out, u64 n, cudaStream_t s);
 void reduce_max_u32(const u32* in, u64 n, u32* out, cudaStream_t s);
 
 // ---- bins.cu: degree bins + pass reset ------------------------------------
-constexpr int kBins = 6;  // 0 isolated, 1 thread, 2 group8, 3 warp, 4 block, 5 global table
+// Degree classes (the kernel that handles a row / community):
+enum : int {
+  kBinIso = 0,     // no arcs
+  kBinThread = 1,  // deg <= thread_max: thread per vertex, registers
+  kBinSort8 = 2,   // deg <= 8 (and <= group_max): 8 lanes, register bitonic sort
+  kBinSort16 = 3,  // deg <= 16
+  kBinSort32 = 4,  // deg <= 32
+  kBinSort64 = 5,  // deg <= 64: 32 lanes x 2 registers
+  kBinWarp = 6,    // deg <= warp_max: warp, smem hash table
+  kBinBlock = 7,   // deg <= block_max: block, smem hash table
+  kBinGlobal = 8,  // larger: block, global-memory hash table
+  kBins = 9
+};
 struct BinEdges {
   u32 thread_max = 4, group_max = 64, warp_max = 256, block_max = 4096;
+};
+// A set of per-bin vertex lists (the full bins, or the active subset of an iteration)
+struct BinView {
+  const u32* list = nullptr;
+  u64 off[kBins] = {};
+  u64 cnt[kBins] = {};
+  u64 max_degree = 0;
+  BinEdges edges;
+  u64 count(int b) const { return cnt[b]; }
+  const u32* of(int b) const { return list + off[b]; }
 };
 struct Bins {
   DBuf<u32> list;       // vertex ids grouped by bin, ascending within a bin
@@ -25,7 +47,19 @@ struct Bins {
   BinEdges edges;
   u64 count(int b) const { return start[b + 1] - start[b]; }
   const u32* of(int b) const { return list.p + start[b]; }
+  BinView view() const {
+    BinView v;
+    v.list = list.p;
+    for (int b = 0; b < kBins; ++b) v.off[b] = start[b], v.cnt[b] = count(b);
+    v.max_degree = max_degree;
+    v.edges = edges;
+    return v;
+  }
 };
+// active subset of b: out_list gets, inside each bin's segment, the vertices
+// whose flag is set (order within a bin not preserved); counts[b] (device,
+// zeroed here) receives the per-bin sizes
+void compact_active(const Bins& b, const u8* flags, u32* out_list, ull* counts, cudaStream_t s);
 // bin of row v by min(off[v+1]-off[v], cap): rows of a CSR, or community
 // budgets during aggregation. Synchronises (reads the bin sizes).
 void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStream_t s,
@@ -56,9 +90,8 @@ struct MoveArgs {
   u64 chunk = ~u64(0);         // max vertices of one bin decided per launch
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
 };
-// one sweep over bins 1..5 (thread, group8, warp, block, global); the
-// force_kernel >= 0 variant routes every vertex to at least that class.
-void move_sweep(const MoveArgs& a, const Bins& bins, int value_bits, cudaStream_t s);
+// one sweep over the bins of `bins` (see the kBin* classes)
+void move_sweep(const MoveArgs& a, const BinView& bins, int value_bits, cudaStream_t s);
 size_t move_table_bytes(u64 max_degree, int value_bits, int* blocks);
 u64 move_table_slots(u64 max_degree);
 // mark every slot of the bin-5 tables empty (done whenever they are allocated)

@@ -110,21 +110,21 @@ void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot,
   LVN_CUDA(cudaMemsetAsync(tot, 0, width * sizeof(double), s));
   LVN_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), s));
   const int sms = sm_count();
-  const u64 small = b.count(0) + b.count(1) + b.count(2);
+  const u64 small = b.start[kBinWarp] - b.start[kBinIso];  // rows of <= 64 arcs
   if (small) {
     const u64 blocks = std::min<u64>((small + 255) / 256, u64(sms) * 8);
-    mod_thread<<<unsigned(blocks), 256, 0, s>>>(g, b.of(0), small, C, tot, sums);
+    mod_thread<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinIso), small, C, tot, sums);
     LVN_LAUNCH();
   }
-  if (b.count(3)) {
-    const u64 blocks = std::min<u64>((b.count(3) + 7) / 8, u64(sms) * 8);
-    mod_warp<<<unsigned(blocks), 256, 0, s>>>(g, b.of(3), b.count(3), C, tot, sums);
+  if (b.count(kBinWarp)) {
+    const u64 blocks = std::min<u64>((b.count(kBinWarp) + 7) / 8, u64(sms) * 8);
+    mod_warp<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinWarp), b.count(kBinWarp), C, tot, sums);
     LVN_LAUNCH();
   }
-  const u64 big = b.count(4) + b.count(5);
+  const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
   if (big) {
     const u64 blocks = std::min<u64>(big, u64(sms) * 4);
-    mod_block<<<unsigned(blocks), 512, 0, s>>>(g, b.of(4), big, C, tot, sums);
+    mod_block<<<unsigned(blocks), 512, 0, s>>>(g, b.of(kBinBlock), big, C, tot, sums);
     LVN_LAUNCH();
   }
   if (width) {

@@ -202,8 +202,8 @@ __device__ __forceinline__ void scan_arcs(const MoveArgs& x, const Tab& tab, u32
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       const u64 a = base + u64(k) * stride;
-      t[k] = a < hi ? x.g.tgt[a] : u;  // out of range reads as a self-loop: skipped
-      w[k] = a < hi ? V(x.g.w[a]) : V(0);
+      t[k] = a < hi ? __ldcs(x.g.tgt + a) : u;  // out of range reads as a self-loop: skipped
+      w[k] = a < hi ? V(__ldcs(x.g.w + a)) : V(0);
     }
 #pragma unroll
     for (int k = 0; k < B; ++k) c[k] = t[k] != u ? x.C[t[k]] : kEmpty;
@@ -316,6 +316,165 @@ __global__ void __launch_bounds__(THREADS, 4) lm_group(MoveArgs x, const u32* __
     if (!DRY && tile.shfl(moved, 0) && x.prune)
       for (u64 a = lo + lane; a < lo + d; a += G) x.flags[x.g.tgt[a]] = 1;
     tile.sync();
+  }
+  tl.flush(x);
+}
+
+// ---- sort bins: G lanes x K registers per vertex, register bitonic sort --------
+// The (community, weight) pairs of a vertex's arcs are sorted by community
+// across the G lanes of its group (element e lives in lane e / K, register
+// e % K), so equal communities form adjacent runs, and a segmented scan leaves
+// K_{u->c} on the last element of each run. The network is data-independent:
+// every lane of a warp runs the same instruction stream (no atomics, no
+// shared memory, no probe loops), which the hash kernels cannot achieve on
+// short rows where each group's probing diverges. Row arcs are streamed with
+// evict-first loads so the gathered C / Sigma lines keep their L2 residency.
+template <int G, int K, class V, bool DRY>
+__global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict__ list, u64 count) {
+  constexpr int GPB = 256 / G;
+  constexpr int N = G * K;
+  constexpr u32 FULL = 0xffffffffu;
+  const u32 lane = threadIdx.x & (G - 1);
+  const u32 gi = threadIdx.x / G;
+  Tally tl;
+  // the trip count is uniform across the block, so every lane reaches every shuffle
+  for (u64 i0 = u64(blockIdx.x) * GPB; i0 < count; i0 += u64(gridDim.x) * GPB) {
+    const u64 i = i0 + gi;
+    const bool have = i < count;
+    u32 u = 0, from = kEmpty;
+    u64 lo = 0, hi = 0;
+    double ku = 0.0, sf = 0.0;
+    if (have) {
+      u = list[i];
+      lo = x.g.off[u];
+      hi = x.g.off[u + 1];
+      from = x.C[u];
+      ku = x.K[u];
+      sf = x.sigma[from];
+    }
+    u32 t[K], key[K];
+    V val[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const u64 a = lo + u64(r) * G + lane;
+      const bool ok = a < hi;
+      t[r] = ok ? __ldcs(x.g.tgt + a) : kEmpty;
+      val[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+    }
+#pragma unroll
+    for (int r = 0; r < K; ++r) key[r] = (t[r] != kEmpty && t[r] != u) ? x.C[t[r]] : kEmpty;
+
+    // bitonic sort, ascending by key (padding and self-loops carry kEmpty and sort last)
+#pragma unroll
+    for (int size = 2; size <= N; size <<= 1) {
+#pragma unroll
+      for (int j = size >> 1; j > 0; j >>= 1) {
+        if (j < K) {
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            if (r & j) continue;
+            const int r2 = r | j;
+            const bool asc = ((lane * K + r) & size) == 0;
+            if ((key[r] > key[r2]) == asc) {
+              const u32 tk = key[r];
+              key[r] = key[r2];
+              key[r2] = tk;
+              const V tv = val[r];
+              val[r] = val[r2];
+              val[r2] = tv;
+            }
+          }
+        } else {
+          const int lj = j / K;
+#pragma unroll
+          for (int r = 0; r < K; ++r) {
+            const u32 pk = __shfl_xor_sync(FULL, key[r], lj, G);
+            const V pv = __shfl_xor_sync(FULL, val[r], lj, G);
+            const bool asc = ((lane * K + r) & size) == 0;
+            const bool lower = (lane & lj) == 0;
+            if (lower == asc ? pk < key[r] : pk > key[r]) key[r] = pk, val[r] = pv;
+          }
+        }
+      }
+    }
+
+    // run heads, in-lane segmented sums, then the carry of the run entering the lane
+    const u32 prev_last = __shfl_up_sync(FULL, key[K - 1], 1, G);
+    bool head[K];
+    V run[K];
+    bool lane_head = false;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      head[r] = r == 0 ? (lane == 0 || key[0] != prev_last) : key[r] != key[r - 1];
+      run[r] = (r == 0 || head[r]) ? val[r] : run[r - 1] + val[r];
+      lane_head = lane_head || head[r];
+    }
+    V agg = run[K - 1];
+    int f = lane_head;
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+      const V pa = __shfl_up_sync(FULL, agg, d, G);
+      const int pf = __shfl_up_sync(FULL, f, d, G);
+      if (lane >= u32(d)) {
+        if (!f) agg = pa + agg;
+        f = f | pf;
+      }
+    }
+    const V carry_in = __shfl_up_sync(FULL, agg, 1, G);
+    bool open = lane != 0;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      open = open && !head[r];
+      if (open) run[r] += carry_in;
+    }
+    const int next_head = __shfl_down_sync(FULL, int(head[0]), 1, G);
+
+    // own community weight and the best other community
+    V own_l = V(0);
+    bool cand[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const bool tail = r + 1 < K ? head[r + 1] : (lane == G - 1 || next_head);
+      if (tail && key[r] == from) own_l = run[r];
+      cand[r] = tail && key[r] != kEmpty && key[r] != from;
+    }
+    V own = own_l;
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) own += __shfl_xor_sync(FULL, own, o, G);
+    double sc[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      if (cand[r]) cand[r] = key_ok(x, key[r]);
+      sc[r] = cand[r] ? x.sigma[key[r]] : 0.0;
+    }
+    double bg = -INFINITY, bk = 0.0;
+    u32 bc = kEmpty;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      if (!cand[r]) continue;
+      const double g = score<DRY>(x, double(run[r]), double(own), ku, sc[r], sf);
+      if (better(g, key[r], bg, bc)) bg = g, bc = key[r], bk = double(run[r]);
+    }
+#pragma unroll
+    for (int o = G / 2; o > 0; o >>= 1) {
+      const double og = __shfl_xor_sync(FULL, bg, o, G);
+      const u32 oc = __shfl_xor_sync(FULL, bc, o, G);
+      const double ok = __shfl_xor_sync(FULL, bk, o, G);
+      if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
+    }
+    int moved = 0;
+    if (have && lane == 0) {
+      if (!DRY) x.flags[u] = 0;
+      ++tl.verts;
+      tl.arcs += hi - lo;
+      moved = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own), tl);
+    }
+    moved = __shfl_sync(FULL, moved, 0, G);
+    if (!DRY && moved && x.prune) {
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (t[r] != kEmpty) x.flags[t[r]] = 1;
+    }
   }
   tl.flush(x);
 }
@@ -443,40 +602,47 @@ void launch_chunks(K kernel, const MoveArgs& a, const u32* list, u64 count, int 
   }
 }
 
+template <int G, int K, class V, bool DRY>
+void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
+  if (!b.count(bin)) return;
+  constexpr int T = 256;
+  auto k = lm_sort<G, K, V, DRY>;
+  static const int occ = occupancy(k, T, 0);
+  launch_chunks(k, a, b.of(bin), b.count(bin), T, T / G, u64(sm_count()) * occ, 0, s);
+}
+
 template <class Tab, bool DRY>
-void sweep(const MoveArgs& a, const Bins& b, cudaStream_t s) {
+void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
   using V = typename Tab::V;
   const int sms = sm_count();
-  if (b.count(1)) {
+  if (b.count(kBinThread)) {
     auto k = lm_thread<V, DRY>;
     static const int occ = occupancy(k, 256, 0);
-    launch_chunks(k, a, b.of(1), b.count(1), 256, 256, u64(sms) * occ, 0, s);
+    launch_chunks(k, a, b.of(kBinThread), b.count(kBinThread), 256, 256, u64(sms) * occ, 0, s);
   }
-  if (b.count(2)) {
-    constexpr int T = 256;
-    auto k = lm_group<Tab, 8, kGroupCapLog, T, DRY>;
-    constexpr size_t smem = group_smem<Tab, 8, kGroupCapLog, T>();
-    static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
-    launch_chunks(k, a, b.of(2), b.count(2), T, T / 8, u64(sms) * occ, smem, s);
-  }
-  if (b.count(3)) {
+  launch_sort<8, 1, V, DRY>(a, b, kBinSort8, s);
+  launch_sort<16, 1, V, DRY>(a, b, kBinSort16, s);
+  launch_sort<32, 1, V, DRY>(a, b, kBinSort32, s);
+  launch_sort<32, 2, V, DRY>(a, b, kBinSort64, s);
+  if (b.count(kBinWarp)) {
     constexpr int T = 256;
     auto k = lm_group<Tab, 32, kWarpCapLog, T, DRY>;
     constexpr size_t smem = group_smem<Tab, 32, kWarpCapLog, T>();
     static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
-    launch_chunks(k, a, b.of(3), b.count(3), T, T / 32, u64(sms) * occ, smem, s);
+    launch_chunks(k, a, b.of(kBinWarp), b.count(kBinWarp), T, T / 32, u64(sms) * occ, smem, s);
   }
-  if (b.count(4)) {
+  if (b.count(kBinBlock)) {
     auto k = lm_block<Tab, false, DRY>;
     constexpr size_t smem = block_smem<Tab>();
     static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
-    launch_chunks(k, a, b.of(4), b.count(4), kBlockThreads, 1, u64(sms) * occ, smem, s);
+    launch_chunks(k, a, b.of(kBinBlock), b.count(kBinBlock), kBlockThreads, 1, u64(sms) * occ, smem, s);
   }
-  if (b.count(5)) {
+  if (b.count(kBinGlobal)) {
     if (!a.table || !a.table_slots) fail(kInternal, "global move table not provisioned");
     int blocks = 0;
     move_table_bytes(b.max_degree, sizeof(V) == 4 ? 32 : 64, &blocks);
-    launch_chunks(lm_block<Tab, true, DRY>, a, b.of(5), b.count(5), kBlockThreads, 1, u64(blocks), 0, s);
+    launch_chunks(lm_block<Tab, true, DRY>, a, b.of(kBinGlobal), b.count(kBinGlobal), kBlockThreads, 1,
+                  u64(blocks), 0, s);
   }
 }
 
@@ -511,7 +677,7 @@ void move_table_init(void* table, u64 max_degree, int value_bits, cudaStream_t s
   }
 }
 
-void move_sweep(const MoveArgs& a0, const Bins& b, int value_bits, cudaStream_t s) {
+void move_sweep(const MoveArgs& a0, const BinView& b, int value_bits, cudaStream_t s) {
   if (b.edges.thread_max > kThreadMaxD || b.edges.group_max > (1u << (kGroupCapLog - 1)) ||
       b.edges.warp_max > (1u << (kWarpCapLog - 1)) ||
       b.edges.block_max > (1u << (kBlockCapLog - 1)))
