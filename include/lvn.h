@@ -99,7 +99,18 @@ typedef struct lvn_params {
    * sweep (launches run in vertex order, later ones see earlier moves);
    * 0 = automatic (scaled to the graph), UINT32_MAX = one launch per bin */
   uint32_t sweep_chunk;
-  int reserved[6];
+  /* order of the degree classes within a sweep range: 0 low degree first
+   * (the reference compact engine's order, default), 1 hubs first */
+  int sweep_order;
+  /* a sweep visits the vertex ids in this many consecutive ranges, each range
+   * running all its degree classes before the next starts (1 = one range, the
+   * reference compact order; larger approaches the id order of louvain_mc);
+   * 0 = automatic */
+  int sweep_ranges;
+  /* 1: a singleton may join another singleton community only if its id is
+   * lower (concurrent symmetric pairs merge instead of swapping labels) */
+  int singleton_rule;
+  int reserved[3];
 } lvn_params;
 
 /* Per-kernel-family device accounting (CUDA events on the engine stream). */

@@ -62,7 +62,10 @@ class lvn_params(C.Structure):
         ("bin_block_max", C.c_uint32),
         ("membership_on_device", C.c_int),
         ("sweep_chunk", C.c_uint32),
-        ("reserved", C.c_int * 6),
+        ("sweep_order", C.c_int),
+        ("sweep_ranges", C.c_int),
+        ("singleton_rule", C.c_int),
+        ("reserved", C.c_int * 3),
     ]
 
 

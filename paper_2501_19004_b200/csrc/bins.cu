@@ -64,7 +64,7 @@ __global__ void __launch_bounds__(kT) bin_count(const u64* __restrict__ off, u32
 
 __global__ void __launch_bounds__(kT) bin_scatter(const u64* __restrict__ off, u32 n, BinEdges e,
                                                   u64 cap, const u64* __restrict__ pos,
-                                                  u32 nblocks, u32* __restrict__ list) {
+                                                  u32 nblocks, u32* __restrict__ list, u32 id_base) {
   __shared__ u32 wc[kT / 32][kBins];
   __shared__ u64 run[kBins];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -90,7 +90,7 @@ __global__ void __launch_bounds__(kT) bin_scatter(const u64* __restrict__ off, u
     if (b >= 0) {
       u64 o = run[b];
       for (int w = 0; w < wid; ++w) o += wc[w][b];
-      list[o + my_rank] = u32(v);
+      list[o + my_rank] = u32(v) + id_base;
     }
     __syncthreads();
     if (threadIdx.x < kBins) {
@@ -219,7 +219,8 @@ void compact_active(const Bins& b, const u8* flags, u32* out_list, ull* counts, 
   LVN_LAUNCH();
 }
 
-void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStream_t s, u64 cap) {
+void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStream_t s, u64 cap,
+                  u32 id_base) {
   out.edges = e;
   out.list.ensure(n ? n : 1);
   if (n == 0) {
@@ -235,7 +236,7 @@ void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStrea
   bin_count<<<nblocks, kT, 0, s>>>(off, n, e, cap, counts.p, nblocks, mx.p);
   LVN_LAUNCH();
   exclusive_scan_u64(counts.p, pos.p, ncnt, s);
-  bin_scatter<<<nblocks, kT, 0, s>>>(off, n, e, cap, pos.p, nblocks, out.list.p);
+  bin_scatter<<<nblocks, kT, 0, s>>>(off, n, e, cap, pos.p, nblocks, out.list.p, id_base);
   LVN_LAUNCH();
   gather_starts<<<1, 32, 0, s>>>(pos.p, nblocks, mx.p, small.p);
   LVN_LAUNCH();

@@ -87,6 +87,11 @@ __global__ void iota_k(u32* p, u64 n) {
     p[i] = u32(i);
 }
 
+__global__ void fill_k(u32* p, u64 n, u32 v) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+    p[i] = v;
+}
+
 // ---- segmented sort ----------------------------------------------------------------
 constexpr int kSortThreads = 512;
 constexpr u32 kSmemSortMax = 4096;
@@ -241,6 +246,12 @@ void segmented_sort_u32(u32* keys, float* vals, const u64* off, u32 nseg, u64 ma
 void iota_u32(u32* p, u64 n, cudaStream_t s) {
   if (!n) return;
   iota_k<<<grid_for(n, 256), 256, 0, s>>>(p, n);
+  LVN_LAUNCH();
+}
+
+void fill_u32(u32* p, u64 n, u32 v, cudaStream_t s) {
+  if (!n) return;
+  fill_k<<<grid_for(n, 256), 256, 0, s>>>(p, n, v);
   LVN_LAUNCH();
 }
 

@@ -96,7 +96,7 @@ void init_context(int device) {
   c->sms = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
   LVN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
-  LVN_CUDA(cudaMallocHost(&c->pinned, 512 * sizeof(u64)));
+  LVN_CUDA(cudaMallocHost(&c->pinned, 8192 * sizeof(u64)));
   g_ctx = c;
 }
 
@@ -156,6 +156,7 @@ void validate(const lvn_params& p) {
     fail(kInvalid, "pick-less period must be even and >= 2");
   if (p.value_bits != 32 && p.value_bits != 64) fail(kInvalid, "value_bits must be 32 or 64");
   if (p.probing < 0 || p.probing > 3) fail(kInvalid, "unknown probing mode");
+  if (p.sweep_order != 0 && p.sweep_order != 1) fail(kInvalid, "sweep_order must be 0 or 1");
   if (!(p.bin_thread_max <= p.bin_group_max && p.bin_group_max <= p.bin_warp_max &&
         p.bin_warp_max <= p.bin_block_max))
     fail(kInvalid, "degree bin edges must be non-decreasing");
@@ -289,11 +290,20 @@ struct Timing {
   }
 };
 
+constexpr int kMaxRanges = 64;
+
 struct IterRecord {  // device scratch read back once per iteration
   double gain;
   ull verts, arcs, moves;
-  ull active[kBins];  // per-bin sizes of the next iteration's active lists
+  ull active[kMaxRanges * kBins];  // per-(range, bin) sizes of the next active lists
 };
+
+// vertex-id ranges of one sweep (lvn_params.sweep_ranges)
+int sweep_ranges(const lvn_params& p, u32 nv) {
+  int r = p.sweep_ranges > 0 ? p.sweep_ranges : 1;
+  r = std::min(r, kMaxRanges);
+  return int(std::max<u64>(1, std::min<u64>(u64(r), nv)));
+}
 
 // ---- renumbering: ids of C (all < width) -> 0..count-1 ascending, returns count
 u32 renumber_device(u32* C, u64 n, u64 width, DBuf<u32>& used, DBuf<u32>& rank, cudaStream_t s,
@@ -481,7 +491,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
   const BinEdges edges = edges_of(p);
   Timing tm;
 
-  DBuf<u32> global(N ? N : 1), C(N ? N : 1), used, rank, active;
+  DBuf<u32> global(N ? N : 1), C(N ? N : 1), used, rank, active, csize;
   DBuf<double> K(N ? N : 1), S(N ? N : 1), table;
   DBuf<u8> flags(N ? N : 1);
   DBuf<IterRecord> rec(1);
@@ -523,6 +533,12 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
     a.counters = &rec.p->verts;
     a.err = err.p;
     a.chunk = sweep_chunk(p, nv);
+    a.hubs_first = p.sweep_order == 1;
+    if (p.singleton_rule) {
+      csize.ensure(nv ? nv : 1);
+      fill_u32(csize.p, nv, 1u, s);
+      a.csize = csize.p;
+    }
     if (B.count(kBinGlobal)) {
       int blocks = 0;
       const size_t bytes = move_table_bytes(B.max_degree, p.value_bits, &blocks);
@@ -531,29 +547,46 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
       a.table = table.p;
       a.table_slots = move_table_slots(B.max_degree);
     }
+    // A sweep visits R consecutive vertex-id ranges in order, each with its own
+    // degree bins: within a range the degree classes run low to high (the
+    // reference compact order), across ranges the sweep follows vertex ids
+    // like louvain_mc's, which matters for quality on skewed graphs.
+    const int R = sweep_ranges(p, nv);
+    std::vector<Bins> rbins(R > 1 ? R : 0);
+    std::vector<u64> rbase(R + 1);
+    for (int k = 0; k <= R; ++k) rbase[k] = u64(nv) * k / R;
+    std::vector<BinView> views(R);
+    for (int k = 0; k < R; ++k) {
+      if (R > 1)
+        compute_bins(cur.off + rbase[k], u32(rbase[k + 1] - rbase[k]), edges, rbins[k], s, ~u64(0),
+                     u32(rbase[k]));
+      views[k] = R > 1 ? rbins[k].view() : B.view();
+    }
     const auto t0 = Clock::now();
     int iterations = 0;
     // iteration 0 sweeps every row with arcs (all flagged); later iterations
     // sweep the flagged rows only, compacted right after the previous sweep
-    BinView view = B.view();
     active.ensure(nv ? nv : 1);
     for (int it = 0; it < p.max_iterations; ++it) {
       a.pickless = pick_less_active(it, p.pick_less_period);
       LVN_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(IterRecord), s));
       sp = tm.begin(LVN_STAT_MOVE, s);
-      move_sweep(a, view, p.value_bits, s);
+      for (int k = 0; k < R; ++k) move_sweep(a, views[k], p.value_bits, s);
       tm.end(sp, s, 0.0);
-      if (p.prune) compact_active(B, flags.p, active.p, rec.p->active, s);
+      if (p.prune)
+        for (int k = 0; k < R; ++k)
+          compact_active(R > 1 ? rbins[k] : B, flags.p, active.p + rbase[k], rec.p->active + k * kBins, s);
       IterRecord* h = reinterpret_cast<IterRecord*>(c.pinned);
       LVN_CUDA(cudaMemcpyAsync(h, rec.p, sizeof(IterRecord), cudaMemcpyDeviceToHost, s));
       LVN_CUDA(cudaStreamSynchronize(s));
       tm.set_bytes(sp, 12.0 * double(h->arcs) + 32.0 * double(h->verts), h->verts, h->arcs);
       ++iterations;
       if (h->gain <= tolerance) break;  // louvain_compact.cpp:209
-      if (p.prune) {
-        view.list = active.p;
-        for (int b = 0; b < kBins; ++b) view.cnt[b] = h->active[b];
-      }
+      if (p.prune)
+        for (int k = 0; k < R; ++k) {
+          views[k].list = active.p + rbase[k];
+          for (int b = 0; b < kBins; ++b) views[k].cnt[b] = h->active[k * kBins + b];
+        }
     }
     t_move += since(t0);
     check_err(err.p, s);
@@ -727,6 +760,9 @@ void lvn_params_default(lvn_params* p) {
   p->bin_block_max = 4096;
   p->membership_on_device = 0;
   p->sweep_chunk = 0;
+  p->sweep_order = 0;
+  p->sweep_ranges = 0;
+  p->singleton_rule = 0;
 }
 
 int lvn_init(int num_gpus, const int* devices) {

@@ -62,8 +62,10 @@ struct Bins {
 void compact_active(const Bins& b, const u8* flags, u32* out_list, ull* counts, cudaStream_t s);
 // bin of row v by min(off[v+1]-off[v], cap): rows of a CSR, or community
 // budgets during aggregation. Synchronises (reads the bin sizes).
+// id_base is added to the row index written into the lists (bins of a
+// vertex range: off points at the range's first offset).
 void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStream_t s,
-                  u64 cap = ~u64(0));
+                  u64 cap = ~u64(0), u32 id_base = 0);
 // K_u = row sums (fp64), Sigma = K, C = identity, flags = deg > 0
 void pass_reset(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C, u8* flags,
                 cudaStream_t s);
@@ -89,6 +91,8 @@ struct MoveArgs {
   u64 table_slots = 0;         // slots per block
   u64 chunk = ~u64(0);         // max vertices of one bin decided per launch
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
+  int hubs_first = 0;          // bin order of a sweep: highest degree class first
+  u32* csize = nullptr;        // community member counts (singleton-pair rule), or null
 };
 // one sweep over the bins of `bins` (see the kBin* classes)
 void move_sweep(const MoveArgs& a, const BinView& bins, int value_bits, cudaStream_t s);
@@ -114,6 +118,7 @@ void community_scatter(const u32* C, u32 n, const u64* coff, u32 count, u32* cur
 void segmented_sort_u32(u32* keys, float* vals, const u64* off, u32 nseg, u64 max_seg,
                         cudaStream_t s);
 void iota_u32(u32* p, u64 n, cudaStream_t s);
+void fill_u32(u32* p, u64 n, u32 v, cudaStream_t s);
 
 // ---- aggregate.cu -----------------------------------------------------------
 struct AggArgs {

@@ -107,6 +107,11 @@ __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, doubl
     return false;
   }
   if (mv && x.pickless && bc > from) mv = false;
+  // singleton pairs: two singletons that pick each other would swap labels
+  // instead of merging when they decide concurrently; only the move toward
+  // the lower id is taken, so the pair merges (Pick-Less, restricted to the
+  // one configuration where it is always needed)
+  if (mv && x.csize && bc > from && x.csize[from] == 1 && x.csize[bc] == 1) mv = false;
   if (mv) {
     const double sigma_c = atomicAdd(&x.sigma[bc], ku);
     const double sigma_d = *reinterpret_cast<volatile double*>(&x.sigma[from]);
@@ -114,6 +119,10 @@ __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, doubl
     if (g > 0.0) {
       atomicAdd(&x.sigma[from], -ku);
       x.C[u] = bc;
+      if (x.csize) {
+        atomicSub(&x.csize[from], 1u);
+        atomicAdd(&x.csize[bc], 1u);
+      }
       t.gain += g;
       ++t.moves;
     } else {
@@ -615,35 +624,51 @@ template <class Tab, bool DRY>
 void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
   using V = typename Tab::V;
   const int sms = sm_count();
-  if (b.count(kBinThread)) {
-    auto k = lm_thread<V, DRY>;
-    static const int occ = occupancy(k, 256, 0);
-    launch_chunks(k, a, b.of(kBinThread), b.count(kBinThread), 256, 256, u64(sms) * occ, 0, s);
-  }
-  launch_sort<8, 1, V, DRY>(a, b, kBinSort8, s);
-  launch_sort<16, 1, V, DRY>(a, b, kBinSort16, s);
-  launch_sort<32, 1, V, DRY>(a, b, kBinSort32, s);
-  launch_sort<32, 2, V, DRY>(a, b, kBinSort64, s);
-  if (b.count(kBinWarp)) {
-    constexpr int T = 256;
-    auto k = lm_group<Tab, 32, kWarpCapLog, T, DRY>;
-    constexpr size_t smem = group_smem<Tab, 32, kWarpCapLog, T>();
-    static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
-    launch_chunks(k, a, b.of(kBinWarp), b.count(kBinWarp), T, T / 32, u64(sms) * occ, smem, s);
-  }
-  if (b.count(kBinBlock)) {
-    auto k = lm_block<Tab, false, DRY>;
-    constexpr size_t smem = block_smem<Tab>();
-    static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
-    launch_chunks(k, a, b.of(kBinBlock), b.count(kBinBlock), kBlockThreads, 1, u64(sms) * occ, smem, s);
-  }
-  if (b.count(kBinGlobal)) {
-    if (!a.table || !a.table_slots) fail(kInternal, "global move table not provisioned");
-    int blocks = 0;
-    move_table_bytes(b.max_degree, sizeof(V) == 4 ? 32 : 64, &blocks);
-    launch_chunks(lm_block<Tab, true, DRY>, a, b.of(kBinGlobal), b.count(kBinGlobal), kBlockThreads, 1,
-                  u64(blocks), 0, s);
-  }
+  auto launch_bin = [&](int bin) {
+    if (!b.count(bin)) return;
+    switch (bin) {
+      case kBinThread: {
+        auto k = lm_thread<V, DRY>;
+        static const int occ = occupancy(k, 256, 0);
+        launch_chunks(k, a, b.of(bin), b.count(bin), 256, 256, u64(sms) * occ, 0, s);
+        break;
+      }
+      case kBinSort8: launch_sort<8, 1, V, DRY>(a, b, bin, s); break;
+      case kBinSort16: launch_sort<16, 1, V, DRY>(a, b, bin, s); break;
+      case kBinSort32: launch_sort<32, 1, V, DRY>(a, b, bin, s); break;
+      case kBinSort64: launch_sort<32, 2, V, DRY>(a, b, bin, s); break;
+      case kBinWarp: {
+        constexpr int T = 256;
+        auto k = lm_group<Tab, 32, kWarpCapLog, T, DRY>;
+        constexpr size_t smem = group_smem<Tab, 32, kWarpCapLog, T>();
+        static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
+        launch_chunks(k, a, b.of(bin), b.count(bin), T, T / 32, u64(sms) * occ, smem, s);
+        break;
+      }
+      case kBinBlock: {
+        auto k = lm_block<Tab, false, DRY>;
+        constexpr size_t smem = block_smem<Tab>();
+        static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
+        launch_chunks(k, a, b.of(bin), b.count(bin), kBlockThreads, 1, u64(sms) * occ, smem, s);
+        break;
+      }
+      case kBinGlobal: {
+        if (!a.table || !a.table_slots) fail(kInternal, "global move table not provisioned");
+        int blocks = 0;
+        move_table_bytes(b.max_degree, sizeof(V) == 4 ? 32 : 64, &blocks);
+        launch_chunks(lm_block<Tab, true, DRY>, a, b.of(bin), b.count(bin), kBlockThreads, 1, u64(blocks), 0, s);
+        break;
+      }
+      default: break;
+    }
+  };
+  // hubs first: the highest-degree vertices settle before the rows that follow
+  // them (on power-law graphs this is what a sequential id-order sweep does,
+  // since hubs carry low ids); the reference compact engine sweeps low degree first
+  if (a.hubs_first)
+    for (int bin = kBinGlobal; bin >= kBinThread; --bin) launch_bin(bin);
+  else
+    for (int bin = kBinThread; bin <= kBinGlobal; ++bin) launch_bin(bin);
 }
 
 }  // namespace

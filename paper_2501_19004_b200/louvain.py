@@ -124,6 +124,9 @@ class CompactOptions:  # louvain_compact.hpp:35-40
     value_bits: int = 32
     bins: DeviceBins = field(default_factory=DeviceBins)
     sweep_chunk: int = 0  # vertices per launch of a sweep; 0 automatic, 2**32-1 unbounded
+    sweep_order: int = 0  # 0 low degree first (reference compact order), 1 hubs first
+    sweep_ranges: int = 0  # vertex-id ranges per sweep (1 = compact order); 0 automatic
+    singleton_rule: bool = False  # singleton joins singleton only toward the lower id
 
 
 @dataclass
@@ -304,6 +307,9 @@ def _params(params: LouvainParams | None, options: CompactOptions | None, on_dev
     p.bin_block_max = options.bins.block_max
     p.membership_on_device = int(on_device)
     p.sweep_chunk = options.sweep_chunk
+    p.sweep_order = options.sweep_order
+    p.sweep_ranges = options.sweep_ranges
+    p.singleton_rule = int(bool(options.singleton_rule))
     return p
 
 
