@@ -384,14 +384,11 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
             if (r & j) continue;
             const int r2 = r | j;
             const bool asc = ((lane * K + r) & size) == 0;
-            if ((key[r] > key[r2]) == asc) {
-              const u32 tk = key[r];
-              key[r] = key[r2];
-              key[r2] = tk;
-              const V tv = val[r];
-              val[r] = val[r2];
-              val[r2] = tv;
-            }
+            const u32 lo_k = asc ? min(key[r], key[r2]) : max(key[r], key[r2]);
+            const u32 hi_k = asc ? max(key[r], key[r2]) : min(key[r], key[r2]);
+            const bool sw = lo_k != key[r];  // branch-free exchange
+            const V v1 = sw ? val[r2] : val[r], v2 = sw ? val[r] : val[r2];
+            key[r] = lo_k, key[r2] = hi_k, val[r] = v1, val[r2] = v2;
           }
         } else {
           const int lj = j / K;
@@ -399,9 +396,11 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
           for (int r = 0; r < K; ++r) {
             const u32 pk = __shfl_xor_sync(FULL, key[r], lj, G);
             const V pv = __shfl_xor_sync(FULL, val[r], lj, G);
-            const bool asc = ((lane * K + r) & size) == 0;
-            const bool lower = (lane & lj) == 0;
-            if (lower == asc ? pk < key[r] : pk > key[r]) key[r] = pk, val[r] = pv;
+            // keep the smaller key when (lower lane, ascending) or (upper, descending)
+            const bool keep_min = (((lane & lj) == 0) == (((lane * K + r) & size) == 0));
+            const u32 nk = keep_min ? min(key[r], pk) : max(key[r], pk);
+            val[r] = nk != key[r] ? pv : val[r];
+            key[r] = nk;
           }
         }
       }
