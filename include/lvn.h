@@ -91,7 +91,7 @@ typedef struct lvn_params {
   /* device degree bins: thread <= bin_thread_max < group8 <= bin_group_max
    * < warp <= bin_warp_max < block <= bin_block_max < global-table block */
   uint32_t bin_thread_max;      /* 4 */
-  uint32_t bin_group_max;       /* 64 */
+  uint32_t bin_group_max;       /* 256: rows up to this degree use the register-sort kernels */
   uint32_t bin_warp_max;        /* 256 */
   uint32_t bin_block_max;       /* 4096 */
   int membership_on_device;     /* result membership stays in device memory */

@@ -11,13 +11,17 @@
 // intra-community weight (key == c, the super-vertex self-loop) is kept
 // privately per lane and reduced once: it is the dominant, most contended key.
 //
-// Binned by total member degree: bins 1-2 -> 8-lane groups, 3 -> warp,
-// 4-5 -> block (table in smem when it fits, else in global memory).
+// Binned by total member degree (the community's budget): budgets <= 256 use
+// the register-sort kernels (ag_sort: the member arcs' (C[t], w) pairs are
+// sorted by target community across a lane group and reduced per run, which
+// also emits each row already in canonical target order); larger budgets use
+// smem/global hash tables (warp: ag_group, block: ag_block).
 // Bytes: 12 B x A_in + 16 B x V_in + 8 B x A_out + 8 B x (count+1).
 #include <cooperative_groups.h>
 #include <cooperative_groups/reduce.h>
 
 #include "kernels.cuh"
+#include "sortnet.cuh"
 #include "tables.cuh"
 
 namespace cg = cooperative_groups;
@@ -25,11 +29,69 @@ namespace cg = cooperative_groups;
 namespace lvn {
 namespace {
 
-constexpr int kGroupCapLog = 7;
 constexpr int kWarpCapLog = 9;
 constexpr int kBlockCapLog = 13;
 constexpr int kBlockThreads = 512;
 using Tab = SplitF64;
+
+// Communities with budget <= N = G*K: element e = r*G + lane of the
+// community's member arcs (members in CSR order) is loaded into register r.
+template <int G, int K>
+__global__ void __launch_bounds__(256) ag_sort(AggArgs x, const u32* __restrict__ list, u64 count) {
+  constexpr int GPB = 256 / G;
+  const u32 lane = threadIdx.x & (G - 1);
+  const u32 gi = threadIdx.x / G;
+  for (u64 i0 = u64(blockIdx.x) * GPB; i0 < count; i0 += u64(gridDim.x) * GPB) {
+    const u64 i = i0 + gi;
+    const bool have = i < count;
+    const u32 c = have ? list[i] : 0;
+    u32 key[K];
+    double val[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) key[r] = kEmpty, val[r] = 0.0;
+    u64 mlo = 0, mhi = 0;
+    if (have) mlo = x.coff[c], mhi = x.coff[c + 1];
+    u64 base = 0;
+    for (u64 k = mlo; k < mhi; ++k) {
+      const u32 v = x.members[k];
+      const u64 lo = x.g.off[v], d = x.g.off[v + 1] - lo;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const u64 e = u64(r) * G + lane;
+        if (e >= base && e < base + d) {
+          const u64 a = lo + (e - base);
+          key[r] = x.C[__ldcs(x.g.tgt + a)];
+          val[r] = double(__ldcs(x.g.w + a));
+        }
+      }
+      base += d;
+    }
+    bitonic_sort<G, K, double>(key, val, lane);
+    bool tail[K];
+    segmented_runs<G, K, double>(key, val, tail, lane);
+    u32 mine = 0;
+#pragma unroll
+    for (int r = 0; r < K; ++r) mine += (tail[r] && key[r] != kEmpty) ? 1u : 0u;
+    u32 total;
+    u32 pos = group_exclusive<G>(mine, lane, total);
+    if (have) {
+      const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
+      if (total > hcap) {
+        if (lane == 0) atomicOr(x.err, u32(kErrTable));
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          if (tail[r] && key[r] != kEmpty) {
+            x.htgt[hbase + pos] = key[r];
+            x.hw[hbase + pos] = float(val[r]);  // fp64 sum narrowed once
+            ++pos;
+          }
+        }
+        if (lane == 0) x.fill[c] = total;
+      }
+    }
+  }
+}
 
 // merge one member's arcs into the table
 __device__ __forceinline__ void merge_row(const AggArgs& x, const Tab& tab, u32 lg, u32 c, u32 v,
@@ -214,18 +276,24 @@ size_t aggregate_table_bytes(u64 max_slots, int* blocks) {
 
 void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
   const int sms = sm_count();
-  if (b.edges.group_max > 64 || b.edges.warp_max > 256 || b.edges.block_max > 4096)
+  if (b.edges.thread_max > 8 || b.edges.group_max > 256 || b.edges.warp_max > 256 ||
+      b.edges.block_max > 4096)
     fail(kInvalid, "aggregation bin edges exceed the device table capacities");
-  const u64 small = b.start[kBinWarp] - b.start[kBinThread];  // budgets <= group_max (<= 64)
-  if (small) {
-    constexpr int T = 256;
-    auto k = ag_group<8, kGroupCapLog, T>;
-    const size_t smem = size_t(T / 8) * (1u << kGroupCapLog) * Tab::kSlotBytes;
-    static const int occ = occupancy(k, T, smem);
-    const u64 blocks = std::min<u64>((small + T / 8 - 1) / (T / 8), u64(sms) * occ);
-    k<<<unsigned(blocks), T, smem, s>>>(a, b.of(kBinThread), small);
+  // budgets <= 256: register sort, N = G*K elements per community
+  auto sort_bin = [&](int bin, auto kernel, int G) {
+    if (!b.count(bin)) return;
+    const int occ = occupancy(kernel, 256, 0);
+    const u64 blocks = std::min<u64>((b.count(bin) + 256 / G - 1) / (256 / G), u64(sms) * occ);
+    kernel<<<unsigned(blocks), 256, 0, s>>>(a, b.of(bin), b.count(bin));
     LVN_LAUNCH();
-  }
+  };
+  sort_bin(kBinThread, ag_sort<8, 1>, 8);
+  sort_bin(kBinSort8, ag_sort<8, 1>, 8);
+  sort_bin(kBinSort16, ag_sort<16, 1>, 16);
+  sort_bin(kBinSort32, ag_sort<32, 1>, 32);
+  sort_bin(kBinSort64, ag_sort<32, 2>, 32);
+  sort_bin(kBinSort128, ag_sort<32, 4>, 32);
+  sort_bin(kBinSort256, ag_sort<32, 8>, 32);
   if (b.count(kBinWarp)) {
     constexpr int T = 256;
     auto k = ag_group<32, kWarpCapLog, T>;

@@ -21,7 +21,9 @@ __device__ __forceinline__ int bin_of(u64 deg, const BinEdges& e) {
     if (deg <= 8) return kBinSort8;
     if (deg <= 16) return kBinSort16;
     if (deg <= 32) return kBinSort32;
-    return kBinSort64;
+    if (deg <= 64) return kBinSort64;
+    if (deg <= 128) return kBinSort128;
+    return kBinSort256;
   }
   if (deg <= e.warp_max) return kBinWarp;
   if (deg <= e.block_max) return kBinBlock;
@@ -170,11 +172,14 @@ void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C
   if (g.n == 0) return;
   const int sms = sm_count();
   const u64 tb = std::min<u64>((g.n + 255) / 256, u64(sms) * 16);
-  reset_thread<<<unsigned(tb), 256, 0, s>>>(g, b.edges.group_max, K, sigma, C, flags);
+  // rows of <= 32 arcs: one thread, sequential sum (the reference's order)
+  reset_thread<<<unsigned(tb), 256, 0, s>>>(g, 32u, K, sigma, C, flags);
   LVN_LAUNCH();
-  if (b.count(kBinWarp)) {
-    const u64 wb = std::min<u64>((b.count(kBinWarp) + 7) / 8, u64(sms) * 16);
-    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinWarp), b.count(kBinWarp), K, sigma);
+  // 32 < deg <= warp_max (plus any short rows binned there): one warp per row
+  const u64 mid = b.start[kBinBlock] - b.start[kBinSort64];
+  if (mid) {
+    const u64 wb = std::min<u64>((mid + 7) / 8, u64(sms) * 16);
+    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinSort64), mid, K, sigma);
     LVN_LAUNCH();
   }
   const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);

@@ -160,9 +160,9 @@ void validate(const lvn_params& p) {
   if (!(p.bin_thread_max <= p.bin_group_max && p.bin_group_max <= p.bin_warp_max &&
         p.bin_warp_max <= p.bin_block_max))
     fail(kInvalid, "degree bin edges must be non-decreasing");
-  if (p.bin_thread_max > 8 || p.bin_group_max > 64 || p.bin_warp_max > 256 ||
+  if (p.bin_thread_max > 8 || p.bin_group_max > 256 || p.bin_warp_max > 256 ||
       p.bin_block_max > 4096)
-    fail(kInvalid, "degree bin edges exceed the device table capacities (8/64/256/4096)");
+    fail(kInvalid, "degree bin edges exceed the device kernel capacities (8/256/256/4096)");
 }
 
 // pick_less_active (louvain_compact.hpp:22-24)
@@ -755,7 +755,7 @@ void lvn_params_default(lvn_params* p) {
   p->probing = LVN_QUADRATIC_DOUBLE;
   p->value_bits = 32;
   p->bin_thread_max = 4;
-  p->bin_group_max = 64;
+  p->bin_group_max = 256;
   p->bin_warp_max = 256;
   p->bin_block_max = 4096;
   p->membership_on_device = 0;

@@ -16,19 +16,21 @@ void reduce_max_u32(const u32* in, u64 n, u32* out, cudaStream_t s);
 // ---- bins.cu: degree bins + pass reset ------------------------------------
 // Degree classes (the kernel that handles a row / community):
 enum : int {
-  kBinIso = 0,     // no arcs
-  kBinThread = 1,  // deg <= thread_max: thread per vertex, registers
-  kBinSort8 = 2,   // deg <= 8 (and <= group_max): 8 lanes, register bitonic sort
-  kBinSort16 = 3,  // deg <= 16
-  kBinSort32 = 4,  // deg <= 32
-  kBinSort64 = 5,  // deg <= 64: 32 lanes x 2 registers
-  kBinWarp = 6,    // deg <= warp_max: warp, smem hash table
-  kBinBlock = 7,   // deg <= block_max: block, smem hash table
-  kBinGlobal = 8,  // larger: block, global-memory hash table
-  kBins = 9
+  kBinIso = 0,      // no arcs
+  kBinThread = 1,   // deg <= thread_max: thread per vertex, registers
+  kBinSort8 = 2,    // deg <= 8 (and <= group_max): 8 lanes, register bitonic sort
+  kBinSort16 = 3,   // deg <= 16: 16 lanes
+  kBinSort32 = 4,   // deg <= 32: 32 lanes
+  kBinSort64 = 5,   // deg <= 64: 32 lanes x 2 registers
+  kBinSort128 = 6,  // deg <= 128: 32 lanes x 4 registers
+  kBinSort256 = 7,  // deg <= 256: 32 lanes x 8 registers
+  kBinWarp = 8,     // deg <= warp_max: warp, smem hash table
+  kBinBlock = 9,    // deg <= block_max: block, smem hash table
+  kBinGlobal = 10,  // larger: block, global-memory hash table
+  kBins = 11
 };
 struct BinEdges {
-  u32 thread_max = 4, group_max = 64, warp_max = 256, block_max = 4096;
+  u32 thread_max = 4, group_max = 256, warp_max = 256, block_max = 4096;
 };
 // A set of per-bin vertex lists (the full bins, or the active subset of an iteration)
 struct BinView {

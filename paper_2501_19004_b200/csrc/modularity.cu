@@ -110,15 +110,16 @@ void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot,
   LVN_CUDA(cudaMemsetAsync(tot, 0, width * sizeof(double), s));
   LVN_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), s));
   const int sms = sm_count();
-  const u64 small = b.start[kBinWarp] - b.start[kBinIso];  // rows of <= 64 arcs
+  const u64 small = b.start[kBinSort64] - b.start[kBinIso];  // rows of <= 32 arcs
   if (small) {
     const u64 blocks = std::min<u64>((small + 255) / 256, u64(sms) * 8);
     mod_thread<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinIso), small, C, tot, sums);
     LVN_LAUNCH();
   }
-  if (b.count(kBinWarp)) {
-    const u64 blocks = std::min<u64>((b.count(kBinWarp) + 7) / 8, u64(sms) * 8);
-    mod_warp<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinWarp), b.count(kBinWarp), C, tot, sums);
+  const u64 mid = b.start[kBinBlock] - b.start[kBinSort64];
+  if (mid) {
+    const u64 blocks = std::min<u64>((mid + 7) / 8, u64(sms) * 8);
+    mod_warp<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinSort64), mid, C, tot, sums);
     LVN_LAUNCH();
   }
   const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);

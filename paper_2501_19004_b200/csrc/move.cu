@@ -37,6 +37,7 @@
 #include <cmath>
 
 #include "kernels.cuh"
+#include "sortnet.cuh"
 #include "tables.cuh"
 
 namespace cg = cooperative_groups;
@@ -45,7 +46,6 @@ namespace lvn {
 namespace {
 
 constexpr int kThreadMaxD = 8;
-constexpr int kGroupCapLog = 7;    // 128 slots (group_max <= 64)
 constexpr int kWarpCapLog = 9;     // 512 slots (warp_max <= 256)
 constexpr int kBlockCapLog = 13;   // 8192 slots (block_max <= 4096)
 constexpr int kBlockThreads = 512;
@@ -341,7 +341,6 @@ __global__ void __launch_bounds__(THREADS, 4) lm_group(MoveArgs x, const u32* __
 template <int G, int K, class V, bool DRY>
 __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict__ list, u64 count) {
   constexpr int GPB = 256 / G;
-  constexpr int N = G * K;
   constexpr u32 FULL = 0xffffffffu;
   const u32 lane = threadIdx.x & (G - 1);
   const u32 gi = threadIdx.x / G;
@@ -373,78 +372,20 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
 #pragma unroll
     for (int r = 0; r < K; ++r) key[r] = (t[r] != kEmpty && t[r] != u) ? x.C[t[r]] : kEmpty;
 
-    // bitonic sort, ascending by key (padding and self-loops carry kEmpty and sort last)
-#pragma unroll
-    for (int size = 2; size <= N; size <<= 1) {
-#pragma unroll
-      for (int j = size >> 1; j > 0; j >>= 1) {
-        if (j < K) {
-#pragma unroll
-          for (int r = 0; r < K; ++r) {
-            if (r & j) continue;
-            const int r2 = r | j;
-            const bool asc = ((lane * K + r) & size) == 0;
-            const u32 lo_k = asc ? min(key[r], key[r2]) : max(key[r], key[r2]);
-            const u32 hi_k = asc ? max(key[r], key[r2]) : min(key[r], key[r2]);
-            const bool sw = lo_k != key[r];  // branch-free exchange
-            const V v1 = sw ? val[r2] : val[r], v2 = sw ? val[r] : val[r2];
-            key[r] = lo_k, key[r2] = hi_k, val[r] = v1, val[r2] = v2;
-          }
-        } else {
-          const int lj = j / K;
-#pragma unroll
-          for (int r = 0; r < K; ++r) {
-            const u32 pk = __shfl_xor_sync(FULL, key[r], lj, G);
-            const V pv = __shfl_xor_sync(FULL, val[r], lj, G);
-            // keep the smaller key when (lower lane, ascending) or (upper, descending)
-            const bool keep_min = (((lane & lj) == 0) == (((lane * K + r) & size) == 0));
-            const u32 nk = keep_min ? min(key[r], pk) : max(key[r], pk);
-            val[r] = nk != key[r] ? pv : val[r];
-            key[r] = nk;
-          }
-        }
-      }
-    }
-
-    // run heads, in-lane segmented sums, then the carry of the run entering the lane
-    const u32 prev_last = __shfl_up_sync(FULL, key[K - 1], 1, G);
-    bool head[K];
-    V run[K];
-    bool lane_head = false;
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
-      head[r] = r == 0 ? (lane == 0 || key[0] != prev_last) : key[r] != key[r - 1];
-      run[r] = (r == 0 || head[r]) ? val[r] : run[r - 1] + val[r];
-      lane_head = lane_head || head[r];
-    }
-    V agg = run[K - 1];
-    int f = lane_head;
-#pragma unroll
-    for (int d = 1; d < G; d <<= 1) {
-      const V pa = __shfl_up_sync(FULL, agg, d, G);
-      const int pf = __shfl_up_sync(FULL, f, d, G);
-      if (lane >= u32(d)) {
-        if (!f) agg = pa + agg;
-        f = f | pf;
-      }
-    }
-    const V carry_in = __shfl_up_sync(FULL, agg, 1, G);
-    bool open = lane != 0;
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
-      open = open && !head[r];
-      if (open) run[r] += carry_in;
-    }
-    const int next_head = __shfl_down_sync(FULL, int(head[0]), 1, G);
+    // sort by community (padding and self-loops carry kEmpty and sort last),
+    // then K_{u->c} lands on the last element of each community's run
+    bitonic_sort<G, K, V>(key, val, lane);
+    bool tail[K];
+    segmented_runs<G, K, V>(key, val, tail, lane);
+    const V (&run)[K] = val;
 
     // own community weight and the best other community
     V own_l = V(0);
     bool cand[K];
 #pragma unroll
     for (int r = 0; r < K; ++r) {
-      const bool tail = r + 1 < K ? head[r + 1] : (lane == G - 1 || next_head);
-      if (tail && key[r] == from) own_l = run[r];
-      cand[r] = tail && key[r] != kEmpty && key[r] != from;
+      if (tail[r] && key[r] == from) own_l = run[r];
+      cand[r] = tail[r] && key[r] != kEmpty && key[r] != from;
     }
     V own = own_l;
 #pragma unroll
@@ -636,6 +577,8 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
       case kBinSort16: launch_sort<16, 1, V, DRY>(a, b, bin, s); break;
       case kBinSort32: launch_sort<32, 1, V, DRY>(a, b, bin, s); break;
       case kBinSort64: launch_sort<32, 2, V, DRY>(a, b, bin, s); break;
+      case kBinSort128: launch_sort<32, 4, V, DRY>(a, b, bin, s); break;
+      case kBinSort256: launch_sort<32, 8, V, DRY>(a, b, bin, s); break;
       case kBinWarp: {
         constexpr int T = 256;
         auto k = lm_group<Tab, 32, kWarpCapLog, T, DRY>;
@@ -702,7 +645,7 @@ void move_table_init(void* table, u64 max_degree, int value_bits, cudaStream_t s
 }
 
 void move_sweep(const MoveArgs& a0, const BinView& b, int value_bits, cudaStream_t s) {
-  if (b.edges.thread_max > kThreadMaxD || b.edges.group_max > (1u << (kGroupCapLog - 1)) ||
+  if (b.edges.thread_max > kThreadMaxD || b.edges.group_max > 256 ||
       b.edges.warp_max > (1u << (kWarpCapLog - 1)) ||
       b.edges.block_max > (1u << (kBlockCapLog - 1)))
     fail(kInvalid, "degree bin edges exceed the device table capacities");

@@ -111,7 +111,7 @@ class DeviceBins:
     block-with-smem-table / block-with-global-table)."""
 
     thread_max: int = 4
-    group_max: int = 64
+    group_max: int = 256
     warp_max: int = 256
     block_max: int = 4096
 

@@ -9,4 +9,5 @@ c = CONFIGS[cfg]
 dg = lvn.generate(c["kind"], **{k: v for k, v in c.items() if k not in ("kind", "desc")})
 for i in range(runs):
     r = lvn.louvain_compact(dg, membership_on_device=True)
-    print(cfg, r.modularity, r.passes, r.iterations_per_pass, {k: round(s.seconds * 1e3, 2) for k, s in r.stats.items()}, flush=True)
+    print(cfg, round(r.modularity, 5), r.passes, r.iterations_per_pass, "V", r.vertices_per_pass, "A", r.arcs_per_pass,
+          {k: round(s.seconds * 1e3, 2) for k, s in r.stats.items()}, "pass_ms", [round(x * 1e3, 1) for x in r.pass_seconds], flush=True)
