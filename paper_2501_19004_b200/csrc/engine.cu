@@ -319,6 +319,15 @@ u32 renumber_device(u32* C, u64 n, u64 width, DBuf<u32>& used, DBuf<u32>& rank, 
 
 bool check_mode();
 
+// LVN_VERBOSE=1: per-iteration trace on stderr (tuning aid)
+bool verbose() {
+  static const bool on = [] {
+    const char* e = std::getenv("LVN_VERBOSE");
+    return e && *e && *e != '0';
+  }();
+  return on;
+}
+
 // ---- aggregation of a graph by a contiguous membership ----------------------
 void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
                       u32* err, cudaStream_t s, bool canonical) {
@@ -580,6 +589,10 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
       LVN_CUDA(cudaMemcpyAsync(h, rec.p, sizeof(IterRecord), cudaMemcpyDeviceToHost, s));
       LVN_CUDA(cudaStreamSynchronize(s));
       tm.set_bytes(sp, 12.0 * double(h->arcs) + 32.0 * double(h->verts), h->verts, h->arcs);
+      if (verbose())
+        std::fprintf(stderr, "[lvn] pass %d it %d: %llu vertices, %llu arcs, %llu moves, gain %.6g\n", pass, it,
+                     (unsigned long long)h->verts, (unsigned long long)h->arcs, (unsigned long long)h->moves,
+                     h->gain);
       ++iterations;
       if (h->gain <= tolerance) break;  // louvain_compact.cpp:209
       if (p.prune)
