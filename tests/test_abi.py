@@ -92,3 +92,47 @@ def test_no_gpu_means_loud_failure():
         lvn.modularity(g, [0, 1])
     with pytest.raises(lvn.CudaError):
         lvn.louvain_compact(g)
+
+
+def test_cpp_facade_builds_against_reference_headers():
+    """include/louvain_gpu.hpp compiles with the reference's own headers and
+    links against liblvn.so; without a GPU the call fails loudly (LVN_CUDA ->
+    std::runtime_error), never falling back to a CPU path."""
+    import subprocess
+    import tempfile
+
+    import torch
+
+    ref_inc = "/root/reference/proj/core/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("reference headers absent (GPU box)")
+    prog = r'''
+#include <cstdio>
+#include "louvain/graph.hpp"
+#include "louvain_gpu.hpp"
+int main() {
+  louvain::CsrGraph g;
+  g.offsets = {0, 1, 2};
+  g.targets = {1, 0};
+  g.weights = {1.0f, 1.0f};
+  g.total_weight = 1.0;
+  try {
+    const auto r = louvain::louvain_gpu(g);
+    std::printf("ok %u %.6f\n", r.num_communities, r.modularity);
+  } catch (const std::runtime_error& e) {
+    std::printf("runtime_error %s\n", e.what());
+  }
+  return 0;
+}'''
+    lib = os.path.join(ROOT, "paper_2501_19004_b200", "lib")
+    with tempfile.TemporaryDirectory() as d:
+        src = os.path.join(d, "facade.cpp")
+        open(src, "w").write(prog)
+        exe = os.path.join(d, "facade")
+        subprocess.run(["/usr/bin/g++", "-std=c++20", "-I", ref_inc, "-I", os.path.join(ROOT, "include"), src,
+                        "-L", lib, "-llvn", f"-Wl,-rpath,{lib}", "-o", exe], check=True)
+        out = subprocess.run([exe], check=True, capture_output=True, text=True).stdout
+    if torch.cuda.is_available():
+        assert out.startswith("ok 1"), out
+    else:
+        assert out.startswith("runtime_error"), out
