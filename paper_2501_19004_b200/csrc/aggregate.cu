@@ -15,7 +15,8 @@
 // the register-sort kernels (ag_sort: the member arcs' (C[t], w) pairs are
 // sorted by target community across a lane group and reduced per run, which
 // also emits each row already in canonical target order); larger budgets use
-// smem/global hash tables (warp: ag_group, block: ag_block).
+// smem hash tables (warp: ag_group, block: ag_block) and, beyond block_max,
+// per-community HBM tables filled arc-parallel (ag_big_*).
 // Bytes: 12 B x A_in + 16 B x V_in + 8 B x A_out + 8 B x (count+1).
 #include <cooperative_groups.h>
 #include <cooperative_groups/reduce.h>
@@ -165,7 +166,6 @@ __global__ void __launch_bounds__(THREADS) ag_group(AggArgs x, const u32* __rest
   }
 }
 
-template <bool GLOBAL>
 __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32 c, u32 lg, double* red,
                              u32* red_seen, u32* cursor) {
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
@@ -226,13 +226,171 @@ __global__ void __launch_bounds__(kBlockThreads) ag_block(AggArgs x, const u32* 
     const u32 c = list[i];
     const u64 hcap = x.hoff[c + 1] - x.hoff[c];
     const u32 lg = table_log(hcap, 5);
-    if (lg <= u32(kBlockCapLog)) {
-      ag_block_one<false>(x, stab, c, lg, red, red_seen, &cursor);
-    } else if (!x.table || (u64(1) << lg) > x.table_slots) {
+    if (lg > u32(kBlockCapLog)) {  // the Block bin has budgets <= 4096
       if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
-    } else {
-      const Tab gtab(x.table + blockIdx.x * x.table_slots * Tab::kSlotBytes / 8, x.table_slots);
-      ag_block_one<true>(x, gtab, c, lg, red, red_seen, &cursor);
+      continue;
+    }
+    ag_block_one(x, stab, c, lg, red, red_seen, &cursor);
+  }
+}
+
+// ---- communities with budget > block_max: arc-parallel ---------------------------
+// The members of the big communities (grouped by community, vertices without
+// arcs dropped) form a list L whose arcs are cut into fixed chunks of kBigChunk
+// arcs, one chunk per warp task: a hub row is split across many warps and the
+// warps of one community run together, so its HBM table stays hot in L2. Every
+// arc merges into its community's table (claim by CAS, fp64 reductions, a
+// live-slot list); the weight to the community itself (the super-vertex
+// self-loop, usually the dominant key) is summed per lane while the lane stays
+// in one community and added once per run. Then one block per community emits
+// the row.
+constexpr u64 kBigChunk = 1024;
+
+__device__ __forceinline__ u64 big_slots(u64 hcap) {
+  const u32 l = ceil_log2_u64(2 * (hcap ? hcap : 1));
+  return u64(1) << (l > 5 ? l : 5);
+}
+__device__ __forceinline__ u64 big_region_bytes(u64 slots) {
+  return (slots * Tab::kSlotBytes + slots / 2 * 4 + 15) & ~u64(15);
+}
+// largest i in [0, n) with p[i] <= x (p ascending, p[0] <= x)
+__device__ __forceinline__ u64 last_le(const u64* __restrict__ p, u64 n, u64 x) {
+  u64 lo = 0, hi = n;
+  while (hi - lo > 1) {
+    const u64 mid = (lo + hi) >> 1;
+    if (p[mid] <= x) lo = mid; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void ag_big_plan(const u32* __restrict__ big, u64 nbig, const u64* __restrict__ hoff,
+                            const u64* __restrict__ coff, u32* __restrict__ index, u64* __restrict__ bytes,
+                            u32* __restrict__ mcount) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < nbig; i += u64(gridDim.x) * blockDim.x) {
+    const u32 c = big[i];
+    index[c] = u32(i);
+    bytes[i] = big_region_bytes(big_slots(hoff[c + 1] - hoff[c]));
+    mcount[i] = u32(coff[c + 1] - coff[c]);
+  }
+}
+
+__global__ void ag_big_clear(const u32* __restrict__ big, u64 nbig, const u64* __restrict__ hoff,
+                             const u64* __restrict__ tab_off, unsigned char* tables) {
+  for (u64 i = blockIdx.x; i < nbig; i += gridDim.x) {
+    const u32 c = big[i];
+    const u64 slots = big_slots(hoff[c + 1] - hoff[c]);
+    const Tab tab(tables + tab_off[i], slots);
+    for (u64 s = threadIdx.x; s < slots; s += blockDim.x) tab.clear(u32(s));
+  }
+}
+
+// j-th member of the big communities (j < M): vertex and whether it has arcs
+__global__ void ag_big_keep(AggArgs x, const u32* __restrict__ big, u64 nbig, const u64* __restrict__ moff,
+                            u64 M, u32* __restrict__ vert, u32* __restrict__ keep) {
+  for (u64 j = blockIdx.x * u64(blockDim.x) + threadIdx.x; j < M; j += u64(gridDim.x) * blockDim.x) {
+    const u64 pi = last_le(moff, nbig, j);
+    const u32 v = x.members[x.coff[big[pi]] + (j - moff[pi])];
+    vert[j] = v;
+    keep[j] = x.g.off[v + 1] > x.g.off[v] ? 1u : 0u;
+  }
+}
+
+__global__ void ag_big_list(const DGraph g, const u32* __restrict__ vert, const u32* __restrict__ keep,
+                            const u32* __restrict__ kpos, u64 M, u32* __restrict__ L, u32* __restrict__ D) {
+  for (u64 j = blockIdx.x * u64(blockDim.x) + threadIdx.x; j < M; j += u64(gridDim.x) * blockDim.x) {
+    if (!keep[j]) continue;
+    const u32 v = vert[j];
+    L[kpos[j]] = v;
+    D[kpos[j]] = u32(g.off[v + 1] - g.off[v]);
+  }
+}
+
+// P: exclusive scan of the arc counts of L (nL + 1 entries, P[nL] = all arcs)
+__global__ void __launch_bounds__(256) ag_big_arcs(AggArgs x, const u32* __restrict__ index,
+                                                   const u64* __restrict__ tab_off, unsigned char* tables,
+                                                   u32* __restrict__ live_n, double* __restrict__ own_sum,
+                                                   u32* __restrict__ own_seen, const u32* __restrict__ L,
+                                                   const u64* __restrict__ P, const u32* __restrict__ nL_p) {
+  const u32 lane = threadIdx.x & 31;
+  const u64 nL = *nL_p;
+  if (!nL) return;
+  const u64 E = P[nL];
+  const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
+  for (u64 w = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; w * kBigChunk < E; w += warps) {
+    const u64 lo = w * kBigChunk, hi = min(E, lo + kBigChunk);
+    u64 i0 = last_le(P, nL, lo);  // owner of the chunk's first arc (every vertex of L has arcs)
+    u32 own_pi = ~0u, seen = 0;
+    double own = 0.0;
+    for (u64 b = lo; b < hi; b += 32) {
+      // the batch's <= 32 arcs span <= 32 consecutive L entries from i0:
+      // a 5-step shuffle search over their ends finds each lane's owner
+      const u64 wend = (i0 + lane + 1 <= nL) ? P[i0 + lane + 1] : ~u64(0);
+      const u64 a = b + lane;
+      u32 k = 0;
+#pragma unroll
+      for (u32 step = 16; step; step >>= 1) {
+        const u64 e = __shfl_sync(0xffffffffu, wend, k + step - 1);
+        if (e <= a) k += step;
+      }
+      const u64 owner = i0 + k;
+      i0 += __shfl_sync(0xffffffffu, k, 31);
+      if (a >= hi) continue;
+      const u32 v = L[owner];
+      const u32 c = x.C[v];
+      const u32 pi = index[c];
+      const u64 ga = x.g.off[v] + (a - P[owner]);
+      const u32 key = x.C[__ldcs(x.g.tgt + ga)];
+      const double wt = double(__ldcs(x.g.w + ga));
+      if (key == c) {
+        if (pi != own_pi) {
+          if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
+          own_pi = pi, own = 0.0;
+        }
+        own += wt;
+        seen = 1;
+        continue;
+      }
+      const u64 slots = big_slots(x.hoff[c + 1] - x.hoff[c]);
+      unsigned char* base = tables + tab_off[pi];
+      const Tab tab(base, slots);
+      const int s = tab.insert(ceil_log2_u64(slots), key, wt);
+      if (s >= 0) reinterpret_cast<u32*>(base + slots * Tab::kSlotBytes)[atomicAdd(&live_n[pi], 1u)] = u32(s);
+    }
+    if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
+  }
+}
+
+__global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, const u32* __restrict__ big, u64 nbig,
+                                                             const u64* __restrict__ tab_off,
+                                                             unsigned char* tables, const u32* __restrict__ live_n,
+                                                             const double* __restrict__ own_sum,
+                                                             const u32* __restrict__ own_seen) {
+  for (u64 i = blockIdx.x; i < nbig; i += gridDim.x) {
+    const u32 c = big[i];
+    const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
+    const u64 slots = big_slots(hcap);
+    unsigned char* base = tables + tab_off[i];
+    const Tab tab(base, slots);
+    const u32* live = reinterpret_cast<const u32*>(base + slots * Tab::kSlotBytes);
+    const u32 n = live_n[i];
+    const u32 self = own_seen[i] ? 1u : 0u;
+    if (n + self > hcap) {
+      if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
+      continue;
+    }
+    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) {
+      u32 key;
+      double val;
+      tab.read(live[j], key, val);
+      x.htgt[hbase + j] = key;
+      x.hw[hbase + j] = float(val);  // fp64 sum narrowed once
+    }
+    if (threadIdx.x == 0) {
+      if (self) {
+        x.htgt[hbase + n] = c;
+        x.hw[hbase + n] = float(own_sum[i]);
+      }
+      x.fill[c] = n + self;
     }
   }
 }
@@ -269,10 +427,6 @@ int occupancy(K kernel, int threads, size_t smem) {
 
 }  // namespace
 
-size_t aggregate_table_bytes(u64 max_slots, int* blocks) {
-  if (blocks) *blocks = sm_count();
-  return size_t(max_slots) * Tab::kSlotBytes * size_t(sm_count());
-}
 
 void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
   const int sms = sm_count();
@@ -303,12 +457,54 @@ void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
     k<<<unsigned(blocks), T, smem, s>>>(a, b.of(kBinWarp), b.count(kBinWarp));
     LVN_LAUNCH();
   }
-  const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
-  if (big) {
+  if (b.count(kBinBlock)) {
     const size_t smem = (size_t(1) << kBlockCapLog) * Tab::kSlotBytes;
     static const int occ = occupancy(ag_block, kBlockThreads, smem);
-    const u64 blocks = std::min<u64>(big, u64(sms) * (a.table ? 1 : occ));
-    ag_block<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(kBinBlock), big);
+    const u64 blocks = std::min<u64>(b.count(kBinBlock), u64(sms) * occ);
+    ag_block<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(kBinBlock), b.count(kBinBlock));
+    LVN_LAUNCH();
+  }
+  const u64 nbig = b.count(kBinGlobal);
+  if (nbig) {
+    const u32* big = b.of(kBinGlobal);
+    DBuf<u32> index(a.count), live_n(nbig), own_seen(nbig), mcount(nbig);
+    DBuf<u64> bytes(nbig), tab_off(nbig + 1), moff(nbig + 1);
+    DBuf<double> own(nbig);
+    LVN_CUDA(cudaMemsetAsync(live_n.p, 0, nbig * sizeof(u32), s));
+    LVN_CUDA(cudaMemsetAsync(own_seen.p, 0, nbig * sizeof(u32), s));
+    LVN_CUDA(cudaMemsetAsync(own.p, 0, nbig * sizeof(double), s));
+    const unsigned pg = unsigned(std::min<u64>((nbig + 255) / 256, u64(sms) * 4));
+    ag_big_plan<<<pg, 256, 0, s>>>(big, nbig, a.hoff, a.coff, index.p, bytes.p, mcount.p);
+    LVN_LAUNCH();
+    exclusive_scan_u64(bytes.p, tab_off.p, nbig, s);
+    exclusive_scan_u32_to_u64(mcount.p, moff.p, nbig, s);
+    u64* h = ctx().pinned;
+    LVN_CUDA(cudaMemcpyAsync(h, tab_off.p + nbig, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(h + 1, moff.p + nbig, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    const u64 table_bytes = h[0], M = h[1];
+    DBuf<unsigned char> tables(table_bytes ? table_bytes : 16);
+    ag_big_clear<<<unsigned(std::min<u64>(nbig, u64(sms) * 4)), 256, 0, s>>>(big, nbig, a.hoff, tab_off.p,
+                                                                             tables.p);
+    LVN_LAUNCH();
+    // L = members of the big communities with arcs, P = scan of their degrees
+    DBuf<u32> vert(M ? M : 1), keep(M + 1), kpos(M + 1), L(M ? M : 1), D(M ? M : 1);
+    DBuf<u64> P(M + 1);
+    const unsigned mg = unsigned(std::min<u64>((M + 255) / 256 + 1, u64(sms) * 8));
+    ag_big_keep<<<mg, 256, 0, s>>>(a, big, nbig, moff.p, M, vert.p, keep.p);
+    LVN_LAUNCH();
+    exclusive_scan_u32(keep.p, kpos.p, M, s);
+    // D past nL = kpos[M] stays 0, so P[nL..M] all hold the arc total
+    LVN_CUDA(cudaMemsetAsync(D.p, 0, (M ? M : 1) * sizeof(u32), s));
+    ag_big_list<<<mg, 256, 0, s>>>(a.g, vert.p, keep.p, kpos.p, M, L.p, D.p);
+    LVN_LAUNCH();
+    exclusive_scan_u32_to_u64(D.p, P.p, M, s);
+    static const int occ = occupancy(ag_big_arcs, 256, 0);
+    ag_big_arcs<<<unsigned(u64(sms) * occ), 256, 0, s>>>(a, index.p, tab_off.p, tables.p, live_n.p, own.p,
+                                                          own_seen.p, L.p, P.p, kpos.p + M);
+    LVN_LAUNCH();
+    ag_big_emit<<<unsigned(std::min<u64>(nbig, u64(sms) * 4)), kBlockThreads, 0, s>>>(
+        a, big, nbig, tab_off.p, tables.p, live_n.p, own.p, own_seen.p);
     LVN_LAUNCH();
   }
 }

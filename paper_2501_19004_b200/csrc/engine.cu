@@ -361,16 +361,6 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   a.hw = hw.p;
   a.fill = fill.p;
   a.err = err;
-  DBuf<double> table;
-  const u64 max_cap = std::min<u64>(ab.max_degree, count);
-  const u64 slots = u64(1) << std::max<u32>(5, ceil_log2_u64(2 * (max_cap ? max_cap : 1)));
-  if (slots > (u64(1) << 13) && (ab.count(kBinBlock) + ab.count(kBinGlobal))) {
-    int blocks = 0;
-    const size_t bytes = aggregate_table_bytes(slots, &blocks);
-    table.alloc(bytes / sizeof(double) + 1);
-    a.table = table.p;
-    a.table_slots = slots;
-  }
   aggregate_rows(a, ab, s);
   if (check_mode()) {
     std::vector<u64> h_coff(count + 1), h_boff(count + 1), h_hoff(count + 1), h_off(u64(g.n) + 1);
@@ -501,7 +491,8 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
   Timing tm;
 
   DBuf<u32> global(N ? N : 1), C(N ? N : 1), used, rank, active, csize;
-  DBuf<double> K(N ? N : 1), S(N ? N : 1), table;
+  DBuf<double> K(N ? N : 1), S(N ? N : 1);
+  HubPlan hubs;
   DBuf<u8> flags(N ? N : 1);
   DBuf<IterRecord> rec(1);
   DBuf<u32> err(1);
@@ -549,12 +540,8 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
       a.csize = csize.p;
     }
     if (B.count(kBinGlobal)) {
-      int blocks = 0;
-      const size_t bytes = move_table_bytes(B.max_degree, p.value_bits, &blocks);
-      table.ensure(bytes / sizeof(double) + 1);
-      move_table_init(table.p, B.max_degree, p.value_bits, s);
-      a.table = table.p;
-      a.table_slots = move_table_slots(B.max_degree);
+      hub_plan_build(cur, B.of(kBinGlobal), B.count(kBinGlobal), p.value_bits, hubs, s);
+      hubs.attach(a);
     }
     // A sweep visits R consecutive vertex-id ranges in order, each with its own
     // degree bins: within a range the degree classes run low to high (the
@@ -1036,7 +1023,7 @@ int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const doubl
     const u32 n = ig.g.n;
     DevU32 mb;
     load_u32(membership, n, LVN_HOST, s, mb);
-    DBuf<double> K(n ? n : 1), S(n ? n : 1), og(n ? n : 1), table;
+    DBuf<double> K(n ? n : 1), S(n ? n : 1), og(n ? n : 1);
     DBuf<u32> ot(n ? n : 1);
     if (n) {
       LVN_CUDA(cudaMemcpyAsync(K.p, vertex_w, n * sizeof(double), cudaMemcpyHostToDevice, s));
@@ -1070,13 +1057,10 @@ int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const doubl
     a.gain_acc = &rec.p->gain;
     a.counters = &rec.p->verts;
     a.err = err.p;
+    HubPlan hubs;
     if (b.count(kBinGlobal)) {
-      int blocks = 0;
-      const size_t bytes = move_table_bytes(b.max_degree, pp.value_bits, &blocks);
-      table.alloc(bytes / sizeof(double) + 1);
-      move_table_init(table.p, b.max_degree, pp.value_bits, s);
-      a.table = table.p;
-      a.table_slots = move_table_slots(b.max_degree);
+      hub_plan_build(ig.g, b.of(kBinGlobal), b.count(kBinGlobal), pp.value_bits, hubs, s);
+      hubs.attach(a);
     }
     move_sweep(a, b.view(), pp.value_bits, s);
     if (n) {

@@ -89,19 +89,37 @@ struct MoveArgs {
   double* gain_acc = nullptr;  // summed gain of applied moves
   ull* counters = nullptr;     // [0] vertices processed, [1] arcs scanned, [2] moves
   u32* err = nullptr;
-  double* table = nullptr;     // global-table scratch for bin 5 (see move_table_bytes)
-  u64 table_slots = 0;         // slots per block
   u64 chunk = ~u64(0);         // max vertices of one bin decided per launch
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
   int hubs_first = 0;          // bin order of a sweep: highest degree class first
   u32* csize = nullptr;        // community member counts (singleton-pair rule), or null
+  // hub plan of the pass (kBinGlobal vertices): see HubPlan
+  const u32* hub_index = nullptr;
+  const u64* hub_tab_off = nullptr;
+  u32* hub_live = nullptr;
+  void* hub_own = nullptr;
+  unsigned char* hub_tables = nullptr;
 };
+
+// Per-pass storage for the chunked hub kernels: every kBinGlobal vertex owns an
+// HBM table of next_pow2(2 min(deg, n)) slots plus a live list, kept empty
+// between sweeps by the kernels themselves.
+struct HubPlan {
+  DBuf<u32> index;            // vertex -> position in the pass hub list
+  DBuf<u64> tab_off;          // position -> byte offset of its region
+  DBuf<u32> live;             // position -> live entries
+  DBuf<double> own;           // position -> weight to the own community (f32 or f64 view)
+  DBuf<unsigned char> tables;
+  u64 count = 0;
+  void attach(MoveArgs& a) const {
+    a.hub_index = index.p, a.hub_tab_off = tab_off.p, a.hub_live = live.p;
+    a.hub_own = own.p, a.hub_tables = tables.p;
+  }
+};
+void hub_plan_build(const DGraph& g, const u32* hubs, u64 count, int value_bits, HubPlan& p,
+                    cudaStream_t s);
 // one sweep over the bins of `bins` (see the kBin* classes)
 void move_sweep(const MoveArgs& a, const BinView& bins, int value_bits, cudaStream_t s);
-size_t move_table_bytes(u64 max_degree, int value_bits, int* blocks);
-u64 move_table_slots(u64 max_degree);
-// mark every slot of the bin-5 tables empty (done whenever they are allocated)
-void move_table_init(void* table, u64 max_degree, int value_bits, cudaStream_t s);
 
 // ---- community.cu -----------------------------------------------------------
 // used[c] = 1 for every c in C (used zeroed here), sized n
@@ -135,13 +153,11 @@ struct AggArgs {
   float* hw = nullptr;
   u32* fill = nullptr;           // entries written per row
   u32* err = nullptr;
-  double* table = nullptr;       // global-table scratch
-  u64 table_slots = 0;
 };
+// Synchronises once when the kBinGlobal bin is non-empty (sizes its HBM tables).
 void aggregate_rows(const AggArgs& a, const Bins& bins, cudaStream_t s);
 // capped[c] = min(budget[c], count): holey row capacity
 void cap_budgets(const u64* budget, u64* capped, u32 count, cudaStream_t s);
-size_t aggregate_table_bytes(u64 max_slots, int* blocks);
 // out rows = holey rows compacted (noff = scan of fill), total weight (fp64) into *tw
 void compact_rows(const u64* hoff, const u32* htgt, const float* hw, const u32* fill,
                   const u64* noff, u32 count, u32* otgt, float* ow, double* tw,

@@ -434,7 +434,7 @@ constexpr size_t block_smem() {
   return (size_t(1) << kBlockCapLog) * Tab::kSlotBytes + (size_t(1) << (kBlockCapLog - 1)) * 4;
 }
 
-template <class Tab, bool GLOBAL, bool DRY>
+template <class Tab, bool DRY>
 __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32* __restrict__ list,
                                                           u64 count) {
   using V = typename Tab::V;
@@ -444,15 +444,10 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
   __shared__ double red_g[W], red_k[W];
   __shared__ u32 red_c[W];
   __shared__ u32 bcast, nlive;
-  // global tables: per-block region of table_slots slots followed by table_slots/2 live entries
-  const size_t gstride = x.table_slots * Tab::kSlotBytes + x.table_slots / 2 * 4;
-  unsigned char* gbase = reinterpret_cast<unsigned char*>(x.table) + blockIdx.x * gstride;
-  const Tab tab = GLOBAL ? Tab(gbase, x.table_slots) : Tab(smem, u64(1) << kBlockCapLog);
-  u32* live = GLOBAL ? reinterpret_cast<u32*>(gbase + x.table_slots * Tab::kSlotBytes)
-                     : reinterpret_cast<u32*>(smem + (size_t(1) << kBlockCapLog) * Tab::kSlotBytes);
+  const Tab tab(smem, u64(1) << kBlockCapLog);
+  u32* live = reinterpret_cast<u32*>(smem + (size_t(1) << kBlockCapLog) * Tab::kSlotBytes);
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  if (!GLOBAL)  // smem starts dirty; the global table is kept empty between vertices and launches
-    for (u32 s = threadIdx.x; s < (1u << kBlockCapLog); s += kBlockThreads) tab.clear(s);
+  for (u32 s = threadIdx.x; s < (1u << kBlockCapLog); s += kBlockThreads) tab.clear(s);
   if (threadIdx.x == 0) nlive = 0;
   __syncthreads();
   Tally tl;
@@ -473,7 +468,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
     const u64 d = x.g.off[u + 1] - lo;
     const u32 from = x.C[u];
     const u32 lg = table_log(d, 5);
-    if (GLOBAL ? (u64(1) << lg) > x.table_slots : lg > u32(kBlockCapLog)) {  // capacity invariant
+    if (lg > u32(kBlockCapLog)) {  // capacity invariant
       if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
       continue;
     }
@@ -517,9 +512,166 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
   tl.flush(x);
 }
 
-__global__ void fill_u64(ull* p, u64 n, ull v) {
-  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
-    p[i] = v;
+// ---- hubs (kBinGlobal): a hub's row is split into chunks of kHubChunk arcs --------
+// so that many blocks share one hub instead of one block walking millions of
+// arcs (the reference's team sweep processes hubs across the whole thread team
+// for the same reason, louvain_compact.cpp:80-114, 165-205).
+//   lm_hub_chunks  block per chunk: K_{u->c} of the chunk in an smem table (own
+//                  community privatised), flushed into the hub's HBM table
+//                  (claim by CAS, L2 reductions, live-slot list)
+//   lm_hub_decide  block per hub: rank the live entries, apply the validated
+//                  move, mark the neighbours, restore the table to empty
+constexpr u32 kHubChunk = 4096;  // <= 4096 distinct keys: fits the 8192-slot smem table
+
+__host__ __device__ __forceinline__ u64 hub_slots(u64 deg, u32 n) {
+  const u64 distinct = deg < n ? deg : n;
+  const u32 l = ceil_log2_u64(2 * (distinct ? distinct : 1));
+  return u64(1) << (l > 5 ? l : 5);
+}
+
+template <class Tab>
+__host__ __device__ __forceinline__ u64 hub_region_bytes(u64 slots) {
+  return (slots * Tab::kSlotBytes + slots / 2 * 4 + 15) & ~u64(15);
+}
+
+template <class Tab>
+__global__ void hub_plan_k(const u32* __restrict__ hubs, u64 count, DGraph g, u32* __restrict__ index,
+                           u64* __restrict__ bytes) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < count; i += u64(gridDim.x) * blockDim.x) {
+    const u32 u = hubs[i];
+    index[u] = u32(i);
+    bytes[i] = hub_region_bytes<Tab>(hub_slots(g.off[u + 1] - g.off[u], g.n));
+  }
+}
+
+template <class Tab>
+__global__ void hub_clear_k(const u32* __restrict__ hubs, u64 count, DGraph g, const u64* __restrict__ tab_off,
+                            unsigned char* tables) {
+  for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
+    const u32 u = hubs[i];
+    const u64 slots = hub_slots(g.off[u + 1] - g.off[u], g.n);
+    const Tab tab(tables + tab_off[i], slots);
+    for (u64 s = threadIdx.x; s < slots; s += blockDim.x) tab.clear(u32(s));
+  }
+}
+
+__global__ void hub_chunk_counts_k(const u32* __restrict__ hubs, u64 count, const u64* __restrict__ off,
+                                   u32* __restrict__ chunks) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < count; i += u64(gridDim.x) * blockDim.x) {
+    const u32 u = hubs[i];
+    chunks[i] = u32((off[u + 1] - off[u] + kHubChunk - 1) / kHubChunk);
+  }
+}
+
+template <class Tab>
+__global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const u32* __restrict__ hubs,
+                                                               u64 count, const u64* __restrict__ chunk_off) {
+  using V = typename Tab::V;
+  extern __shared__ __align__(16) unsigned char smem[];
+  __shared__ u32 nlive;
+  __shared__ V red[kBlockThreads / 32];
+  const Tab stab(smem, u64(1) << kBlockCapLog);
+  u32* slive = reinterpret_cast<u32*>(smem + (size_t(1) << kBlockCapLog) * Tab::kSlotBytes);
+  for (u32 s = threadIdx.x; s < (1u << kBlockCapLog); s += kBlockThreads) stab.clear(s);
+  if (threadIdx.x == 0) nlive = 0;
+  __syncthreads();
+  const u64 total = chunk_off[count];
+  for (u64 v = blockIdx.x; v < total; v += gridDim.x) {
+    u64 lo = 0, hi = count;  // hub of chunk v: last i with chunk_off[i] <= v
+    while (hi - lo > 1) {
+      const u64 mid = (lo + hi) / 2;
+      if (chunk_off[mid] <= v) lo = mid; else hi = mid;
+    }
+    const u32 u = hubs[lo];
+    const u32 pi = x.hub_index[u];
+    const u64 row = x.g.off[u], row_end = x.g.off[u + 1];
+    const u64 a0 = row + (v - chunk_off[lo]) * kHubChunk;
+    const u64 a1 = min(a0 + kHubChunk, row_end);
+    const u32 from = x.C[u];
+    V own = V(0);
+    scan_arcs<kBatch>(x, stab, u32(kBlockCapLog), u, from, a0, a1, threadIdx.x, kBlockThreads, own, slive,
+                      &nlive);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = own;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      V t = V(0);
+      for (int w = 0; w < kBlockThreads / 32; ++w) t += red[w];
+      if (t != V(0)) atomicAdd(static_cast<V*>(x.hub_own) + pi, t);
+    }
+    const u64 slots = hub_slots(row_end - row, x.g.n);
+    unsigned char* base = x.hub_tables + x.hub_tab_off[pi];
+    const Tab gtab(base, slots);
+    u32* glive = reinterpret_cast<u32*>(base + slots * Tab::kSlotBytes);
+    const u32 glg = ceil_log2_u64(slots);
+    const u32 n = nlive;
+    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) {
+      const u32 s = slive[j];
+      u32 key;
+      double val;
+      stab.read(s, key, val);
+      const int gs = gtab.insert(glg, key, V(val));
+      if (gs >= 0) glive[atomicAdd(&x.hub_live[pi], 1u)] = u32(gs);
+      stab.clear(s);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) nlive = 0;
+    __syncthreads();
+  }
+}
+
+template <class Tab, bool DRY>
+__global__ void __launch_bounds__(kBlockThreads) lm_hub_decide(MoveArgs x, const u32* __restrict__ hubs,
+                                                               u64 count) {
+  using V = typename Tab::V;
+  constexpr int W = kBlockThreads / 32;
+  __shared__ double red_g[W], red_k[W];
+  __shared__ u32 red_c[W];
+  __shared__ u32 bcast;
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  Tally tl;
+  for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
+    const u32 u = hubs[i];
+    const u32 pi = x.hub_index[u];
+    const u64 lo = x.g.off[u], d = x.g.off[u + 1] - lo;
+    const u32 from = x.C[u];
+    const double own = double(static_cast<const V*>(x.hub_own)[pi]);
+    const u32 n = x.hub_live[pi];
+    const u64 slots = hub_slots(d, x.g.n);
+    unsigned char* base = x.hub_tables + x.hub_tab_off[pi];
+    const Tab gtab(base, slots);
+    const u32* glive = reinterpret_cast<const u32*>(base + slots * Tab::kSlotBytes);
+    const double ku = x.K[u], sf = x.sigma[from];
+    double bg = -INFINITY, bk = 0.0;
+    u32 bc = kEmpty;
+    rank_live<kBatch, DRY>(x, gtab, glive, n, threadIdx.x, kBlockThreads, own, ku, sf, bg, bc, bk);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+      const u32 oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
+    }
+    if (lane == 0) red_g[wid] = bg, red_c[wid] = bc, red_k[wid] = bk;
+    __syncthreads();
+    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) gtab.clear(glive[j]);
+    if (threadIdx.x == 0) {
+      for (int k = 1; k < W; ++k)
+        if (better(red_g[k], red_c[k], bg, bc)) bg = red_g[k], bc = red_c[k], bk = red_k[k];
+      x.hub_live[pi] = 0;
+      static_cast<V*>(x.hub_own)[pi] = V(0);
+      if (!DRY) x.flags[u] = 0;
+      ++tl.verts;
+      tl.arcs += d;
+      bcast = decide<DRY>(x, u, from, ku, bc, bg, bk, own, tl);
+    }
+    __syncthreads();
+    if (!DRY && bcast && x.prune)
+      for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) x.flags[x.g.tgt[a]] = 1;
+    __syncthreads();
+  }
+  tl.flush(x);
 }
 
 // ---- launch plumbing ----------------------------------------------------------
@@ -588,17 +740,29 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         break;
       }
       case kBinBlock: {
-        auto k = lm_block<Tab, false, DRY>;
+        auto k = lm_block<Tab, DRY>;
         constexpr size_t smem = block_smem<Tab>();
         static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
         launch_chunks(k, a, b.of(bin), b.count(bin), kBlockThreads, 1, u64(sms) * occ, smem, s);
         break;
       }
       case kBinGlobal: {
-        if (!a.table || !a.table_slots) fail(kInternal, "global move table not provisioned");
-        int blocks = 0;
-        move_table_bytes(b.max_degree, sizeof(V) == 4 ? 32 : 64, &blocks);
-        launch_chunks(lm_block<Tab, true, DRY>, a, b.of(bin), b.count(bin), kBlockThreads, 1, u64(blocks), 0, s);
+        if (!a.hub_tables) fail(kInternal, "hub plan not provisioned");
+        const u64 cnt = b.count(bin);
+        const u32* hubs = b.of(bin);
+        DBuf<u32> chunks(cnt);
+        DBuf<u64> coff(cnt + 1);
+        hub_chunk_counts_k<<<unsigned(std::min<u64>((cnt + 255) / 256, u64(sms) * 4)), 256, 0, s>>>(
+            hubs, cnt, a.g.off, chunks.p);
+        LVN_LAUNCH();
+        exclusive_scan_u32_to_u64(chunks.p, coff.p, cnt, s);
+        auto kc = lm_hub_chunks<Tab>;
+        constexpr size_t smem = block_smem<Tab>();
+        static const int occ = (set_smem(kc, smem), occupancy(kc, kBlockThreads, smem));
+        kc<<<unsigned(sms * occ), kBlockThreads, smem, s>>>(a, hubs, cnt, coff.p);
+        LVN_LAUNCH();
+        lm_hub_decide<Tab, DRY><<<unsigned(std::min<u64>(cnt, u64(sms) * 4)), kBlockThreads, 0, s>>>(a, hubs, cnt);
+        LVN_LAUNCH();
         break;
       }
       default: break;
@@ -613,35 +777,39 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
     for (int bin = kBinThread; bin <= kBinGlobal; ++bin) launch_bin(bin);
 }
 
+template <class Tab>
+void hub_plan_impl(const DGraph& g, const u32* hubs, u64 count, HubPlan& p, cudaStream_t s) {
+  p.count = count;
+  if (!count) return;
+  const int sms = sm_count();
+  p.index.ensure(g.n ? g.n : 1);
+  p.tab_off.ensure(count + 1);
+  DBuf<u64> bytes(count);
+  hub_plan_k<Tab><<<unsigned(std::min<u64>((count + 255) / 256, u64(sms) * 4)), 256, 0, s>>>(
+      hubs, count, g, p.index.p, bytes.p);
+  LVN_LAUNCH();
+  exclusive_scan_u64(bytes.p, p.tab_off.p, count, s);
+  u64* h = ctx().pinned;
+  LVN_CUDA(cudaMemcpyAsync(h, p.tab_off.p + count, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  p.tables.ensure(h[0] ? h[0] : 16);
+  hub_clear_k<Tab><<<unsigned(std::min<u64>(count, u64(sms) * 4)), 256, 0, s>>>(hubs, count, g, p.tab_off.p,
+                                                                                p.tables.p);
+  LVN_LAUNCH();
+  p.live.ensure(count);
+  p.own.ensure(count);
+  LVN_CUDA(cudaMemsetAsync(p.live.p, 0, count * sizeof(u32), s));
+  LVN_CUDA(cudaMemsetAsync(p.own.p, 0, count * sizeof(double), s));
+}
+
 }  // namespace
 
-size_t move_table_bytes(u64 max_degree, int value_bits, int* blocks) {
-  const u64 slots = u64(1) << std::max<u32>(5, ceil_log2_u64(2 * (max_degree ? max_degree : 1)));
-  if (blocks) *blocks = sm_count();
-  const size_t per = slots * (value_bits == 64 ? SplitF64::kSlotBytes : PackedF32::kSlotBytes) + slots / 2 * 4;
-  return per * size_t(sm_count());
-}
-
-u64 move_table_slots(u64 max_degree) {
-  return u64(1) << std::max<u32>(5, ceil_log2_u64(2 * (max_degree ? max_degree : 1)));
-}
-
-// every slot of every per-block region empty (the kernels keep it that way)
-void move_table_init(void* table, u64 max_degree, int value_bits, cudaStream_t s) {
-  const u64 slots = move_table_slots(max_degree);
-  const int blocks = sm_count();
-  const size_t stride = slots * (value_bits == 64 ? SplitF64::kSlotBytes : PackedF32::kSlotBytes) + slots / 2 * 4;
-  for (int b = 0; b < blocks; ++b) {
-    unsigned char* base = static_cast<unsigned char*>(table) + size_t(b) * stride;
-    if (value_bits == 64) {
-      LVN_CUDA(cudaMemsetAsync(base, 0, slots * 8, s));                // values
-      LVN_CUDA(cudaMemsetAsync(base + slots * 8, 0xFF, slots * 4, s));  // keys
-    } else {
-      fill_u64<<<unsigned(std::min<u64>((slots + 255) / 256, 1024)), 256, 0, s>>>(
-          reinterpret_cast<ull*>(base), slots, kEmptySlot64);
-      LVN_LAUNCH();
-    }
-  }
+void hub_plan_build(const DGraph& g, const u32* hubs, u64 count, int value_bits, HubPlan& p,
+                    cudaStream_t s) {
+  if (value_bits == 64)
+    hub_plan_impl<SplitF64>(g, hubs, count, p, s);
+  else
+    hub_plan_impl<PackedF32>(g, hubs, count, p, s);
 }
 
 void move_sweep(const MoveArgs& a0, const BinView& b, int value_bits, cudaStream_t s) {

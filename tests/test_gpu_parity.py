@@ -164,6 +164,38 @@ def test_aggregate_global_table_path(lvn, port):
     agg_equal(lvn.compact_aggregate(G_(g, lvn), m2), port.aggregate(g, m2))
 
 
+def hubs_graph(n, hubs, hub_deg, extra, seed):
+    """`hubs` vertices with hub_deg random neighbours each (several 4096-arc
+    chunks per hub) over a sparse random background of `extra` edges"""
+    rng = np.random.default_rng(seed)
+    src = [np.repeat(np.arange(hubs, dtype=np.uint32), hub_deg)]
+    dst = [rng.integers(hubs, n, hubs * hub_deg).astype(np.uint32)]
+    src.append(rng.integers(0, n, extra).astype(np.uint32))
+    dst.append(rng.integers(0, n, extra).astype(np.uint32))
+    w = rng.integers(1, 5, hubs * hub_deg + extra).astype(np.float64)
+    from oracle import port
+
+    return port.build_csr(n, np.concatenate(src), np.concatenate(dst), w)
+
+
+@pytest.mark.parametrize("k_big", [1, 3, 17])
+def test_aggregate_member_parallel(lvn, port, k_big):
+    # communities whose member-degree budget exceeds block_max (4096) take the
+    # member-parallel HBM-table path; mixed with small ones in the same call
+    g = random_graph(40000, 400000, 90 + k_big)
+    m = random_membership(g.n, 3000, k_big).astype(np.int64)
+    m[: 24000] = np.arange(24000) % k_big  # k_big giant communities
+    m = np.unique(m, return_inverse=True)[1].astype(np.uint32)
+    agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
+
+
+def test_aggregate_member_parallel_hubs(lvn, port):
+    g = hubs_graph(30000, 4, 20000, 100000, 5)
+    for m in (np.zeros(g.n, np.uint32), (np.arange(g.n) % 2).astype(np.uint32),
+              random_membership(g.n, 50, 4)):
+        agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
+
+
 def test_aggregate_planted(lvn, port):
     g = planted(50000, 100, 32, 0.1, 9)
     m = (np.arange(g.n) // 500).astype(np.uint32)
@@ -208,6 +240,22 @@ def test_decisions_hub(lvn, port):
     g = star(9000)
     memb = random_membership(g.n, 700, 8)
     decisions_equal(lvn, port, g, memb)
+
+
+@pytest.mark.parametrize("value_bits", [32, 64])
+@pytest.mark.parametrize("k", [30, 3000])
+def test_decisions_chunked_hubs(lvn, port, value_bits, k):
+    # 5 hubs of 20000 arcs: 5 chunks of 4096 arcs each, merged in HBM tables
+    g = hubs_graph(25000, 5, 20000, 60000, k)
+    memb = random_membership(g.n, k, 9)
+    decisions_equal(lvn, port, g, memb, -1, value_bits)
+
+
+def test_engine_chunked_hubs(lvn, port):
+    g = hubs_graph(60000, 8, 30000, 400000, 2)
+    r = lvn.louvain_compact(G_(g, lvn))
+    assert_q(r.modularity, port.modularity(g, np.asarray(r.membership, np.uint32)))
+    assert r.modularity > 0.0
 
 
 # ------------------------------------------------------------ engine end to end
