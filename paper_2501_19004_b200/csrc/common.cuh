@@ -11,6 +11,7 @@
 #include <mutex>
 #include <string>
 #include <unordered_map>
+#include <unordered_set>
 #include <vector>
 
 namespace lvn {
@@ -63,18 +64,23 @@ struct DGraph {
 };
 
 // ---------------------------------------------------------------------------
-// Caching device pool: one cudaMalloc per size class, reused across calls.
+// Device memory: stream-ordered allocations from the device's memory pool
+// (cudaMallocAsync on the context stream, release threshold unlimited), so
+// temporaries of any size are recycled without a cudaMalloc or a device
+// synchronisation once the pool has grown to the working set.
 // ---------------------------------------------------------------------------
 class Pool {
  public:
+  void bind(int device, cudaStream_t s);
   void* get(size_t bytes);
   void put(void* p);
-  void trim();  // return cached blocks to the driver
-  ~Pool();
+  void trim();         // return cached memory to the driver
+  void release_all();  // free every outstanding allocation (context teardown)
 
  private:
-  std::multimap<size_t, void*> free_;
-  std::unordered_map<void*, size_t> used_;
+  cudaMemPool_t pool_ = nullptr;
+  cudaStream_t stream_ = nullptr;
+  std::unordered_set<void*> used_;
 };
 
 // Engine context: one device, one stream, pinned scratch for small readbacks.
@@ -136,6 +142,25 @@ __host__ __device__ inline u32 ceil_log2_u64(u64 x) {
 #else
   return x <= 1 ? 0u : 64u - u32(__builtin_clzll(x - 1));
 #endif
+}
+
+// L2 eviction priority for the random gathers of a sweep (C[t], Sigma[c]):
+// evict_last keeps those arrays resident while the streamed rows (loaded
+// evict-first) pass through L2.
+__device__ __forceinline__ ull l2_keep_policy() {
+  ull p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ u32 ld_keep(const u32* a, ull pol) {
+  u32 v;
+  asm("ld.global.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ld_keep(const double* a, ull pol) {
+  double v;
+  asm("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
 }
 
 // multiplicative hash into a power-of-two table of 2^log_size slots

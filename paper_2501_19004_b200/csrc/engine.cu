@@ -30,48 +30,44 @@ void launch_check(const char* file, int line) {
 // ---------------------------------------------------------------------------
 // Pool / context
 // ---------------------------------------------------------------------------
+void Pool::bind(int device, cudaStream_t s) {
+  LVN_CUDA(cudaDeviceGetDefaultMemPool(&pool_, device));
+  std::uint64_t keep = ~std::uint64_t(0);
+  LVN_CUDA(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &keep));
+  stream_ = s;
+}
+
 void* Pool::get(size_t bytes) {
-  const size_t r = bytes <= (size_t(1) << 20) ? ((bytes + 511) & ~size_t(511))
-                                              : ((bytes + (size_t(2) << 20) - 1) & ~((size_t(2) << 20) - 1));
-  auto it = free_.lower_bound(r);
-  if (it != free_.end() && it->first <= 2 * r) {
-    void* p = it->second;
-    used_[p] = it->first;
-    free_.erase(it);
-    return p;
-  }
   void* p = nullptr;
-  cudaError_t e = cudaMalloc(&p, r);
+  cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 1, stream_);
   if (e == cudaErrorMemoryAllocation) {
     (void)cudaGetLastError();
     trim();
-    e = cudaMalloc(&p, r);
+    e = cudaMallocAsync(&p, bytes ? bytes : 1, stream_);
   }
   if (e != cudaSuccess) {
     (void)cudaGetLastError();
     fail(e == cudaErrorMemoryAllocation ? kOom : kCuda,
-         "cudaMalloc(" + std::to_string(r) + " bytes): " + cudaGetErrorString(e));
+         "cudaMallocAsync(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
   }
-  used_[p] = r;
+  used_.insert(p);
   return p;
 }
 
 void Pool::put(void* p) {
-  auto it = used_.find(p);
-  if (it == used_.end()) return;
-  free_.emplace(it->second, p);
-  used_.erase(it);
+  if (!p || !used_.erase(p)) return;
+  (void)cudaFreeAsync(p, stream_);
 }
 
 void Pool::trim() {
-  (void)cudaDeviceSynchronize();
-  for (auto& kv : free_) (void)cudaFree(kv.second);
-  free_.clear();
+  (void)cudaStreamSynchronize(stream_);
+  if (pool_) (void)cudaMemPoolTrimTo(pool_, 0);
 }
 
-Pool::~Pool() {
-  for (auto& kv : free_) (void)cudaFree(kv.second);
-  for (auto& kv : used_) (void)cudaFree(kv.first);
+void Pool::release_all() {
+  for (void* p : used_) (void)cudaFreeAsync(p, stream_);
+  used_.clear();
+  if (stream_) (void)cudaStreamSynchronize(stream_);
 }
 
 static Context* g_ctx = nullptr;
@@ -96,6 +92,7 @@ void init_context(int device) {
   c->sms = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
   LVN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  c->pool.bind(device, c->stream);
   LVN_CUDA(cudaMallocHost(&c->pinned, 8192 * sizeof(u64)));
   g_ctx = c;
 }
@@ -111,6 +108,7 @@ void destroy_context() {
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   if (!g_ctx) return;
   (void)cudaStreamSynchronize(g_ctx->stream);
+  g_ctx->pool.release_all();
   (void)cudaFreeHost(g_ctx->pinned);
   (void)cudaStreamDestroy(g_ctx->stream);
   delete g_ctx;

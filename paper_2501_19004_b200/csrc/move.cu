@@ -338,48 +338,76 @@ __global__ void __launch_bounds__(THREADS, 4) lm_group(MoveArgs x, const u32* __
 // shared memory, no probe loops), which the hash kernels cannot achieve on
 // short rows where each group's probing diverges. Row arcs are streamed with
 // evict-first loads so the gathered C / Sigma lines keep their L2 residency.
+//
+// Software-pipelined one vertex deep: the loads of the group's next vertex
+// (list entry, row bounds, own community, arcs, their communities, Sigma of
+// the own community) are issued in stages between the compute steps of the
+// current one (sort, Sigma gathers, scoring, decision), so each group keeps two
+// vertices' dependent load chains in flight. The next vertex's gathers may
+// miss the current vertex's move (one more source of the asynchrony the
+// validated join already tolerates); the DRY path writes no state, so its
+// results are unaffected.
 template <int G, int K, class V, bool DRY>
 __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict__ list, u64 count) {
   constexpr int GPB = 256 / G;
   constexpr u32 FULL = 0xffffffffu;
   const u32 lane = threadIdx.x & (G - 1);
   const u32 gi = threadIdx.x / G;
+  const u64 stride = u64(gridDim.x) * GPB;
+  const ull keep = l2_keep_policy();
   Tally tl;
-  // the trip count is uniform across the block, so every lane reaches every shuffle
-  for (u64 i0 = u64(blockIdx.x) * GPB; i0 < count; i0 += u64(gridDim.x) * GPB) {
-    const u64 i = i0 + gi;
-    const bool have = i < count;
-    u32 u = 0, from = kEmpty;
-    u64 lo = 0, hi = 0;
-    double ku = 0.0, sf = 0.0;
-    if (have) {
-      u = list[i];
-      lo = x.g.off[u];
-      hi = x.g.off[u + 1];
-      from = x.C[u];
-      ku = x.K[u];
-      sf = x.sigma[from];
-    }
-    u32 t[K], key[K];
-    V val[K];
+  // vertex in flight (the trip count is uniform across the block, so every
+  // lane reaches every shuffle)
+  u64 i0 = u64(blockIdx.x) * GPB;
+  bool have = i0 + gi < count;
+  u32 u = 0, from = kEmpty;
+  u64 lo = 0, hi = 0;
+  double ku = 0.0, sf = 0.0;
+  u32 t[K], key[K];
+  V val[K];
+  if (have) {
+    u = list[i0 + gi];
+    lo = x.g.off[u];
+    hi = x.g.off[u + 1];
+    from = x.C[u];
+    ku = x.K[u];
+  }
 #pragma unroll
-    for (int r = 0; r < K; ++r) {
-      const u64 a = lo + u64(r) * G + lane;
-      const bool ok = a < hi;
-      t[r] = ok ? __ldcs(x.g.tgt + a) : kEmpty;
-      val[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
-    }
+  for (int r = 0; r < K; ++r) {
+    const u64 a = lo + u64(r) * G + lane;
+    const bool ok = a < hi;
+    t[r] = ok ? __ldcs(x.g.tgt + a) : kEmpty;
+    val[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+  }
+  if (have) sf = x.sigma[from];
 #pragma unroll
-    for (int r = 0; r < K; ++r) key[r] = (t[r] != kEmpty && t[r] != u) ? x.C[t[r]] : kEmpty;
+  for (int r = 0; r < K; ++r) key[r] = (t[r] != kEmpty && t[r] != u) ? ld_keep(x.C + t[r], keep) : kEmpty;
 
-    // sort by community (padding and self-loops carry kEmpty and sort last),
-    // then K_{u->c} lands on the last element of each community's run
+  for (; i0 < count; i0 += stride) {
+    // stage 1 (next): list entry
+    const u64 in = i0 + stride + gi;
+    const bool nhave = in < count;
+    const u32 nu = nhave ? list[in] : 0u;
+
+    // current: sort by community (padding and self-loops carry kEmpty and
+    // sort last); K_{u->c} lands on the last element of each run
     bitonic_sort<G, K, V>(key, val, lane);
     bool tail[K];
     segmented_runs<G, K, V>(key, val, tail, lane);
     const V (&run)[K] = val;
 
-    // own community weight and the best other community
+    // stage 2 (next): row bounds, own community, vertex weight
+    u64 nlo = 0, nhi = 0;
+    u32 nfrom = kEmpty;
+    double nku = 0.0;
+    if (nhave) {
+      nlo = x.g.off[nu];
+      nhi = x.g.off[nu + 1];
+      nfrom = x.C[nu];
+      nku = x.K[nu];
+    }
+
+    // current: own community weight, Sigma of the candidates
     V own_l = V(0);
     bool cand[K];
 #pragma unroll
@@ -394,8 +422,21 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
 #pragma unroll
     for (int r = 0; r < K; ++r) {
       if (cand[r]) cand[r] = key_ok(x, key[r]);
-      sc[r] = cand[r] ? x.sigma[key[r]] : 0.0;
+      sc[r] = cand[r] ? ld_keep(x.sigma + key[r], keep) : 0.0;
     }
+
+    // stage 3 (next): arcs
+    u32 nt[K];
+    V nval[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const u64 a = nlo + u64(r) * G + lane;
+      const bool ok = a < nhi;
+      nt[r] = ok ? __ldcs(x.g.tgt + a) : kEmpty;
+      nval[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+    }
+
+    // current: rank the candidates, group argmax
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
 #pragma unroll
@@ -411,6 +452,14 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
       const double ok = __shfl_xor_sync(FULL, bk, o, G);
       if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
     }
+
+    // stage 4 (next): communities of the arcs, Sigma of the own community
+    u32 nkey[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) nkey[r] = (nt[r] != kEmpty && nt[r] != nu) ? ld_keep(x.C + nt[r], keep) : kEmpty;
+    const double nsf = nhave ? x.sigma[nfrom] : 0.0;
+
+    // current: decide and apply
     int moved = 0;
     if (have && lane == 0) {
       if (!DRY) x.flags[u] = 0;
@@ -424,6 +473,187 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
       for (int r = 0; r < K; ++r)
         if (t[r] != kEmpty) x.flags[t[r]] = 1;
     }
+
+    // rotate
+    have = nhave, u = nu, lo = nlo, hi = nhi, from = nfrom, ku = nku, sf = nsf;
+#pragma unroll
+    for (int r = 0; r < K; ++r) t[r] = nt[r], key[r] = nkey[r], val[r] = nval[r];
+  }
+  tl.flush(x);
+}
+
+// ---- sort bins, match variant: warp per vertex, K arcs per lane ----------------
+// Equal communities among the 32 arcs of one register round are found with
+// one match.any; the lowest lane of each peer set (the leader) sums the peers'
+// weights in ascending lane (= row) order from a per-warp smem buffer. With
+// K = 1 the leaders are the candidates. With K > 1 the leaders of every round
+// merge their partial sums into a per-warp smem table: keys are distinct
+// within a round, so a claim never races another lane of the warp for a key.
+// Pipelined across vertices like lm_sort.
+template <int K, class Tab>
+constexpr size_t match_smem() {
+  constexpr size_t cap = K > 1 ? size_t(64) * K : 0;
+  return 8 * (32 * sizeof(typename Tab::V) + cap * Tab::kSlotBytes + cap / 2 * 4);
+}
+
+template <int K, class Tab, bool DRY>
+__global__ void __launch_bounds__(256) lm_match(MoveArgs x, const u32* __restrict__ list, u64 count) {
+  using V = typename Tab::V;
+  constexpr u32 FULL = 0xffffffffu;
+  constexpr u32 CAP = K > 1 ? 64u * K : 1u;
+  constexpr int WPB = 8;
+  extern __shared__ __align__(16) unsigned char smem[];
+  const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const u32 lt = (1u << lane) - 1u;
+  V* buf = reinterpret_cast<V*>(smem) + wid * 32;
+  unsigned char* tb = smem + WPB * 32 * sizeof(V) + size_t(wid) * (CAP * Tab::kSlotBytes + CAP / 2 * 4);
+  const Tab tab(tb, CAP);
+  u32* live = reinterpret_cast<u32*>(tb + CAP * Tab::kSlotBytes);
+  if (K > 1)
+    for (u32 j = lane; j < CAP; j += 32) tab.clear(j);
+  __syncwarp();
+  const u64 stride = u64(gridDim.x) * WPB;
+  Tally tl;
+  u64 i0 = u64(blockIdx.x) * WPB;
+  bool have = i0 + wid < count;
+  u32 u = 0, from = kEmpty;
+  u64 lo = 0, hi = 0;
+  double ku = 0.0, sf = 0.0;
+  u32 t[K], key[K];
+  V val[K];
+  if (have) {
+    u = list[i0 + wid];
+    lo = x.g.off[u];
+    hi = x.g.off[u + 1];
+    from = x.C[u];
+    ku = x.K[u];
+  }
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const u64 a = lo + u64(r) * 32 + lane;
+    const bool ok = a < hi;
+    t[r] = ok ? __ldcs(x.g.tgt + a) : kEmpty;
+    val[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+  }
+  if (have) sf = x.sigma[from];
+#pragma unroll
+  for (int r = 0; r < K; ++r) key[r] = (t[r] != kEmpty && t[r] != u) ? x.C[t[r]] : kEmpty;
+
+  for (; i0 < count; i0 += stride) {
+    // stage 1 (next)
+    const u64 in = i0 + stride + wid;
+    const bool nhave = in < count;
+    const u32 nu = nhave ? list[in] : 0u;
+
+    // current: per-round peer sums
+    V own_l = V(0);
+    u32 ckey = kEmpty;  // K == 1: this lane's candidate
+    V cval = V(0);
+    u32 n = 0;          // K > 1: live entries
+    const u32 lg = K > 1 ? table_log(hi - lo, 5) : 0;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const u32 peers = __match_any_sync(FULL, key[r]);
+      const bool lead = key[r] != kEmpty && (peers & lt) == 0;
+      buf[lane] = val[r];
+      __syncwarp();
+      V sum = V(0);
+      if (lead)
+        for (u32 m = peers; m; m &= m - 1) sum += buf[__ffs(m) - 1];
+      __syncwarp();
+      bool fresh = false;
+      int slot = -1;
+      if (lead) {
+        if (key[r] == from) {
+          own_l += sum;
+        } else if (K == 1) {
+          ckey = key[r], cval = sum;
+        } else {
+          slot = tab.insert(lg, key[r], sum);
+          fresh = slot >= 0;
+        }
+      }
+      if (K > 1) {
+        const u32 nb = __ballot_sync(FULL, fresh);
+        if (fresh) live[n + __popc(nb & lt)] = u32(slot);
+        n += __popc(nb);
+      }
+    }
+    V own = own_l;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(FULL, own, o);
+
+    // stage 2 (next)
+    u64 nlo = 0, nhi = 0;
+    u32 nfrom = kEmpty;
+    double nku = 0.0;
+    if (nhave) {
+      nlo = x.g.off[nu];
+      nhi = x.g.off[nu + 1];
+      nfrom = x.C[nu];
+      nku = x.K[nu];
+    }
+
+    double bg = -INFINITY, bk = 0.0;
+    u32 bc = kEmpty;
+    if (K == 1) {
+      const bool cand = ckey != kEmpty && key_ok(x, ckey);
+      const double sc = cand ? x.sigma[ckey] : 0.0;
+      if (cand) {
+        bg = score<DRY>(x, double(cval), double(own), ku, sc, sf);
+        bc = ckey, bk = double(cval);
+      }
+    } else {
+      __syncwarp();
+      rank_live<2, DRY>(x, tab, live, n, lane, 32, double(own), ku, sf, bg, bc, bk);
+    }
+
+    // stage 3 (next)
+    u32 nt[K];
+    V nval[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const u64 a = nlo + u64(r) * 32 + lane;
+      const bool ok = a < nhi;
+      nt[r] = ok ? __ldcs(x.g.tgt + a) : kEmpty;
+      nval[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+    }
+
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double og = __shfl_xor_sync(FULL, bg, o);
+      const u32 oc = __shfl_xor_sync(FULL, bc, o);
+      const double ok = __shfl_xor_sync(FULL, bk, o);
+      if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
+    }
+    if (K > 1) {
+      for (u32 j = lane; j < n; j += 32) tab.clear(live[j]);
+      __syncwarp();
+    }
+
+    // stage 4 (next)
+    u32 nkey[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) nkey[r] = (nt[r] != kEmpty && nt[r] != nu) ? x.C[nt[r]] : kEmpty;
+    const double nsf = nhave ? x.sigma[nfrom] : 0.0;
+
+    int moved = 0;
+    if (have && lane == 0) {
+      if (!DRY) x.flags[u] = 0;
+      ++tl.verts;
+      tl.arcs += hi - lo;
+      moved = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own), tl);
+    }
+    moved = __shfl_sync(FULL, moved, 0);
+    if (!DRY && moved && x.prune) {
+#pragma unroll
+      for (int r = 0; r < K; ++r)
+        if (t[r] != kEmpty) x.flags[t[r]] = 1;
+    }
+
+    have = nhave, u = nu, lo = nlo, hi = nhi, from = nfrom, ku = nku, sf = nsf;
+#pragma unroll
+    for (int r = 0; r < K; ++r) t[r] = nt[r], key[r] = nkey[r], val[r] = nval[r];
   }
   tl.flush(x);
 }
@@ -712,6 +942,26 @@ void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
   launch_chunks(k, a, b.of(bin), b.count(bin), T, T / G, u64(sm_count()) * occ, 0, s);
 }
 
+template <int K, class Tab, bool DRY>
+void launch_match(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
+  if (!b.count(bin)) return;
+  constexpr int T = 256;
+  auto k = lm_match<K, Tab, DRY>;
+  constexpr size_t smem = match_smem<K, Tab>();
+  static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
+  launch_chunks(k, a, b.of(bin), b.count(bin), T, T / 32, u64(sm_count()) * occ, smem, s);
+}
+
+// LVN_MOVE_KERNEL=match selects the match.any kernels for the sort bins
+// (tuning aid; the register-sort kernels are faster on the configs measured)
+bool use_match() {
+  static const bool on = [] {
+    const char* e = std::getenv("LVN_MOVE_KERNEL");
+    return e && std::string(e) == "match";
+  }();
+  return on;
+}
+
 template <class Tab, bool DRY>
 void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
   using V = typename Tab::V;
@@ -727,10 +977,18 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
       }
       case kBinSort8: launch_sort<8, 1, V, DRY>(a, b, bin, s); break;
       case kBinSort16: launch_sort<16, 1, V, DRY>(a, b, bin, s); break;
-      case kBinSort32: launch_sort<32, 1, V, DRY>(a, b, bin, s); break;
-      case kBinSort64: launch_sort<32, 2, V, DRY>(a, b, bin, s); break;
-      case kBinSort128: launch_sort<32, 4, V, DRY>(a, b, bin, s); break;
-      case kBinSort256: launch_sort<32, 8, V, DRY>(a, b, bin, s); break;
+      case kBinSort32:
+        if (use_match()) launch_match<1, Tab, DRY>(a, b, bin, s); else launch_sort<32, 1, V, DRY>(a, b, bin, s);
+        break;
+      case kBinSort64:
+        if (use_match()) launch_match<2, Tab, DRY>(a, b, bin, s); else launch_sort<32, 2, V, DRY>(a, b, bin, s);
+        break;
+      case kBinSort128:
+        if (use_match()) launch_match<4, Tab, DRY>(a, b, bin, s); else launch_sort<32, 4, V, DRY>(a, b, bin, s);
+        break;
+      case kBinSort256:
+        if (use_match()) launch_match<8, Tab, DRY>(a, b, bin, s); else launch_sort<32, 8, V, DRY>(a, b, bin, s);
+        break;
       case kBinWarp: {
         constexpr int T = 256;
         auto k = lm_group<Tab, 32, kWarpCapLog, T, DRY>;
