@@ -324,7 +324,9 @@ def main():
                               "other": r.phase.other},
             "kernel_seconds": {k: s.seconds for k, s in r.stats.items()},
             "kernel_gbps": {k: s.gbps for k, s in r.stats.items()},
-            "roofline": {"bound": "hbm", "kernel": "local-moving sweep (lm_thread/lm_group/lm_block)",
+            "roofline": {"bound": "hbm",
+                         "kernel": "local-moving sweep (lm_thread/lm_sort/lm_group/lm_block/lm_hub_*); "
+                                   "one launch = every local-moving kernel of one iteration",
                          "achieved": move_gbps, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": move_gbps / peak if peak else None,
                          "bytes_per_launch": per_launch_bytes,
