@@ -216,8 +216,16 @@ def main():
     import torch.distributed as dist
 
     if world > 1:
-        torch.cuda.set_device(local)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        # LVN_DIST_BACKEND=gloo lets several ranks share one GPU (exercise of the
+        # sharded path on a 1-GPU box); the measured runs use NCCL
+        backend = os.environ.get("LVN_DIST_BACKEND", "nccl")
+        if backend == "gloo":
+            local = local % max(torch.cuda.device_count(), 1)
+            torch.cuda.set_device(local)
+            dist.init_process_group("gloo")
+        else:
+            torch.cuda.set_device(local)
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
 
     if args.impl == "reference":
         run_reference(args, world, rank)
@@ -240,6 +248,18 @@ def main():
     n, arcs = dg.num_vertices(), dg.num_arcs()
     log(f"[rank {rank}] {args.config}: {n} vertices, {arcs} arcs, generated in {time.time() - t0:.1f}s")
     opts = lvn.CompactOptions(value_bits=args.value_bits)
+    # N > 1: one process per GPU, passes sharded by row range over NCCL
+    # (SURVEY.md 8(e)); the whole job's work is fixed as N grows (strong scaling)
+    comm = None
+    if world > 1:
+        from paper_2501_19004_b200.distributed import Collectives
+
+        comm = Collectives(location="cuda")
+
+    def run(g, on_device):
+        if comm is not None:
+            return lvn.louvain_sharded(g, comm, None, opts, membership_on_device=on_device)
+        return lvn.louvain_compact(g, None, opts, membership_on_device=on_device)
 
     def barrier():
         if world > 1:
@@ -255,7 +275,7 @@ def main():
 
     # ---- value: device-resident input -------------------------------------------
     for _ in range(args.warmup):
-        lvn.louvain_compact(dg, None, opts, membership_on_device=True)
+        run(dg, True)
     sampler = ClockSampler(local)
     results = []
     l0 = lvn.launch_count()
@@ -264,13 +284,13 @@ def main():
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(args.steps):
-            results.append(lvn.louvain_compact(dg, None, opts, membership_on_device=True))
+            results.append(run(dg, True))
         e1.record()
         barrier()
     launches = (lvn.launch_count() - l0) // args.steps
     elapsed = max_over_ranks(e0.elapsed_time(e1) / 1e3)
     step_s = elapsed / args.steps
-    value = world * arcs / step_s
+    value = arcs / step_s
     clocks = sampler.summary()
     r = results[-1]
     mv = r.stats["move"]
@@ -288,17 +308,17 @@ def main():
         off_pinned[:] = host.offsets
         hg = lvn.CsrGraph(off_pinned, host.targets, host.weights, host.total_weight)
         assert hg.offsets.ctypes.data == off_pinned.ctypes.data
-        lvn.louvain_compact(hg, None, opts)
+        run(hg, False)
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         qs = []
         f0.record()
         for _ in range(args.steps):
-            qs.append(lvn.louvain_compact(hg, None, opts).modularity)
+            qs.append(run(hg, False).modularity)
         f1.record()
         barrier()
         e2e_s = max_over_ranks(f0.elapsed_time(f1) / 1e3) / args.steps
-        e2e = {"value": world * arcs / e2e_s, "unit": "edges/s", "ms_per_step": e2e_s * 1e3,
+        e2e = {"value": arcs / e2e_s, "unit": "edges/s", "ms_per_step": e2e_s * 1e3,
                "h2d_bytes_per_step": 8 * (n + 1) + 8 * arcs, "d2h_bytes_per_step": 4 * n}
     else:
         host = None
@@ -312,13 +332,14 @@ def main():
     if rank == 0:
         out = {
             "metric": METRIC, "value": value, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": step_s * 1e3, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64" if args.value_bits == 64 else "f32+f64",
             "data": "synthetic (device-generated, seeded)",
             "config": {"workload": args.config, "desc": cfg["desc"], "vertices": n, "arcs": arcs,
-                       "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+                       "parallelism": f"row-sharded x{world} over NCCL" if world > 1 else "single GPU",
                        "l2_flush": "not needed: CSR >> 126 MB L2"},
             "modularity": r.modularity, "num_communities": r.num_communities, "passes": r.passes,
+            "sharded_passes": r.sharded_passes, "exchange_seconds": r.exchange_seconds,
             "iterations_per_pass": r.iterations_per_pass,
             "phase_seconds": {"local_moving": r.phase.local_moving, "aggregation": r.phase.aggregation,
                               "other": r.phase.other},

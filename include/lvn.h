@@ -110,7 +110,11 @@ typedef struct lvn_params {
   /* 1: a singleton may join another singleton community only if its id is
    * lower (concurrent symmetric pairs merge instead of swapping labels) */
   int singleton_rule;
-  int reserved[3];
+  /* lvn_louvain_sharded: a pass is sharded across the ranks while its graph
+   * has at least 2^shard_min_arcs_log2 arcs; smaller graphs run whole on
+   * every rank (the collapse of SURVEY.md 8(e)) */
+  int shard_min_arcs_log2;      /* 22 */
+  int reserved[2];
 } lvn_params;
 
 /* Per-kernel-family device accounting (CUDA events on the engine stream). */
@@ -146,6 +150,9 @@ typedef struct lvn_result {
   double d2h_seconds;     /* membership download */
   lvn_phase_stats stats[LVN_STAT_COUNT];
   int membership_on_device;
+  int num_shards;         /* ranks of lvn_louvain_sharded (1 otherwise) */
+  int sharded_passes;     /* passes run sharded (the rest ran whole on every rank) */
+  double exchange_seconds; /* host time inside the collectives */
 } lvn_result;
 
 /* ---- lifecycle -------------------------------------------------------- */
@@ -189,6 +196,38 @@ int lvn_aggregate(const lvn_csr* g, const uint32_t* membership, int membership_l
 int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
                        const double* community_w, double m, const lvn_params* p,
                        int force_kernel, uint32_t* to, double* gain);
+
+/* ---- sharded multi-GPU run -------------------------------
+ * One process per GPU, each calling lvn_louvain_sharded on the same graph (its
+ * own device copy, or host input it uploads). A sharded pass gives rank r the
+ * rows [bounds[r], bounds[r+1]) of lvn_partition_rows: it decides the moves of
+ * those vertices against replicated membership C and community weights Sigma,
+ * then per iteration the ranks allreduce the Sigma deltas (f64 sum), the
+ * neighbour marks (u8 max), the gain and counters, and allgather C of their
+ * rows; aggregation emits the super-rows of a community range per rank and
+ * allgathers them. Passes whose graph has fewer than 2^shard_min_arcs_log2
+ * arcs run whole on every rank. The collectives are supplied by the caller
+ * (paper_2501_19004_b200.distributed wraps torch.distributed / NCCL): buffers
+ * are device pointers on this process's GPU, the library's stream is idle
+ * when a callback runs, and a callback returns 0 once its result is in place. */
+enum lvn_dtype { LVN_U8 = 0, LVN_U32 = 1, LVN_U64 = 2, LVN_F64 = 3 };
+enum lvn_redop { LVN_SUM = 0, LVN_MAX = 1 };
+typedef struct lvn_comm {
+  int rank;
+  int size;
+  void* user;
+  /* in-place allreduce of count elements of dtype */
+  int (*allreduce)(void* user, void* buf, uint64_t count, int dtype, int op);
+  /* rank r contributes counts[r] bytes from send; recv (sum of counts bytes)
+   * receives the contributions concatenated in rank order; send may lie
+   * inside recv at its own rank's position */
+  int (*allgatherv)(void* user, const void* send, void* recv, const uint64_t* counts);
+} lvn_comm;
+int lvn_louvain_sharded(const lvn_csr* g, const lvn_params* p, const lvn_comm* comm, lvn_result** out);
+/* rows [0, n) cut into `parts` contiguous ranges of about A/parts arcs each:
+ * bounds[k] = the first row whose offset reaches floor(k A / parts), bounds[parts] = n
+ * (host offsets; the engine applies the same rule on the device) */
+int lvn_partition_rows(const uint64_t* offsets, uint32_t n, int parts, uint32_t* bounds);
 
 /* ---- device-resident graphs (bench / generators) ----------------------- */
 typedef struct lvn_dgraph lvn_dgraph;

@@ -34,7 +34,9 @@ from .louvain import (  # noqa: F401
     louvain_aggregate,
     louvain_compact,
     louvain_gpu,
+    louvain_sharded,
     modularity,
+    partition_rows,
     pick_less_active,
     renumber_communities,
     vertex_weights,

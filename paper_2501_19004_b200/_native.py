@@ -65,7 +65,8 @@ class lvn_params(C.Structure):
         ("sweep_order", C.c_int),
         ("sweep_ranges", C.c_int),
         ("singleton_rule", C.c_int),
-        ("reserved", C.c_int * 3),
+        ("shard_min_arcs_log2", C.c_int),
+        ("reserved", C.c_int * 2),
     ]
 
 
@@ -100,6 +101,25 @@ class lvn_result(C.Structure):
         ("d2h_seconds", C.c_double),
         ("stats", lvn_phase_stats * 5),
         ("membership_on_device", C.c_int),
+        ("num_shards", C.c_int),
+        ("sharded_passes", C.c_int),
+        ("exchange_seconds", C.c_double),
+    ]
+
+
+LVN_U8, LVN_U32, LVN_U64, LVN_F64 = 0, 1, 2, 3
+LVN_SUM, LVN_MAX = 0, 1
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int)
+ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64))
+
+
+class lvn_comm(C.Structure):
+    _fields_ = [
+        ("rank", C.c_int),
+        ("size", C.c_int),
+        ("user", C.c_void_p),
+        ("allreduce", ALLREDUCE_FN),
+        ("allgatherv", ALLGATHERV_FN),
     ]
 
 
@@ -127,6 +147,7 @@ EXPORTS = (
     "lvn_count_communities", "lvn_renumber", "lvn_lookup_dendrogram", "lvn_community_csr",
     "lvn_aggregate", "lvn_evaluate_moves", "lvn_generate", "lvn_dgraph_upload", "lvn_dgraph_view",
     "lvn_dgraph_download", "lvn_dgraph_free", "lvn_device_alloc", "lvn_device_free", "lvn_memcpy",
+    "lvn_louvain_sharded", "lvn_partition_rows",
 )
 
 _lib = None
@@ -161,6 +182,9 @@ def lib() -> C.CDLL:
     L.lvn_graph_free.argtypes = [C.POINTER(lvn_graph_out)]
     L.lvn_graph_free.restype = None
     L.lvn_louvain.argtypes = [C.POINTER(lvn_csr), C.POINTER(lvn_params), C.POINTER(C.POINTER(lvn_result))]
+    L.lvn_louvain_sharded.argtypes = [C.POINTER(lvn_csr), C.POINTER(lvn_params), C.POINTER(lvn_comm),
+                                      C.POINTER(C.POINTER(lvn_result))]
+    L.lvn_partition_rows.argtypes = [vp, C.c_uint32, i, vp]
     L.lvn_modularity.argtypes = [C.POINTER(lvn_csr), vp, i, C.POINTER(C.c_double)]
     L.lvn_vertex_weights.argtypes = [C.POINTER(lvn_csr), vp]
     L.lvn_count_communities.argtypes = [vp, C.c_uint64, i, C.POINTER(C.c_uint32)]

@@ -64,10 +64,12 @@ struct DGraph {
 };
 
 // ---------------------------------------------------------------------------
-// Device memory: stream-ordered allocations from the device's memory pool
-// (cudaMallocAsync on the context stream, release threshold unlimited), so
-// temporaries of any size are recycled without a cudaMalloc or a device
-// synchronisation once the pool has grown to the working set.
+// Device memory. Everything is stream-ordered on the engine stream:
+// requests below 64 MB come from the device memory pool (cudaMallocAsync /
+// cudaFreeAsync, release threshold unlimited); larger ones (graph arrays,
+// holey rows, tables) are rounded up to 1/16 of their power of two and kept in
+// a best-fit cache of their own, so the multi-GB buffers of consecutive runs
+// land on the same blocks instead of fragmenting the pool.
 // ---------------------------------------------------------------------------
 class Pool {
  public:
@@ -76,11 +78,30 @@ class Pool {
   void put(void* p);
   void trim();         // return cached memory to the driver
   void release_all();  // free every outstanding allocation (context teardown)
+  void report();       // pool occupancy on stderr (LVN_VERBOSE)
 
  private:
+  void* raw(size_t bytes);
   cudaMemPool_t pool_ = nullptr;
   cudaStream_t stream_ = nullptr;
   std::unordered_set<void*> used_;
+  std::unordered_map<void*, size_t> big_used_;
+  std::multimap<size_t, void*> big_free_;
+};
+
+// Pinned host blocks for results handed to the caller (membership): device
+// to host copies run at full link speed and without first-touch page faults
+// once a block has been used; lvn_result_free returns the block here.
+class HostCache {
+ public:
+  void* get(size_t bytes);
+  bool put(void* p);  // false: not a block of this cache
+  ~HostCache();
+
+ private:
+  std::mutex mu_;
+  std::multimap<size_t, void*> free_;
+  std::unordered_map<void*, size_t> used_;
 };
 
 // Engine context: one device, one stream, pinned scratch for small readbacks.
@@ -90,7 +111,8 @@ struct Context {
   size_t smem_optin = 227 * 1024;
   cudaStream_t stream = nullptr;
   Pool pool;
-  u64* pinned = nullptr;  // 512 u64 of pinned host scratch
+  HostCache host;
+  u64* pinned = nullptr;  // 8192 u64 of pinned host scratch
   std::mutex mu;
 };
 

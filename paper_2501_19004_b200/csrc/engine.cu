@@ -37,7 +37,7 @@ void Pool::bind(int device, cudaStream_t s) {
   stream_ = s;
 }
 
-void* Pool::get(size_t bytes) {
+void* Pool::raw(size_t bytes) {
   void* p = nullptr;
   cudaError_t e = cudaMallocAsync(&p, bytes ? bytes : 1, stream_);
   if (e == cudaErrorMemoryAllocation) {
@@ -50,24 +50,101 @@ void* Pool::get(size_t bytes) {
     fail(e == cudaErrorMemoryAllocation ? kOom : kCuda,
          "cudaMallocAsync(" + std::to_string(bytes) + " bytes): " + cudaGetErrorString(e));
   }
+  return p;
+}
+
+constexpr size_t kBigBytes = size_t(64) << 20;
+
+void* Pool::get(size_t bytes) {
+  if (bytes >= kBigBytes) {
+    const size_t unit = (size_t(1) << (63 - __builtin_clzll(bytes))) / 16;
+    const size_t r = (bytes + unit - 1) / unit * unit;
+    auto it = big_free_.lower_bound(r);
+    void* p = nullptr;
+    size_t have = r;
+    if (it != big_free_.end() && it->first <= r + r / 4) {
+      p = it->second, have = it->first;
+      big_free_.erase(it);
+    } else {
+      p = raw(r);
+    }
+    big_used_[p] = have;
+    return p;
+  }
+  void* p = raw(bytes);
   used_.insert(p);
   return p;
 }
 
 void Pool::put(void* p) {
-  if (!p || !used_.erase(p)) return;
-  (void)cudaFreeAsync(p, stream_);
+  if (!p) return;
+  auto it = big_used_.find(p);
+  if (it != big_used_.end()) {
+    big_free_.emplace(it->second, p);
+    big_used_.erase(it);
+    return;
+  }
+  if (used_.erase(p)) (void)cudaFreeAsync(p, stream_);
 }
 
 void Pool::trim() {
+  for (auto& kv : big_free_) (void)cudaFreeAsync(kv.second, stream_);
+  big_free_.clear();
   (void)cudaStreamSynchronize(stream_);
   if (pool_) (void)cudaMemPoolTrimTo(pool_, 0);
+}
+
+void Pool::report() {
+  std::uint64_t v[4] = {0, 0, 0, 0};
+  (void)cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrReservedMemCurrent, &v[0]);
+  (void)cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrReservedMemHigh, &v[1]);
+  (void)cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemCurrent, &v[2]);
+  (void)cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemHigh, &v[3]);
+  size_t cached = 0;
+  for (auto& kv : big_free_) cached += kv.first;
+  std::fprintf(stderr, "[lvn] pool reserved %.2f GB (high %.2f), used %.2f GB (high %.2f), %zu small + %zu big live, "
+               "%.2f GB big cached\n", v[0] / 1e9, v[1] / 1e9, v[2] / 1e9, v[3] / 1e9, used_.size(), big_used_.size(),
+               cached / 1e9);
 }
 
 void Pool::release_all() {
   for (void* p : used_) (void)cudaFreeAsync(p, stream_);
   used_.clear();
+  for (auto& kv : big_used_) (void)cudaFreeAsync(kv.first, stream_);
+  big_used_.clear();
+  for (auto& kv : big_free_) (void)cudaFreeAsync(kv.second, stream_);
+  big_free_.clear();
   if (stream_) (void)cudaStreamSynchronize(stream_);
+}
+
+void* HostCache::get(size_t bytes) {
+  std::lock_guard<std::mutex> lk(mu_);
+  const size_t r = (bytes + 4095) & ~size_t(4095);
+  auto it = free_.lower_bound(r);
+  void* p = nullptr;
+  size_t have = r;
+  if (it != free_.end() && it->first <= 2 * r) {
+    p = it->second, have = it->first;
+    free_.erase(it);
+  } else {
+    LVN_CUDA(cudaMallocHost(&p, r));
+  }
+  used_[p] = have;
+  return p;
+}
+
+bool HostCache::put(void* p) {
+  std::lock_guard<std::mutex> lk(mu_);
+  auto it = used_.find(p);
+  if (it == used_.end()) return false;
+  free_.emplace(it->second, p);
+  used_.erase(it);
+  return true;
+}
+
+// blocks still held by results are released by lvn_result_free (cudaFreeHost)
+HostCache::~HostCache() {
+  for (auto& kv : free_) (void)cudaFreeHost(kv.second);
 }
 
 static Context* g_ctx = nullptr;
@@ -155,6 +232,7 @@ void validate(const lvn_params& p) {
   if (p.value_bits != 32 && p.value_bits != 64) fail(kInvalid, "value_bits must be 32 or 64");
   if (p.probing < 0 || p.probing > 3) fail(kInvalid, "unknown probing mode");
   if (p.sweep_order != 0 && p.sweep_order != 1) fail(kInvalid, "sweep_order must be 0 or 1");
+  if (p.shard_min_arcs_log2 < 0 || p.shard_min_arcs_log2 > 62) fail(kInvalid, "shard_min_arcs_log2 must be in [0, 62]");
   if (!(p.bin_thread_max <= p.bin_group_max && p.bin_group_max <= p.bin_warp_max &&
         p.bin_warp_max <= p.bin_block_max))
     fail(kInvalid, "degree bin edges must be non-decreasing");
@@ -303,6 +381,67 @@ int sweep_ranges(const lvn_params& p, u32 nv) {
   return int(std::max<u64>(1, std::min<u64>(u64(r), nv)));
 }
 
+// ---- sharded runs: row split and the caller's collectives ---------------------
+// bounds[k] = first row whose offset reaches floor(k A / parts), bounds[parts] = n
+__host__ __device__ inline u64 split_target(u64 A, int parts, int k) {
+  return A / u64(parts) * u64(k) + (A % u64(parts)) * u64(k) / u64(parts);
+}
+__global__ void split_rows_k(const u64* __restrict__ off, u32 n, int parts, u32* __restrict__ bounds) {
+  const int k = threadIdx.x;
+  if (k > parts) return;
+  if (k == parts) {
+    bounds[k] = n;
+    return;
+  }
+  const u64 target = split_target(off[n], parts, k);
+  u32 lo = 0, hi = n;
+  while (lo < hi) {
+    const u32 mid = lo + (hi - lo) / 2;
+    if (off[mid] >= target) hi = mid; else lo = mid + 1;
+  }
+  bounds[k] = lo;
+}
+std::vector<u32> split_rows(const u64* off, u32 n, int parts, cudaStream_t s) {
+  DBuf<u32> b(parts + 1);
+  split_rows_k<<<1, 1024, 0, s>>>(off, n, parts, b.p);
+  LVN_LAUNCH();
+  std::vector<u32> h(parts + 1);
+  LVN_CUDA(cudaMemcpyAsync(ctx().pinned, b.p, (parts + 1) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(h.data(), ctx().pinned, (parts + 1) * sizeof(u32));
+  return h;
+}
+
+struct Comm {
+  const lvn_comm* c = nullptr;
+  double seconds = 0.0;
+  bool on() const { return c && c->size > 1; }
+  int rank() const { return c ? c->rank : 0; }
+  int size() const { return c ? c->size : 1; }
+  void allreduce(void* buf, u64 count, int dtype, int op, cudaStream_t s) {
+    LVN_CUDA(cudaStreamSynchronize(s));
+    const auto t0 = Clock::now();
+    if (c->allreduce(c->user, buf, count, dtype, op) != 0) fail(kCuda, "allreduce collective failed");
+    seconds += since(t0);
+  }
+  void allgatherv(const void* send, void* recv, const std::vector<u64>& counts, cudaStream_t s) {
+    LVN_CUDA(cudaStreamSynchronize(s));
+    const auto t0 = Clock::now();
+    if (c->allgatherv(c->user, send, recv, counts.data()) != 0) fail(kCuda, "allgatherv collective failed");
+    seconds += since(t0);
+  }
+};
+
+__global__ void sigma_delta_k(double* __restrict__ S, const double* __restrict__ S0, u64 n, int apply) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
+    S[i] = apply ? S0[i] + S[i] : S[i] - S0[i];
+}
+void sigma_delta(double* S, const double* S0, u64 n, bool apply, cudaStream_t s) {
+  if (!n) return;
+  sigma_delta_k<<<unsigned(std::min<u64>((n + 255) / 256, u64(sm_count()) * 8)), 256, 0, s>>>(S, S0, n, apply);
+  LVN_LAUNCH();
+}
+
 // ---- renumbering: ids of C (all < width) -> 0..count-1 ascending, returns count
 u32 renumber_device(u32* C, u64 n, u64 width, DBuf<u32>& used, DBuf<u32>& rank, cudaStream_t s,
                     bool apply) {
@@ -327,8 +466,12 @@ bool verbose() {
 }
 
 // ---- aggregation of a graph by a contiguous membership ----------------------
+// With a sharding comm, rank r emits the super-rows of communities
+// [cb[r], cb[r+1]) (split by member-degree budget) and the ranks allgather the
+// row lengths and then the rows, so every rank ends with the whole super-graph.
 void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
-                      u32* err, cudaStream_t s, bool canonical) {
+                      u32* err, cudaStream_t s, bool canonical, Comm* comm = nullptr) {
+  const bool sh = comm && comm->on();
   DBuf<u32> msize(count ? count : 1);
   DBuf<u64> budget(count + 1), coff(count + 1), boff(count + 1), hoff(count + 1), capped(count + 1);
   community_counts(g, C, count, msize.p, budget.p, s);
@@ -340,8 +483,14 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   DBuf<u32> members(g.n ? g.n : 1), cursor(count ? count : 1);
   community_scatter(C, g.n, coff.p, count, cursor.p, members.p, s);
   msize.release();
+  std::vector<u32> cb;
+  u32 c0 = 0, c1 = count;
+  if (sh) {
+    cb = split_rows(boff.p, count, comm->size(), s);
+    c0 = cb[comm->rank()], c1 = cb[comm->rank() + 1];
+  }
   Bins ab;
-  compute_bins(boff.p, count, e, ab, s);  // synchronises
+  compute_bins(boff.p + c0, c1 - c0, e, ab, s, ~u64(0), c0);  // synchronises
   const u64 H = read_scalar(hoff.p + count, s);
   DBuf<u32> htgt(H ? H : 1), fill(count ? count : 1);
   DBuf<float> hw(H ? H : 1);
@@ -392,8 +541,18 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
                             std::to_string(h_coff[c + 1] - h_coff[c]) + ")");
     }
   }
+  // rows of other ranks' communities stay empty in `fill`; `fill_all` holds every row
+  DBuf<u32> fill_all;
+  const u32* rows = fill.p;
+  if (sh) {
+    fill_all.alloc(count ? count : 1);
+    std::vector<u64> bytes(comm->size());
+    for (int k = 0; k < comm->size(); ++k) bytes[k] = 4ull * (cb[k + 1] - cb[k]);
+    comm->allgatherv(fill.p + c0, fill_all.p, bytes, s);
+    rows = fill_all.p;
+  }
   DBuf<u64> noff(count + 1);
-  exclusive_scan_u32_to_u64(fill.p, noff.p, count, s);
+  exclusive_scan_u32_to_u64(rows, noff.p, count, s);
   const u64 A = read_scalar(noff.p + count, s);
   out.n = count;
   out.arcs = A;
@@ -402,9 +561,22 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   out.w.alloc(A ? A : 1);
   DBuf<double> tw(1);
   compact_rows(hoff.p, htgt.p, hw.p, fill.p, out.off.p, count, out.tgt.p, out.w.p, tw.p, s);
+  if (sh) {
+    std::vector<u64> at(comm->size() + 1);
+    for (int k = 0; k <= comm->size(); ++k)
+      LVN_CUDA(cudaMemcpyAsync(ctx().pinned + k, out.off.p + cb[k], sizeof(u64), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    for (int k = 0; k <= comm->size(); ++k) at[k] = ctx().pinned[k];
+    std::vector<u64> tb(comm->size()), wb(comm->size());
+    for (int k = 0; k < comm->size(); ++k) tb[k] = 4ull * (at[k + 1] - at[k]), wb[k] = tb[k];
+    const u64 mine = at[comm->rank()];
+    comm->allgatherv(out.tgt.p + mine, out.tgt.p, tb, s);
+    comm->allgatherv(out.w.p + mine, out.w.p, wb, s);
+    comm->allreduce(tw.p, 1, LVN_F64, LVN_SUM, s);
+  }
   if (canonical && A) {
     DBuf<u32> mx(1);
-    reduce_max_u32(fill.p, count, mx.p, s);
+    reduce_max_u32(rows, count, mx.p, s);
     const u32 max_row = read_scalar(mx.p, s);
     segmented_sort_u32(out.tgt.p, out.w.p, out.off.p, count, max_row, s);
   }
@@ -474,7 +646,11 @@ void check_err(const u32* err, cudaStream_t s) {
 // ---------------------------------------------------------------------------
 // Louvain pass shell
 // ---------------------------------------------------------------------------
-void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
+// comm (lvn_louvain_sharded): passes with >= 2^shard_min_arcs_log2 arcs are
+// sharded by row range across the ranks; every rank keeps the
+// whole current graph, the replicated C / Sigma / flags, and ends with the same
+// result (the passes that run whole run redundantly on every rank).
+void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* comm = nullptr) {
   const auto t_start = Clock::now();
   Context& c = ctx();
   cudaStream_t s = c.stream;
@@ -507,7 +683,11 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
   std::vector<double> tols, pass_secs;
   std::vector<u32> vpp;
   std::vector<u64> app;
-  int passes = 0, aggregations = 0;
+  int passes = 0, aggregations = 0, sharded_passes = 0;
+  Comm solo;
+  Comm& cm = comm ? *comm : solo;
+  DBuf<double> S0;
+  Bins own_bins;
 
   for (int pass = 0; pass < p.max_passes; ++pass) {
     const auto t_pass = Clock::now();
@@ -519,6 +699,18 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
     pass_reset(cur, B, K.p, S.p, C.p, flags.p, s);
     tm.end(sp, s, 4.0 * double(cur.arcs) + 29.0 * nv);
 
+    // sharded pass: this rank decides the rows [v0, v1)
+    const bool shard = cm.on() && cur.arcs >= (u64(1) << p.shard_min_arcs_log2);
+    u32 v0 = 0, v1 = nv;
+    std::vector<u32> vb;
+    if (shard) {
+      vb = split_rows(cur.off, nv, cm.size(), s);
+      v0 = vb[cm.rank()], v1 = vb[cm.rank() + 1];
+      compute_bins(cur.off + v0, v1 - v0, edges, own_bins, s, ~u64(0), v0);
+      S0.ensure(nv ? nv : 1);
+      ++sharded_passes;
+    }
+    Bins& SB = shard ? own_bins : B;
     MoveArgs a;
     a.g = cur;
     a.C = C.p;
@@ -537,15 +729,15 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
       fill_u32(csize.p, nv, 1u, s);
       a.csize = csize.p;
     }
-    if (B.count(kBinGlobal)) {
-      hub_plan_build(cur, B.of(kBinGlobal), B.count(kBinGlobal), p.value_bits, hubs, s);
+    if (SB.count(kBinGlobal)) {
+      hub_plan_build(cur, SB.of(kBinGlobal), SB.count(kBinGlobal), p.value_bits, hubs, s);
       hubs.attach(a);
     }
     // A sweep visits R consecutive vertex-id ranges in order, each with its own
     // degree bins: within a range the degree classes run low to high (the
     // reference compact order), across ranges the sweep follows vertex ids
     // like louvain_mc's, which matters for quality on skewed graphs.
-    const int R = sweep_ranges(p, nv);
+    const int R = shard ? 1 : sweep_ranges(p, nv);
     std::vector<Bins> rbins(R > 1 ? R : 0);
     std::vector<u64> rbase(R + 1);
     for (int k = 0; k <= R; ++k) rbase[k] = u64(nv) * k / R;
@@ -554,7 +746,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
       if (R > 1)
         compute_bins(cur.off + rbase[k], u32(rbase[k + 1] - rbase[k]), edges, rbins[k], s, ~u64(0),
                      u32(rbase[k]));
-      views[k] = R > 1 ? rbins[k].view() : B.view();
+      views[k] = R > 1 ? rbins[k].view() : SB.view();
     }
     const auto t0 = Clock::now();
     int iterations = 0;
@@ -564,12 +756,30 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
     for (int it = 0; it < p.max_iterations; ++it) {
       a.pickless = pick_less_active(it, p.pick_less_period);
       LVN_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(IterRecord), s));
+      if (shard) {
+        // Sigma deltas of this sweep are taken against S0; marks of other
+        // ranks' rows start at 0 so the max-allreduce ORs in remote marks only
+        LVN_CUDA(cudaMemcpyAsync(S0.p, S.p, u64(nv) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+        if (v0) LVN_CUDA(cudaMemsetAsync(flags.p, 0, v0, s));
+        if (nv > v1) LVN_CUDA(cudaMemsetAsync(flags.p + v1, 0, nv - v1, s));
+      }
       sp = tm.begin(LVN_STAT_MOVE, s);
       for (int k = 0; k < R; ++k) move_sweep(a, views[k], p.value_bits, s);
       tm.end(sp, s, 0.0);
+      if (shard) {
+        sigma_delta(S.p, S0.p, nv, false, s);
+        cm.allreduce(S.p, nv, LVN_F64, LVN_SUM, s);
+        sigma_delta(S.p, S0.p, nv, true, s);
+        std::vector<u64> cnt(cm.size());
+        for (int k = 0; k < cm.size(); ++k) cnt[k] = 4ull * (vb[k + 1] - vb[k]);
+        cm.allgatherv(C.p + v0, C.p, cnt, s);
+        cm.allreduce(flags.p, nv, LVN_U8, LVN_MAX, s);
+        cm.allreduce(&rec.p->gain, 1, LVN_F64, LVN_SUM, s);
+        cm.allreduce(&rec.p->verts, 3, LVN_U64, LVN_SUM, s);
+      }
       if (p.prune)
         for (int k = 0; k < R; ++k)
-          compact_active(R > 1 ? rbins[k] : B, flags.p, active.p + rbase[k], rec.p->active + k * kBins, s);
+          compact_active(R > 1 ? rbins[k] : SB, flags.p, active.p + rbase[k], rec.p->active + k * kBins, s);
       IterRecord* h = reinterpret_cast<IterRecord*>(c.pinned);
       LVN_CUDA(cudaMemcpyAsync(h, rec.p, sizeof(IterRecord), cudaMemcpyDeviceToHost, s));
       LVN_CUDA(cudaStreamSynchronize(s));
@@ -619,7 +829,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
     const auto t1 = Clock::now();
     OwnedCsr& next = owned[pass & 1];
     sp = tm.begin(LVN_STAT_AGGREGATE, s);
-    aggregate_device(cur, C.p, count, edges, next, err.p, s, false);
+    aggregate_device(cur, C.p, count, edges, next, err.p, s, false, shard ? &cm : nullptr);
     tm.end(sp, s, 12.0 * double(cur.arcs) + 16.0 * nv + 8.0 * double(next.arcs) + 8.0 * (count + 1.0),
            nv, cur.arcs);
     t_aggregate += since(t1);
@@ -667,8 +877,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
     global.n = 0;
     r->membership_on_device = 1;
   } else {
-    r->membership = static_cast<u32*>(std::malloc(size_t(N ? N : 1) * sizeof(u32)));
-    if (!r->membership) fail(kOom, "host allocation of the membership failed");
+    r->membership = static_cast<u32*>(c.host.get(size_t(N ? N : 1) * sizeof(u32)));
     if (N) LVN_CUDA(cudaMemcpyAsync(r->membership, global.p, size_t(N) * sizeof(u32), cudaMemcpyDeviceToHost, s));
     LVN_CUDA(cudaStreamSynchronize(s));
     r->membership_on_device = 0;
@@ -676,6 +885,10 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r) {
   r->d2h_seconds = since(t_d2h);
   tm.collect(r->stats);
   r->wall_seconds = since(t_start);
+  if (verbose()) c.pool.report();
+  r->num_shards = cm.size();
+  r->sharded_passes = sharded_passes;
+  r->exchange_seconds = cm.seconds;
   r->local_moving = t_move;
   r->aggregation = t_aggregate;
   r->other = r->wall_seconds - t_move - t_aggregate;
@@ -761,6 +974,7 @@ void lvn_params_default(lvn_params* p) {
   p->sweep_order = 0;
   p->sweep_ranges = 0;
   p->singleton_rule = 0;
+  p->shard_min_arcs_log2 = 22;
 }
 
 int lvn_init(int num_gpus, const int* devices) {
@@ -788,8 +1002,8 @@ void lvn_result_free(lvn_result* r) {
         ctx().pool.put(r->membership);
       } catch (...) {
       }
-    } else {
-      std::free(r->membership);
+    } else if (!(lvn::g_ctx && lvn::g_ctx->host.put(r->membership))) {
+      (void)cudaFreeHost(r->membership);  // pinned block that outlived its context
     }
   }
   std::free(r->iterations_per_pass);
@@ -806,6 +1020,51 @@ void lvn_graph_free(lvn_graph_out* g) {
   std::free(g->targets);
   std::free(g->weights);
   delete g;
+}
+
+int lvn_louvain_sharded(const lvn_csr* g, const lvn_params* p, const lvn_comm* comm, lvn_result** out) {
+  if (!out) {
+    t_err = "null output";
+    return kInvalid;
+  }
+  *out = nullptr;
+  if (!comm || comm->size < 1 || comm->rank < 0 || comm->rank >= comm->size || comm->size > 1024 ||
+      (comm->size > 1 && (!comm->allreduce || !comm->allgatherv))) {
+    t_err = "invalid lvn_comm (rank/size out of range or missing collectives)";
+    return kInvalid;
+  }
+  lvn_params def;
+  lvn_params_default(&def);
+  auto* r = new lvn_result;
+  std::memset(r, 0, sizeof(*r));
+  lvn::Comm cm;
+  cm.c = comm;
+  const int rc = guard([&](Context&) { run_louvain(g, p ? *p : def, r, &cm); });
+  if (rc) {
+    lvn_result_free(r);
+    return rc;
+  }
+  *out = r;
+  return kOk;
+}
+
+int lvn_partition_rows(const uint64_t* offsets, uint32_t n, int parts, uint32_t* bounds) {
+  if (!offsets || !bounds || parts < 1 || parts > 1024) {
+    t_err = "invalid arguments to lvn_partition_rows";
+    return kInvalid;
+  }
+  const uint64_t A = offsets[n];
+  for (int k = 0; k < parts; ++k) {
+    const uint64_t target = lvn::split_target(A, parts, k);
+    uint32_t lo = 0, hi = n;
+    while (lo < hi) {
+      const uint32_t mid = lo + (hi - lo) / 2;
+      if (offsets[mid] >= target) hi = mid; else lo = mid + 1;
+    }
+    bounds[k] = lo;
+  }
+  bounds[parts] = n;
+  return kOk;
 }
 
 int lvn_louvain(const lvn_csr* g, const lvn_params* p, lvn_result** out) {

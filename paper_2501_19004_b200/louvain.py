@@ -127,6 +127,7 @@ class CompactOptions:  # louvain_compact.hpp:35-40
     sweep_order: int = 0  # 0 low degree first (reference compact order), 1 hubs first
     sweep_ranges: int = 0  # vertex-id ranges per sweep (1 = compact order); 0 automatic
     singleton_rule: bool = False  # singleton joins singleton only toward the lower id
+    shard_min_arcs_log2: int = 22  # louvain_sharded: shard passes with >= 2**this arcs
 
 
 @dataclass
@@ -169,6 +170,9 @@ class LouvainResult:  # louvain.hpp:28-39 (+ device breakdown)
     h2d_seconds: float = 0.0
     d2h_seconds: float = 0.0
     stats: dict = field(default_factory=dict)
+    num_shards: int = 1
+    sharded_passes: int = 0
+    exchange_seconds: float = 0.0
 
 
 @dataclass
@@ -310,6 +314,7 @@ def _params(params: LouvainParams | None, options: CompactOptions | None, on_dev
     p.sweep_order = options.sweep_order
     p.sweep_ranges = options.sweep_ranges
     p.singleton_rule = int(bool(options.singleton_rule))
+    p.shard_min_arcs_log2 = options.shard_min_arcs_log2
     return p
 
 
@@ -340,6 +345,47 @@ def louvain_compact(g, params: LouvainParams | None = None, options: CompactOpti
     csr = g._csr()
     out = C.POINTER(N.lvn_result)()
     _check(N.lib().lvn_louvain(C.byref(csr), C.byref(p), C.byref(out)))
+    return _result(out)
+
+
+def louvain_sharded(g, comm, params: LouvainParams | None = None, options: CompactOptions | None = None,
+                    membership_on_device: bool = False) -> LouvainResult:
+    """louvain_compact sharded over the ranks of `comm` (one process per GPU,
+    SURVEY.md 8(e)); `comm` is a paper_2501_19004_b200.distributed.Collectives
+    (or anything exposing a ctypes `lvn_comm` as `.struct`). Every rank passes
+    the same graph and gets the same result."""
+    p = _params(params, options, membership_on_device)
+    csr = g._csr()
+    out = C.POINTER(N.lvn_result)()
+    _check(N.lib().lvn_louvain_sharded(C.byref(csr), C.byref(p), C.byref(comm.struct), C.byref(out)))
+    return _result(out)
+
+
+def partition_rows(offsets, parts: int) -> np.ndarray:
+    """Row split of a sharded pass: bounds[k] = first row whose offset reaches
+    floor(k*A/parts), bounds[parts] = n (the engine's rule, host copy)."""
+    off = np.ascontiguousarray(offsets, dtype=np.uint64)
+    n = len(off) - 1
+    out = np.empty(parts + 1, np.uint32)
+    _check(N.lib().lvn_partition_rows(off.ctypes.data, n, parts, out.ctypes.data))
+    return out
+
+
+class _ResultHandle:
+    """Keeps an lvn_result alive while its device membership is in use."""
+
+    def __init__(self, out):
+        self.out = out
+
+    def __del__(self):
+        try:
+            N.lib().lvn_result_free(self.out)
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
+def _result(out) -> LouvainResult:
+    keep = False
     try:
         r = out.contents
         k = r.passes
@@ -367,11 +413,18 @@ def louvain_compact(g, params: LouvainParams | None = None, options: CompactOpti
             d2h_seconds=r.d2h_seconds,
             stats={name: KernelStats(s.seconds, s.bytes, s.launches, s.items, s.arcs)
                    for name, s in zip(N.STAT_NAMES, r.stats)},
+            num_shards=max(r.num_shards, 1),
+            sharded_passes=r.sharded_passes,
+            exchange_seconds=r.exchange_seconds,
         )
         res.membership_device_ptr = dev_ptr
+        if dev_ptr is not None:  # valid while the result object lives
+            res._handle = _ResultHandle(out)
+            keep = True
         return res
     finally:
-        N.lib().lvn_result_free(out)
+        if not keep:
+            N.lib().lvn_result_free(out)
 
 
 louvain_gpu = louvain_compact

@@ -52,6 +52,8 @@ int main(void) {
          sizeof(lvn_gen_params), sizeof(lvn_graph_out));
   printf("%zu %zu %zu\n", offsetof(lvn_params, value_bits), offsetof(lvn_result, stats),
          offsetof(lvn_result, membership_on_device));
+  printf("%zu %zu %zu %zu\n", sizeof(lvn_comm), offsetof(lvn_comm, allgatherv),
+         offsetof(lvn_params, shard_min_arcs_log2), offsetof(lvn_result, exchange_seconds));
   return 0;
 }'''
     with tempfile.TemporaryDirectory() as d:
@@ -66,6 +68,8 @@ int main(void) {
     assert sizes[5] == N.lvn_params.value_bits.offset
     assert sizes[6] == N.lvn_result.stats.offset
     assert sizes[7] == N.lvn_result.membership_on_device.offset
+    assert sizes[8:] == [C.sizeof(N.lvn_comm), N.lvn_comm.allgatherv.offset,
+                         N.lvn_params.shard_min_arcs_log2.offset, N.lvn_result.exchange_seconds.offset]
 
 
 def test_params_defaults_mirror_reference():
