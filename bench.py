@@ -207,6 +207,7 @@ def main():
     ap.add_argument("--value-bits", type=int, default=32)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--shard-rounds", type=int, default=0, help="N>1: exchanges per local-moving iteration (0 = 2N)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -247,7 +248,7 @@ def main():
     dg = lvn.generate(cfg["kind"], **{k: v for k, v in cfg.items() if k not in ("kind", "desc")})
     n, arcs = dg.num_vertices(), dg.num_arcs()
     log(f"[rank {rank}] {args.config}: {n} vertices, {arcs} arcs, generated in {time.time() - t0:.1f}s")
-    opts = lvn.CompactOptions(value_bits=args.value_bits)
+    opts = lvn.CompactOptions(value_bits=args.value_bits, shard_rounds=args.shard_rounds)
     # N > 1: one process per GPU, passes sharded by row range over NCCL
     # (SURVEY.md 8(e)); the whole job's work is fixed as N grows (strong scaling)
     comm = None

@@ -114,7 +114,11 @@ typedef struct lvn_params {
    * has at least 2^shard_min_arcs_log2 arcs; smaller graphs run whole on
    * every rank (the collapse of SURVEY.md 8(e)) */
   int shard_min_arcs_log2;      /* 22 */
-  int reserved[2];
+  /* lvn_louvain_sharded: each rank sweeps its rows in this many consecutive
+   * rounds per iteration, exchanging Sigma / C / marks after each (more
+   * rounds: fresher cross-rank state, more collectives); 0 = 2 x ranks */
+  int shard_rounds;             /* 0 */
+  int reserved[1];
 } lvn_params;
 
 /* Per-kernel-family device accounting (CUDA events on the engine stream). */
@@ -201,11 +205,12 @@ int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const doubl
  * One process per GPU, each calling lvn_louvain_sharded on the same graph (its
  * own device copy, or host input it uploads). A sharded pass gives rank r the
  * rows [bounds[r], bounds[r+1]) of lvn_partition_rows: it decides the moves of
- * those vertices against replicated membership C and community weights Sigma,
- * then per iteration the ranks allreduce the Sigma deltas (f64 sum), the
- * neighbour marks (u8 max), the gain and counters, and allgather C of their
- * rows; aggregation emits the super-rows of a community range per rank and
- * allgathers them. Passes whose graph has fewer than 2^shard_min_arcs_log2
+ * those vertices against replicated membership C and community weights Sigma
+ * in shard_rounds consecutive rounds per iteration; after each round the ranks
+ * allgather their move records (u, to) and every rank applies the others'
+ * (C, Sigma, neighbour marks); gain and counters are allreduced once per
+ * iteration. Aggregation emits the super-rows of a community range per rank
+ * and allgathers them. Passes whose graph has fewer than 2^shard_min_arcs_log2
  * arcs run whole on every rank. The collectives are supplied by the caller
  * (paper_2501_19004_b200.distributed wraps torch.distributed / NCCL): buffers
  * are device pointers on this process's GPU, the library's stream is idle

@@ -66,7 +66,8 @@ class lvn_params(C.Structure):
         ("sweep_ranges", C.c_int),
         ("singleton_rule", C.c_int),
         ("shard_min_arcs_log2", C.c_int),
-        ("reserved", C.c_int * 2),
+        ("shard_rounds", C.c_int),
+        ("reserved", C.c_int * 1),
     ]
 
 

@@ -233,6 +233,7 @@ void validate(const lvn_params& p) {
   if (p.probing < 0 || p.probing > 3) fail(kInvalid, "unknown probing mode");
   if (p.sweep_order != 0 && p.sweep_order != 1) fail(kInvalid, "sweep_order must be 0 or 1");
   if (p.shard_min_arcs_log2 < 0 || p.shard_min_arcs_log2 > 62) fail(kInvalid, "shard_min_arcs_log2 must be in [0, 62]");
+  if (p.shard_rounds < 0 || p.shard_rounds > 64) fail(kInvalid, "shard_rounds must be in [0, 64]");
   if (!(p.bin_thread_max <= p.bin_group_max && p.bin_group_max <= p.bin_warp_max &&
         p.bin_warp_max <= p.bin_block_max))
     fail(kInvalid, "degree bin edges must be non-decreasing");
@@ -431,16 +432,6 @@ struct Comm {
     seconds += since(t0);
   }
 };
-
-__global__ void sigma_delta_k(double* __restrict__ S, const double* __restrict__ S0, u64 n, int apply) {
-  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
-    S[i] = apply ? S0[i] + S[i] : S[i] - S0[i];
-}
-void sigma_delta(double* S, const double* S0, u64 n, bool apply, cudaStream_t s) {
-  if (!n) return;
-  sigma_delta_k<<<unsigned(std::min<u64>((n + 255) / 256, u64(sm_count()) * 8)), 256, 0, s>>>(S, S0, n, apply);
-  LVN_LAUNCH();
-}
 
 // ---- renumbering: ids of C (all < width) -> 0..count-1 ascending, returns count
 u32 renumber_device(u32* C, u64 n, u64 width, DBuf<u32>& used, DBuf<u32>& rank, cudaStream_t s,
@@ -686,8 +677,8 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   int passes = 0, aggregations = 0, sharded_passes = 0;
   Comm solo;
   Comm& cm = comm ? *comm : solo;
-  DBuf<double> S0;
   Bins own_bins;
+  DBuf<u32> mrec, mall, mcount;  // sharded: own move records (u, to), everyone's, per-rank counts
 
   for (int pass = 0; pass < p.max_passes; ++pass) {
     const auto t_pass = Clock::now();
@@ -707,7 +698,8 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       vb = split_rows(cur.off, nv, cm.size(), s);
       v0 = vb[cm.rank()], v1 = vb[cm.rank() + 1];
       compute_bins(cur.off + v0, v1 - v0, edges, own_bins, s, ~u64(0), v0);
-      S0.ensure(nv ? nv : 1);
+      mrec.ensure(2 * u64(std::max<u32>(v1 - v0, 1)));
+      mcount.ensure(cm.size() + 1);
       ++sharded_passes;
     }
     Bins& SB = shard ? own_bins : B;
@@ -729,6 +721,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       fill_u32(csize.p, nv, 1u, s);
       a.csize = csize.p;
     }
+    if (shard) a.moves_out = mrec.p, a.moves_n = mcount.p + cm.size();
     if (SB.count(kBinGlobal)) {
       hub_plan_build(cur, SB.of(kBinGlobal), SB.count(kBinGlobal), p.value_bits, hubs, s);
       hubs.attach(a);
@@ -737,10 +730,13 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     // degree bins: within a range the degree classes run low to high (the
     // reference compact order), across ranges the sweep follows vertex ids
     // like louvain_mc's, which matters for quality on skewed graphs.
-    const int R = shard ? 1 : sweep_ranges(p, nv);
+    // Sharded: the own rows are swept in R = shard_rounds consecutive ranges
+    // with an exchange after each, so later rounds see the other ranks' moves.
+    const int R = shard ? std::max(1, std::min(p.shard_rounds ? p.shard_rounds : 2 * cm.size(), kMaxRanges))
+                        : sweep_ranges(p, nv);
     std::vector<Bins> rbins(R > 1 ? R : 0);
     std::vector<u64> rbase(R + 1);
-    for (int k = 0; k <= R; ++k) rbase[k] = u64(nv) * k / R;
+    for (int k = 0; k <= R; ++k) rbase[k] = v0 + u64(v1 - v0) * k / R;
     std::vector<BinView> views(R);
     for (int k = 0; k < R; ++k) {
       if (R > 1)
@@ -756,24 +752,37 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     for (int it = 0; it < p.max_iterations; ++it) {
       a.pickless = pick_less_active(it, p.pick_less_period);
       LVN_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(IterRecord), s));
-      if (shard) {
-        // Sigma deltas of this sweep are taken against S0; marks of other
-        // ranks' rows start at 0 so the max-allreduce ORs in remote marks only
-        LVN_CUDA(cudaMemcpyAsync(S0.p, S.p, u64(nv) * sizeof(double), cudaMemcpyDeviceToDevice, s));
-        if (v0) LVN_CUDA(cudaMemsetAsync(flags.p, 0, v0, s));
-        if (nv > v1) LVN_CUDA(cudaMemsetAsync(flags.p + v1, 0, nv - v1, s));
+      size_t sp0 = 0;
+      for (int k = 0; k < R; ++k) {
+        if (shard) LVN_CUDA(cudaMemsetAsync(a.moves_n, 0, sizeof(u32), s));
+        sp = tm.begin(LVN_STAT_MOVE, s);
+        if (k == 0) sp0 = sp;
+        move_sweep(a, views[k], p.value_bits, s);
+        tm.end(sp, s, 0.0);
+        if (shard) {
+          // every rank applies the other ranks' moves of this round (C, Sigma,
+          // neighbour marks) from their (u, to) records
+          std::vector<u64> four(cm.size(), 4);
+          cm.allgatherv(a.moves_n, mcount.p, four, s);
+          u32* hn = reinterpret_cast<u32*>(c.pinned);
+          LVN_CUDA(cudaMemcpyAsync(hn, mcount.p, cm.size() * sizeof(u32), cudaMemcpyDeviceToHost, s));
+          LVN_CUDA(cudaStreamSynchronize(s));
+          std::vector<u64> bytes(cm.size());
+          u64 total = 0, mine = 0;
+          for (int j = 0; j < cm.size(); ++j) {
+            if (j == cm.rank()) mine = total;
+            bytes[j] = 8ull * hn[j];
+            total += hn[j];
+          }
+          if (total) {
+            mall.ensure(2 * total);
+            cm.allgatherv(mrec.p, mall.p, bytes, s);
+            apply_moves(mall.p, total, mine, mine + hn[cm.rank()], cur, C.p, K.p, S.p, flags.p, p.prune, s);
+          }
+        }
       }
-      sp = tm.begin(LVN_STAT_MOVE, s);
-      for (int k = 0; k < R; ++k) move_sweep(a, views[k], p.value_bits, s);
-      tm.end(sp, s, 0.0);
+      sp = sp0;
       if (shard) {
-        sigma_delta(S.p, S0.p, nv, false, s);
-        cm.allreduce(S.p, nv, LVN_F64, LVN_SUM, s);
-        sigma_delta(S.p, S0.p, nv, true, s);
-        std::vector<u64> cnt(cm.size());
-        for (int k = 0; k < cm.size(); ++k) cnt[k] = 4ull * (vb[k + 1] - vb[k]);
-        cm.allgatherv(C.p + v0, C.p, cnt, s);
-        cm.allreduce(flags.p, nv, LVN_U8, LVN_MAX, s);
         cm.allreduce(&rec.p->gain, 1, LVN_F64, LVN_SUM, s);
         cm.allreduce(&rec.p->verts, 3, LVN_U64, LVN_SUM, s);
       }
@@ -975,6 +984,7 @@ void lvn_params_default(lvn_params* p) {
   p->sweep_ranges = 0;
   p->singleton_rule = 0;
   p->shard_min_arcs_log2 = 22;
+  p->shard_rounds = 0;
 }
 
 int lvn_init(int num_gpus, const int* devices) {

@@ -93,6 +93,9 @@ struct MoveArgs {
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
   int hubs_first = 0;          // bin order of a sweep: highest degree class first
   u32* csize = nullptr;        // community member counts (singleton-pair rule), or null
+  // sharded runs: every applied move appends (u, to) here (count in *moves_n)
+  u32* moves_out = nullptr;
+  u32* moves_n = nullptr;
   // hub plan of the pass (kBinGlobal vertices): see HubPlan
   const u32* hub_index = nullptr;
   const u64* hub_tab_off = nullptr;
@@ -118,6 +121,11 @@ struct HubPlan {
 };
 void hub_plan_build(const DGraph& g, const u32* hubs, u64 count, int value_bits, HubPlan& p,
                     cudaStream_t s);
+// remote moves of a sharded round: records (u, to) pairs [0, total) except
+// [skip_lo, skip_hi) (this rank's own, already applied): C[u] = to, Sigma moves
+// K[u] from C[u] to `to`, and u's neighbours are flagged when prune is set
+void apply_moves(const u32* rec, u64 total, u64 skip_lo, u64 skip_hi, const DGraph& g, u32* C, const double* K,
+                 double* sigma, u8* flags, int prune, cudaStream_t s);
 // one sweep over the bins of `bins` (see the kBin* classes)
 void move_sweep(const MoveArgs& a, const BinView& bins, int value_bits, cudaStream_t s);
 

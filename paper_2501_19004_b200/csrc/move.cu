@@ -119,6 +119,14 @@ __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, doubl
     if (g > 0.0) {
       atomicAdd(&x.sigma[from], -ku);
       x.C[u] = bc;
+      if (x.moves_out) {  // sharded: record the move for the other ranks
+        const auto grp = cg::coalesced_threads();
+        u32 base = 0;
+        if (grp.thread_rank() == 0) base = atomicAdd(x.moves_n, grp.size());
+        const u32 i = grp.shfl(base, 0) + grp.thread_rank();
+        x.moves_out[2 * u64(i)] = u;
+        x.moves_out[2 * u64(i) + 1] = bc;
+      }
       if (x.csize) {
         atomicSub(&x.csize[from], 1u);
         atomicAdd(&x.csize[bc], 1u);
@@ -1060,7 +1068,35 @@ void hub_plan_impl(const DGraph& g, const u32* hubs, u64 count, HubPlan& p, cuda
   LVN_CUDA(cudaMemsetAsync(p.own.p, 0, count * sizeof(double), s));
 }
 
+__global__ void apply_moves_k(const u32* __restrict__ rec, u64 total, u64 skip_lo, u64 skip_hi, DGraph g,
+                              u32* __restrict__ C, const double* __restrict__ K, double* __restrict__ sigma,
+                              u8* __restrict__ flags, int prune) {
+  const u32 lane = threadIdx.x & 31;
+  const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
+  for (u64 i = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; i < total; i += warps) {
+    if (i >= skip_lo && i < skip_hi) continue;
+    const u32 u = rec[2 * i], to = rec[2 * i + 1];
+    if (lane == 0) {
+      const u32 from = C[u];
+      const double ku = K[u];
+      C[u] = to;
+      atomicAdd(&sigma[to], ku);
+      atomicAdd(&sigma[from], -ku);
+    }
+    if (prune)
+      for (u64 a = g.off[u] + lane; a < g.off[u + 1]; a += 32) flags[g.tgt[a]] = 1;
+  }
+}
+
 }  // namespace
+
+void apply_moves(const u32* rec, u64 total, u64 skip_lo, u64 skip_hi, const DGraph& g, u32* C, const double* K,
+                 double* sigma, u8* flags, int prune, cudaStream_t s) {
+  if (total <= skip_hi - skip_lo) return;
+  const u64 blocks = std::min<u64>((total + 7) / 8, u64(sm_count()) * 16);
+  apply_moves_k<<<unsigned(blocks), 256, 0, s>>>(rec, total, skip_lo, skip_hi, g, C, K, sigma, flags, prune);
+  LVN_LAUNCH();
+}
 
 void hub_plan_build(const DGraph& g, const u32* hubs, u64 count, int value_bits, HubPlan& p,
                     cudaStream_t s) {

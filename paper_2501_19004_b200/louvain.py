@@ -128,6 +128,7 @@ class CompactOptions:  # louvain_compact.hpp:35-40
     sweep_ranges: int = 0  # vertex-id ranges per sweep (1 = compact order); 0 automatic
     singleton_rule: bool = False  # singleton joins singleton only toward the lower id
     shard_min_arcs_log2: int = 22  # louvain_sharded: shard passes with >= 2**this arcs
+    shard_rounds: int = 0  # louvain_sharded: exchanges per iteration (rounds over own rows); 0 = 2 x ranks
 
 
 @dataclass
@@ -315,6 +316,7 @@ def _params(params: LouvainParams | None, options: CompactOptions | None, on_dev
     p.sweep_ranges = options.sweep_ranges
     p.singleton_rule = int(bool(options.singleton_rule))
     p.shard_min_arcs_log2 = options.shard_min_arcs_log2
+    p.shard_rounds = options.shard_rounds
     return p
 
 
