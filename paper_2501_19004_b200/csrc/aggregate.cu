@@ -19,6 +19,7 @@
 // per-community HBM tables filled arc-parallel (ag_big_*).
 // Bytes: 12 B x A_in + 16 B x V_in + 8 B x A_out + 8 B x (count+1).
 #include <cooperative_groups.h>
+#include <cstdlib>
 #include <cooperative_groups/reduce.h>
 
 #include "kernels.cuh"
@@ -310,14 +311,15 @@ __global__ void __launch_bounds__(256) ag_big_arcs(AggArgs x, const u32* __restr
                                                    const u64* __restrict__ tab_off, unsigned char* tables,
                                                    u32* __restrict__ live_n, double* __restrict__ own_sum,
                                                    u32* __restrict__ own_seen, const u32* __restrict__ L,
-                                                   const u64* __restrict__ P, const u32* __restrict__ nL_p) {
+                                                   const u64* __restrict__ P, const u32* __restrict__ nL_p,
+                                                   u64 a_lo, u64 a_hi) {
   const u32 lane = threadIdx.x & 31;
   const u64 nL = *nL_p;
   if (!nL) return;
-  const u64 E = P[nL];
+  const u64 E = min(P[nL], a_hi);
   const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
-  for (u64 w = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; w * kBigChunk < E; w += warps) {
-    const u64 lo = w * kBigChunk, hi = min(E, lo + kBigChunk);
+  for (u64 w = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; a_lo + w * kBigChunk < E; w += warps) {
+    const u64 lo = a_lo + w * kBigChunk, hi = min(E, lo + kBigChunk);
     u64 i0 = last_le(P, nL, lo);  // owner of the chunk's first arc (every vertex of L has arcs)
     u32 own_pi = ~0u, seen = 0;
     double own = 0.0;
@@ -478,15 +480,28 @@ void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
     LVN_LAUNCH();
     exclusive_scan_u64(bytes.p, tab_off.p, nbig, s);
     exclusive_scan_u32_to_u64(mcount.p, moff.p, nbig, s);
-    u64* h = ctx().pinned;
-    LVN_CUDA(cudaMemcpyAsync(h, tab_off.p + nbig, sizeof(u64), cudaMemcpyDeviceToHost, s));
-    LVN_CUDA(cudaMemcpyAsync(h + 1, moff.p + nbig, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    // host copies of the region offsets and member offsets (batch planning)
+    std::vector<u64> h_tab(nbig + 1), h_moff(nbig + 1);
+    LVN_CUDA(cudaMemcpyAsync(h_tab.data(), tab_off.p, (nbig + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(h_moff.data(), moff.p, (nbig + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
     LVN_CUDA(cudaStreamSynchronize(s));
-    const u64 table_bytes = h[0], M = h[1];
-    DBuf<unsigned char> tables(table_bytes ? table_bytes : 16);
-    ag_big_clear<<<unsigned(std::min<u64>(nbig, u64(sms) * 4)), 256, 0, s>>>(big, nbig, a.hoff, tab_off.p,
-                                                                             tables.p);
-    LVN_LAUNCH();
+    const u64 M = h_moff[nbig];
+    // The tables of all big communities can exceed device memory (their sum
+    // approaches 28 B per arc); communities are processed in batches whose
+    // regions fit a budget of a quarter of the free memory (at least the
+    // largest single region).
+    size_t free_b = 0, total_b = 0;
+    LVN_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    u64 largest = 0;
+    for (u64 i = 0; i < nbig; ++i) largest = std::max(largest, h_tab[i + 1] - h_tab[i]);
+    u64 budget = std::min<u64>(h_tab[nbig], u64(free_b / 4));
+    if (const char* e = std::getenv("LVN_BIG_TABLE_BUDGET")) budget = std::strtoull(e, nullptr, 10);  // tests
+    budget = std::max<u64>(budget, largest);
+    std::vector<u64> cuts{0};
+    for (u64 i = 0; i < nbig; ++i)
+      if (h_tab[i + 1] - h_tab[cuts.back()] > budget) cuts.push_back(i);
+    cuts.push_back(nbig);
+    DBuf<unsigned char> tables(budget ? budget : 16);
     // L = members of the big communities with arcs, P = scan of their degrees
     DBuf<u32> vert(M ? M : 1), keep(M + 1), kpos(M + 1), L(M ? M : 1), D(M ? M : 1);
     DBuf<u64> P(M + 1);
@@ -500,12 +515,32 @@ void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
     LVN_LAUNCH();
     exclusive_scan_u32_to_u64(D.p, P.p, M, s);
     static const int occ = occupancy(ag_big_arcs, 256, 0);
-    ag_big_arcs<<<unsigned(u64(sms) * occ), 256, 0, s>>>(a, index.p, tab_off.p, tables.p, live_n.p, own.p,
-                                                          own_seen.p, L.p, P.p, kpos.p + M);
-    LVN_LAUNCH();
-    ag_big_emit<<<unsigned(std::min<u64>(nbig, u64(sms) * 4)), kBlockThreads, 0, s>>>(
-        a, big, nbig, tab_off.p, tables.p, live_n.p, own.p, own_seen.p);
-    LVN_LAUNCH();
+    for (size_t bi = 0; bi + 1 < cuts.size(); ++bi) {
+      const u64 b0 = cuts[bi], b1 = cuts[bi + 1], nb = b1 - b0;
+      if (!nb) continue;
+      // regions of this batch start at the buffer's base
+      unsigned char* base = tables.p - h_tab[b0];
+      ag_big_clear<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), 256, 0, s>>>(big + b0, nb, a.hoff, tab_off.p + b0,
+                                                                              base);
+      LVN_LAUNCH();
+      // arc range of the batch: members [moff[b0], moff[b1]) -> kept L entries -> P
+      u64 arc_lo = 0, arc_hi = ~u64(0);
+      if (cuts.size() > 2) {
+        u32 k[2] = {0, 0};
+        LVN_CUDA(cudaMemcpyAsync(&k[0], kpos.p + h_moff[b0], sizeof(u32), cudaMemcpyDeviceToHost, s));
+        LVN_CUDA(cudaMemcpyAsync(&k[1], kpos.p + h_moff[b1], sizeof(u32), cudaMemcpyDeviceToHost, s));
+        LVN_CUDA(cudaStreamSynchronize(s));
+        LVN_CUDA(cudaMemcpyAsync(&arc_lo, P.p + k[0], sizeof(u64), cudaMemcpyDeviceToHost, s));
+        LVN_CUDA(cudaMemcpyAsync(&arc_hi, P.p + k[1], sizeof(u64), cudaMemcpyDeviceToHost, s));
+        LVN_CUDA(cudaStreamSynchronize(s));
+      }
+      ag_big_arcs<<<unsigned(u64(sms) * occ), 256, 0, s>>>(a, index.p, tab_off.p, base, live_n.p, own.p,
+                                                            own_seen.p, L.p, P.p, kpos.p + M, arc_lo, arc_hi);
+      LVN_LAUNCH();
+      ag_big_emit<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), kBlockThreads, 0, s>>>(
+          a, big + b0, nb, tab_off.p + b0, base, live_n.p + b0, own.p + b0, own_seen.p + b0);
+      LVN_LAUNCH();
+    }
   }
 }
 

@@ -87,6 +87,7 @@ class Pool {
   std::unordered_set<void*> used_;
   std::unordered_map<void*, size_t> big_used_;
   std::multimap<size_t, void*> big_free_;
+  size_t cache_budget_ = size_t(16) << 30;  // bytes of free big blocks kept across a miss
 };
 
 // Pinned host blocks for results handed to the caller (membership): device

@@ -35,6 +35,9 @@ void Pool::bind(int device, cudaStream_t s) {
   std::uint64_t keep = ~std::uint64_t(0);
   LVN_CUDA(cudaMemPoolSetAttribute(pool_, cudaMemPoolAttrReleaseThreshold, &keep));
   stream_ = s;
+  size_t free_b = 0, total_b = 0;
+  LVN_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  cache_budget_ = total_b / 4;
 }
 
 void* Pool::raw(size_t bytes) {
@@ -66,6 +69,18 @@ void* Pool::get(size_t bytes) {
       p = it->second, have = it->first;
       big_free_.erase(it);
     } else {
+      // no cached block fits: hand cached blocks (largest first) back to the
+      // device pool while they exceed a quarter of device memory, so a
+      // changing working set (generation, a different graph) cannot pin the
+      // memory a new size class needs
+      size_t cached = 0;
+      for (auto& kv : big_free_) cached += kv.first;
+      while (!big_free_.empty() && cached + r > cache_budget_) {
+        auto last = std::prev(big_free_.end());
+        cached -= last->first;
+        (void)cudaFreeAsync(last->second, stream_);
+        big_free_.erase(last);
+      }
       p = raw(r);
     }
     big_used_[p] = have;

@@ -6,6 +6,7 @@
 //
 // This is input plumbing, not the timed hot path; the key sort uses CUB's
 // radix sort (library code, like cuBLAS for a plain GEMM).
+#include <cub/block/block_scan.cuh>
 #include <cub/device/device_radix_sort.cuh>
 
 #include <cmath>
@@ -117,20 +118,25 @@ __global__ void gen_uniform(ull* keys, u64 edges, u64 n, u64 seed) {
 }
 
 // Web-crawl shape: hosts are contiguous id ranges; vertex u emits deg(u)
-// (truncated power law) edges, most inside its host within a locality
-// window, the rest to global preferential-attachment targets (low ids).
+// (truncated power law) edges, most inside its host within a locality window
+// of +-2 deg(u) ids (clipped to the host, so small hosts saturate towards
+// cliques, as navigation-linked web hosts do), the rest to global
+// preferential-attachment targets (low ids).
 __global__ void gen_web(ull* keys, const u64* __restrict__ eoff, u64 n, const u32* __restrict__ host_lo,
                         const u32* __restrict__ host_hi, double p_local, u64 window, u64 seed) {
   for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n;
        u += u64(gridDim.x) * blockDim.x) {
     const u64 e0 = eoff[u], e1 = eoff[u + 1];
     const u64 lo = host_lo[u], hi = host_hi[u];
+    const u64 d = e1 - e0;
+    const u64 w = d * 2 > window ? d * 2 : window;
+    const double pl = p_local;
     for (u64 e = e0; e < e1; ++e) {
       const u64 r0 = mix64(seed ^ mix64(2 * e)), r1 = mix64(seed ^ mix64(2 * e + 1));
       u64 v;
-      if (unit(r0) < p_local) {
-        const u64 a = u > lo + window ? u - window : lo;
-        const u64 b = u + window + 1 < hi ? u + window + 1 : hi;
+      if (unit(r0) < pl) {
+        const u64 a = u > lo + w ? u - w : lo;
+        const u64 b = u + w + 1 < hi ? u + w + 1 : hi;
         v = a + below(r1, b - a);
       } else {
         // preferential attachment: P(v) ~ v^(-0.8) over the id space
@@ -156,20 +162,50 @@ __global__ void web_degrees(u64* __restrict__ deg, u64 n, double alpha, double d
   }
 }
 
-__global__ void keep_flags(const ull* __restrict__ keys, u64 m, u32* __restrict__ keep) {
-  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < m;
-       i += u64(gridDim.x) * blockDim.x)
-    keep[i] = keys[i] != kDrop && (i == 0 || keys[i] != keys[i - 1]);
+// unique compaction of sorted keys in tiles of kTile keys: pass 1 counts the
+// kept keys per tile, pass 2 re-derives the flags, block-scans them and places
+// targets (no per-key position array, which at 4e9 keys would cost 32 GB)
+constexpr int kTileT = 256, kTileI = 16;
+constexpr u64 kTile = u64(kTileT) * kTileI;
+
+__device__ __forceinline__ bool kept(const ull* keys, u64 i) {
+  const ull k = keys[i];
+  return k != kDrop && (i == 0 || k != keys[i - 1]);
 }
 
-__global__ void place(const ull* __restrict__ keys, u64 m, const u32* __restrict__ keep,
-                      const u64* __restrict__ pos, u32* __restrict__ tgt, u32* __restrict__ deg) {
-  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < m;
-       i += u64(gridDim.x) * blockDim.x) {
-    if (!keep[i]) continue;
-    const ull k = keys[i];
-    tgt[pos[i]] = u32(k);
-    atomicAdd(&deg[u32(k >> 32)], 1u);
+__global__ void __launch_bounds__(kTileT) tile_counts(const ull* __restrict__ keys, u64 m, u32* __restrict__ cnt) {
+  using Scan = cub::BlockScan<u32, kTileT>;
+  __shared__ typename Scan::TempStorage tmp;
+  const u64 base = u64(blockIdx.x) * kTile + u64(threadIdx.x) * kTileI;
+  u32 c = 0;
+#pragma unroll
+  for (int j = 0; j < kTileI; ++j)
+    if (base + j < m && kept(keys, base + j)) ++c;
+  u32 total;
+  Scan(tmp).ExclusiveSum(c, c, total);
+  if (threadIdx.x == 0) cnt[blockIdx.x] = total;
+}
+
+__global__ void __launch_bounds__(kTileT) tile_place(const ull* __restrict__ keys, u64 m,
+                                                     const u64* __restrict__ toff, u32* __restrict__ tgt,
+                                                     u32* __restrict__ deg) {
+  using Scan = cub::BlockScan<u32, kTileT>;
+  __shared__ typename Scan::TempStorage tmp;
+  const u64 base = u64(blockIdx.x) * kTile + u64(threadIdx.x) * kTileI;
+  u32 c = 0;
+#pragma unroll
+  for (int j = 0; j < kTileI; ++j)
+    if (base + j < m && kept(keys, base + j)) ++c;
+  u32 pos;
+  Scan(tmp).ExclusiveSum(c, pos);
+  u64 out = toff[blockIdx.x] + pos;
+#pragma unroll
+  for (int j = 0; j < kTileI; ++j) {
+    if (base + j < m && kept(keys, base + j)) {
+      const ull k = keys[base + j];
+      tgt[out++] = u32(k);
+      atomicAdd(&deg[u32(k >> 32)], 1u);
+    }
   }
 }
 
@@ -198,13 +234,16 @@ void keys_to_csr(DBuf<ull>& keys, u64 nkeys, u64 n, OwnedCsr& out, cudaStream_t 
     LVN_CUDA(cudaStreamSynchronize(s));
   }
   keys.release();
-  DBuf<u32> keep(nkeys);
-  keep_flags<<<grid(nkeys), 256, 0, s>>>(sorted.p, nkeys, keep.p);
-  LVN_LAUNCH();
-  DBuf<u64> pos(nkeys + 1);
-  exclusive_scan_u32_to_u64(keep.p, pos.p, nkeys, s);
+  const u64 tiles = (nkeys + kTile - 1) / kTile;
+  DBuf<u32> cnt(tiles ? tiles : 1);
+  DBuf<u64> toff(tiles + 1);
+  if (tiles) {
+    tile_counts<<<unsigned(tiles), kTileT, 0, s>>>(sorted.p, nkeys, cnt.p);
+    LVN_LAUNCH();
+  }
+  exclusive_scan_u32_to_u64(cnt.p, toff.p, tiles, s);
   u64 arcs = 0;
-  LVN_CUDA(cudaMemcpyAsync(&arcs, pos.p + nkeys, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaMemcpyAsync(&arcs, toff.p + tiles, sizeof(u64), cudaMemcpyDeviceToHost, s));
   LVN_CUDA(cudaStreamSynchronize(s));
   out.n = u32(n);
   out.arcs = arcs;
@@ -213,8 +252,11 @@ void keys_to_csr(DBuf<ull>& keys, u64 nkeys, u64 n, OwnedCsr& out, cudaStream_t 
   out.off.alloc(n + 1);
   DBuf<u32> deg(n ? n : 1);
   LVN_CUDA(cudaMemsetAsync(deg.p, 0, (n ? n : 1) * sizeof(u32), s));
-  place<<<grid(nkeys), 256, 0, s>>>(sorted.p, nkeys, keep.p, pos.p, out.tgt.p, deg.p);
-  LVN_LAUNCH();
+  if (tiles) {
+    tile_place<<<unsigned(tiles), kTileT, 0, s>>>(sorted.p, nkeys, toff.p, out.tgt.p, deg.p);
+    LVN_LAUNCH();
+  }
+  sorted.release();
   exclusive_scan_u32_to_u64(deg.p, out.off.p, n, s);
   fill_ones<<<grid(arcs), 256, 0, s>>>(out.w.p, arcs);
   LVN_LAUNCH();
@@ -274,7 +316,7 @@ void generate(const GenSpec& g, OwnedCsr& out, cudaStream_t s) {
       const double a1 = 1.0 - alpha, a2 = 2.0 - alpha;
       const double mean_raw = (a1 / a2) * (std::pow(dmax, a2) - std::pow(dmin, a2)) /
                               (std::pow(dmax, a1) - std::pow(dmin, a1));
-      const double target = g.avg_degree / 2.0 * 1.06;  // undirected samples per vertex
+      const double target = g.avg_degree / 2.0 * 1.63;  // undirected samples per vertex (dedupe loss)
       web_degrees<<<grid(n), 256, 0, s>>>(deg.p, n, alpha, dmin, dmax, target / mean_raw,
                                           g.seed + 7);
       LVN_LAUNCH();

@@ -5,9 +5,12 @@ import paper_2501_19004_b200 as lvn
 from bench import CONFIGS
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"
 runs = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+# optional CompactOptions overrides: key=value ...
+over = dict(a.split("=") for a in sys.argv[3:])
+opts = lvn.CompactOptions(**{k: int(v) for k, v in over.items()})
 c = CONFIGS[cfg]
 dg = lvn.generate(c["kind"], **{k: v for k, v in c.items() if k not in ("kind", "desc")})
 for i in range(runs):
-    r = lvn.louvain_compact(dg, membership_on_device=True)
+    r = lvn.louvain_compact(dg, None, opts, membership_on_device=True)
     print(cfg, round(r.modularity, 5), r.passes, r.iterations_per_pass, "V", r.vertices_per_pass, "A", r.arcs_per_pass,
           {k: round(s.seconds * 1e3, 2) for k, s in r.stats.items()}, "pass_ms", [round(x * 1e3, 1) for x in r.pass_seconds], flush=True)

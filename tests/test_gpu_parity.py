@@ -189,6 +189,16 @@ def test_aggregate_member_parallel(lvn, port, k_big):
     agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
 
 
+def test_aggregate_member_parallel_batched(lvn, port, monkeypatch):
+    # a tiny table budget forces one batch per giant community
+    monkeypatch.setenv("LVN_BIG_TABLE_BUDGET", "1")
+    g = random_graph(40000, 400000, 93)
+    m = random_membership(g.n, 3000, 7).astype(np.int64)
+    m[: 24000] = np.arange(24000) % 5
+    m = np.unique(m, return_inverse=True)[1].astype(np.uint32)
+    agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
+
+
 def test_aggregate_member_parallel_hubs(lvn, port):
     g = hubs_graph(30000, 4, 20000, 100000, 5)
     for m in (np.zeros(g.n, np.uint32), (np.arange(g.n) % 2).astype(np.uint32),
