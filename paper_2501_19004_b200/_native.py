@@ -11,7 +11,8 @@ import os
 import subprocess
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "liblvn.so")
+# LVN_LIB overrides the library path (A/B timing of two builds)
+LIB_PATH = os.environ.get("LVN_LIB") or os.path.join(HERE, "lib", "liblvn.so")
 CSRC = os.path.join(HERE, "csrc")
 
 LVN_HOST, LVN_DEVICE = 0, 1
@@ -183,9 +184,10 @@ def lib() -> C.CDLL:
     L.lvn_graph_free.argtypes = [C.POINTER(lvn_graph_out)]
     L.lvn_graph_free.restype = None
     L.lvn_louvain.argtypes = [C.POINTER(lvn_csr), C.POINTER(lvn_params), C.POINTER(C.POINTER(lvn_result))]
-    L.lvn_louvain_sharded.argtypes = [C.POINTER(lvn_csr), C.POINTER(lvn_params), C.POINTER(lvn_comm),
-                                      C.POINTER(C.POINTER(lvn_result))]
-    L.lvn_partition_rows.argtypes = [vp, C.c_uint32, i, vp]
+    if hasattr(L, "lvn_louvain_sharded"):  # absent only in older builds loaded through LVN_LIB
+        L.lvn_louvain_sharded.argtypes = [C.POINTER(lvn_csr), C.POINTER(lvn_params), C.POINTER(lvn_comm),
+                                          C.POINTER(C.POINTER(lvn_result))]
+        L.lvn_partition_rows.argtypes = [vp, C.c_uint32, i, vp]
     L.lvn_modularity.argtypes = [C.POINTER(lvn_csr), vp, i, C.POINTER(C.c_double)]
     L.lvn_vertex_weights.argtypes = [C.POINTER(lvn_csr), vp]
     L.lvn_count_communities.argtypes = [vp, C.c_uint64, i, C.POINTER(C.c_uint32)]

@@ -19,6 +19,7 @@
 // per-community HBM tables filled arc-parallel (ag_big_*).
 // Bytes: 12 B x A_in + 16 B x V_in + 8 B x A_out + 8 B x (count+1).
 #include <cooperative_groups.h>
+#include <cstdio>
 #include <cstdlib>
 #include <cooperative_groups/reduce.h>
 
@@ -501,6 +502,10 @@ void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
     for (u64 i = 0; i < nbig; ++i)
       if (h_tab[i + 1] - h_tab[cuts.back()] > budget) cuts.push_back(i);
     cuts.push_back(nbig);
+    if (const char* e = std::getenv("LVN_VERBOSE"); e && *e && *e != '0')
+      std::fprintf(stderr, "[lvn] aggregate: %llu giant communities, %llu members, tables %.2f GB in %zu batches "
+                   "(budget %.2f GB, free %.2f GB)\n", (unsigned long long)nbig, (unsigned long long)M,
+                   h_tab[nbig] / 1e9, cuts.size() - 1, budget / 1e9, free_b / 1e9);
     DBuf<unsigned char> tables(budget ? budget : 16);
     // L = members of the big communities with arcs, P = scan of their degrees
     DBuf<u32> vert(M ? M : 1), keep(M + 1), kpos(M + 1), L(M ? M : 1), D(M ? M : 1);

@@ -209,16 +209,24 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
 // arcs per lane per round: all B target/weight loads, then all B C[t] gathers,
 // are issued before the first dependent use, so each lane keeps B independent
 // memory requests in flight (the sweep is latency-bound otherwise).
-template <int B, class Tab, class V>
+//
+// COMBINE (stride a multiple of 32, consecutive lanes on consecutive arcs):
+// the 32 (community, weight) pairs a warp holds are first sorted across the
+// warp and summed per run, so each distinct community of the batch is merged
+// into the table once. Late passes have few distinct neighbour communities
+// per row; without this, all lanes of a block hammer the same few slots with
+// CAS retries.
+template <int B, bool COMBINE, class Tab, class V>
 __device__ __forceinline__ void scan_arcs(const MoveArgs& x, const Tab& tab, u32 lg, u32 u, u32 from,
                                           u64 lo, u64 hi, u32 lane, u32 stride, V& own, u32* live,
                                           u32* nlive) {
-  for (u64 base = lo + lane; base < hi; base += u64(stride) * B) {
+  // the trip count is uniform across the lanes (COMBINE shuffles need every lane)
+  for (u64 b0 = lo; b0 < hi; b0 += u64(stride) * B) {
     u32 t[B], c[B];
     V w[B];
 #pragma unroll
     for (int k = 0; k < B; ++k) {
-      const u64 a = base + u64(k) * stride;
+      const u64 a = b0 + lane + u64(k) * stride;
       t[k] = a < hi ? __ldcs(x.g.tgt + a) : u;  // out of range reads as a self-loop: skipped
       w[k] = a < hi ? V(__ldcs(x.g.w + a)) : V(0);
     }
@@ -226,7 +234,17 @@ __device__ __forceinline__ void scan_arcs(const MoveArgs& x, const Tab& tab, u32
     for (int k = 0; k < B; ++k) c[k] = t[k] != u ? x.C[t[k]] : kEmpty;
 #pragma unroll
     for (int k = 0; k < B; ++k) {
-      if (c[k] == kEmpty) continue;
+      bool tail = true;
+      // combine only when the batch repeats a community (one match.any tells)
+      if (COMBINE && !__all_sync(0xffffffffu, __match_any_sync(0xffffffffu, c[k]) == (1u << (lane & 31)))) {
+        u32 kk[1] = {c[k]};
+        V vv[1] = {w[k]};
+        bitonic_sort<32, 1, V>(kk, vv, lane & 31);
+        bool tl[1];
+        segmented_runs<32, 1, V>(kk, vv, tl, lane & 31);
+        c[k] = kk[0], w[k] = vv[0], tail = tl[0];
+      }
+      if (!tail || c[k] == kEmpty) continue;
       if (c[k] == from) {
         own += w[k];
       } else {
@@ -307,7 +325,7 @@ __global__ void __launch_bounds__(THREADS, 4) lm_group(MoveArgs x, const u32* __
       continue;
     }
     V own = V(0);
-    scan_arcs<kBatch>(x, tab, lg, u, from, lo, lo + d, lane, G, own, live, nlive);
+    scan_arcs<kBatch, G == 32>(x, tab, lg, u, from, lo, lo + d, lane, G, own, live, nlive);
     own = cg::reduce(tile, own, cg::plus<V>());
     tile.sync();
     const u32 n = *reinterpret_cast<volatile u32*>(nlive);
@@ -711,7 +729,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
       continue;
     }
     V own = V(0);
-    scan_arcs<kBatch>(x, tab, lg, u, from, lo, lo + d, threadIdx.x, kBlockThreads, own, live, &nlive);
+    scan_arcs<kBatch, true>(x, tab, lg, u, from, lo, lo + d, threadIdx.x, kBlockThreads, own, live, &nlive);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
     if (lane == 0) red_v[wid] = own;
@@ -827,7 +845,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const
     const u64 a1 = min(a0 + kHubChunk, row_end);
     const u32 from = x.C[u];
     V own = V(0);
-    scan_arcs<kBatch>(x, stab, u32(kBlockCapLog), u, from, a0, a1, threadIdx.x, kBlockThreads, own, slive,
+    scan_arcs<kBatch, true>(x, stab, u32(kBlockCapLog), u, from, a0, a1, threadIdx.x, kBlockThreads, own, slive,
                       &nlive);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
