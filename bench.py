@@ -165,7 +165,7 @@ def run_reference(args, world, rank):
     v = arcs / t
     out = {
         "metric": METRIC, "value": v, "unit": "edges/s", "n_gpus": world, "steps": args.steps,
-        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "weak",
+        "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic", "impl": "reference",
         "config": {"workload": args.config, "desc": cfg["desc"], "vertices": g.num_vertices(), "arcs": arcs,
                    "engine": "louvain_mc (reference, OpenMP)"},
