@@ -37,6 +37,7 @@
 #include <cmath>
 
 #include "kernels.cuh"
+#include "psort.cuh"
 #include "sortnet.cuh"
 #include "tables.cuh"
 
@@ -508,6 +509,165 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
   tl.flush(x);
 }
 
+// ---- sort bins, packed keys (psort.cuh): the default when n < 2^(32 - LB) -------
+// Same schedule as lm_sort (G lanes x K registers per vertex, pipelined one
+// vertex deep), with fewer instructions per vertex: the network sorts 32-bit
+// (community << LB | row position) keys and the weights are fetched once
+// afterwards; run starts come from a ballot; the group argmax is three
+// redux.sync for G = 32; the lane holding the winning candidate decides
+// (no broadcast of gain and weight); targets are re-read only when u moves.
+template <int G, int K, class V, bool DRY>
+__global__ void __launch_bounds__(256) lm_psort(MoveArgs x, const u32* __restrict__ list, u64 count) {
+  constexpr int GPB = 256 / G;
+  constexpr int N = G * K;
+  constexpr int LB = ilog2<N>();
+  constexpr u32 FULL = 0xffffffffu;
+  constexpr u32 GMASK = G == 32 ? FULL : ((1u << G) - 1u);
+  __shared__ V vbuf[K > 1 ? 256 * K : 1];  // per group: weights in row order (K > 1)
+  const u32 lane = threadIdx.x & (G - 1);
+  const u32 gi = threadIdx.x / G;
+  const u32 gshift = (threadIdx.x & 31u) & ~u32(G - 1);
+  V* gbuf = vbuf + (K > 1 ? gi * N : 0);
+  const ull dirs = psort_dirs<G, K>(lane);
+  const u64 stride = u64(gridDim.x) * GPB;
+  const ull keep = l2_keep_policy();
+  Tally tl;
+  u64 i0 = u64(blockIdx.x) * GPB;
+  bool have = i0 + gi < count;
+  u32 u = 0, from = kEmpty;
+  u64 lo = 0, hi = 0;
+  double ku = 0.0, sf = 0.0;
+  u32 key[K];
+  V val[K];
+  if (have) {
+    u = list[i0 + gi];
+    lo = x.g.off[u];
+    hi = x.g.off[u + 1];
+    from = x.C[u];
+    ku = x.K[u];
+  }
+  {
+    u32 t[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const u64 a = lo + u64(r) * G + lane;
+      const bool ok = a < hi;
+      t[r] = ok ? __ldcs(x.g.tgt + a) : u;
+      val[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+    }
+    if (have) sf = x.sigma[from];
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      key[r] = t[r] != u ? (ld_keep(x.C + t[r], keep) << LB) | u32(r * G + lane) : kNoKey;
+  }
+
+  for (; i0 < count; i0 += stride) {
+    // stage 1 (next): list entry
+    const u64 in = i0 + stride + gi;
+    const bool nhave = in < count;
+    const u32 nu = nhave ? list[in] : 0u;
+
+    // current: group the arcs by community, fetch the weights in sorted order
+    if (K > 1) {
+      __syncwarp();
+#pragma unroll
+      for (int r = 0; r < K; ++r) gbuf[r * G + lane] = val[r];
+      __syncwarp();
+    }
+    psort<G, K>(key, dirs);
+    u32 ck[K];
+    V run[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const u32 pos = key[r] & u32(N - 1);
+      V w;
+      if (K == 1) w = __shfl_sync(FULL, val[0], pos, G);
+      else w = gbuf[pos];
+      ck[r] = key[r] == kNoKey ? kEmpty : key[r] >> LB;
+      run[r] = key[r] == kNoKey ? V(0) : w;
+    }
+    bool tail[K];
+    prun_sums<G, K, V>(ck, run, tail, lane, gshift);
+
+    // stage 2 (next): row bounds, own community, vertex weight
+    u64 nlo = 0, nhi = 0;
+    u32 nfrom = kEmpty;
+    double nku = 0.0;
+    if (nhave) {
+      nlo = x.g.off[nu];
+      nhi = x.g.off[nu + 1];
+      nfrom = x.C[nu];
+      nku = x.K[nu];
+    }
+
+    // current: weight to the own community (one run tail in the group holds it),
+    // Sigma of the candidates
+    V own_l = V(0);
+    bool has_own = false, cand[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      if (tail[r] && ck[r] == from) own_l = run[r], has_own = true;
+      cand[r] = tail[r] && ck[r] != kEmpty && ck[r] != from;
+    }
+    const u32 ob = (__ballot_sync(FULL, has_own) >> gshift) & GMASK;
+    const V own_s = __shfl_sync(FULL, own_l, ob ? __ffs(ob) - 1 : 0, G);
+    const V own = ob ? own_s : V(0);
+    double sc[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      if (cand[r]) cand[r] = key_ok(x, ck[r]);
+      sc[r] = cand[r] ? ld_keep(x.sigma + ck[r], keep) : 0.0;
+    }
+
+    // stage 3 (next): arcs
+    u32 nt[K];
+    V nval[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const u64 a = nlo + u64(r) * G + lane;
+      const bool ok = a < nhi;
+      nt[r] = ok ? __ldcs(x.g.tgt + a) : nu;
+      nval[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+    }
+
+    // current: rank the candidates, group argmax
+    double bg = -INFINITY, bk = 0.0;
+    u32 bc = kEmpty;
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      if (!cand[r]) continue;
+      const double g = score<DRY>(x, double(run[r]), double(own), ku, sc[r], sf);
+      if (better(g, ck[r], bg, bc)) bg = g, bc = ck[r], bk = double(run[r]);
+    }
+    const u32 best = group_best<G>(bg, bc);
+
+    // stage 4 (next): communities of the arcs, Sigma of the own community
+    u32 nkey[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r)
+      nkey[r] = nt[r] != nu ? (ld_keep(x.C + nt[r], keep) << LB) | u32(r * G + lane) : kNoKey;
+    const double nsf = nhave ? x.sigma[nfrom] : 0.0;
+
+    // current: the lane holding the best candidate (lane 0 if none) decides
+    const bool decider = have && (best == kEmpty ? lane == 0 : bc == best);
+    bool moved = false;
+    if (decider) {
+      if (!DRY) x.flags[u] = 0;
+      ++tl.verts;
+      tl.arcs += hi - lo;
+      moved = decide<DRY>(x, u, from, ku, best, best == kEmpty ? -INFINITY : bg, bk, double(own), tl);
+    }
+    if (!DRY && x.prune && ((__ballot_sync(FULL, moved) >> gshift) & GMASK))
+      for (u64 a = lo + lane; a < hi; a += G) x.flags[x.g.tgt[a]] = 1;
+
+    // rotate
+    have = nhave, u = nu, lo = nlo, hi = nhi, from = nfrom, ku = nku, sf = nsf;
+#pragma unroll
+    for (int r = 0; r < K; ++r) key[r] = nkey[r], val[r] = nval[r];
+  }
+  tl.flush(x);
+}
+
 // ---- sort bins, match variant: warp per vertex, K arcs per lane ----------------
 // Equal communities among the 32 arcs of one register round are found with
 // one match.any; the lowest lane of each peer set (the leader) sums the peers'
@@ -959,10 +1119,31 @@ void launch_chunks(K kernel, const MoveArgs& a, const u32* list, u64 count, int 
   }
 }
 
+// LVN_MOVE_KERNEL=sort selects the unpacked register sort (lm_sort) for the
+// sort bins, =match the match.any kernels (tuning aids; lm_psort is the default)
+int move_kernel_choice() {
+  static const int v = [] {
+    const char* e = std::getenv("LVN_MOVE_KERNEL");
+    if (!e) return 0;
+    const std::string s(e);
+    return s == "sort" ? 1 : s == "match" ? 2 : 0;
+  }();
+  return v;
+}
+bool use_match() { return move_kernel_choice() == 2; }
+
 template <int G, int K, class V, bool DRY>
 void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
   if (!b.count(bin)) return;
   constexpr int T = 256;
+  constexpr int LB = ilog2<G * K>();
+  // packed keys need (n - 1) << LB | (N - 1) < 0xFFFFFFFF
+  if (move_kernel_choice() == 0 && u64(a.g.n) < (u64(1) << (32 - LB))) {
+    auto k = lm_psort<G, K, V, DRY>;
+    static const int occ = occupancy(k, T, 0);
+    launch_chunks(k, a, b.of(bin), b.count(bin), T, T / G, u64(sm_count()) * occ, 0, s);
+    return;
+  }
   auto k = lm_sort<G, K, V, DRY>;
   static const int occ = occupancy(k, T, 0);
   launch_chunks(k, a, b.of(bin), b.count(bin), T, T / G, u64(sm_count()) * occ, 0, s);
@@ -976,16 +1157,6 @@ void launch_match(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) 
   constexpr size_t smem = match_smem<K, Tab>();
   static const int occ = (set_smem(k, smem), occupancy(k, T, smem));
   launch_chunks(k, a, b.of(bin), b.count(bin), T, T / 32, u64(sm_count()) * occ, smem, s);
-}
-
-// LVN_MOVE_KERNEL=match selects the match.any kernels for the sort bins
-// (tuning aid; the register-sort kernels are faster on the configs measured)
-bool use_match() {
-  static const bool on = [] {
-    const char* e = std::getenv("LVN_MOVE_KERNEL");
-    return e && std::string(e) == "match";
-  }();
-  return on;
 }
 
 template <class Tab, bool DRY>
