@@ -168,9 +168,22 @@ __global__ void __launch_bounds__(THREADS) ag_group(AggArgs x, const u32* __rest
   }
 }
 
+// One arc per lane per round (kEmpty when the lane has none): the weight to
+// the community itself is summed privately, the rest is pre-combined across
+// the warp and inserted once per distinct key.
+__device__ __forceinline__ void ag_merge_round(const Tab& tab, u32 lg, u32 c, u32 key, double w, u32 lane,
+                                               double& own, u32& own_seen) {
+  if (key == c) {
+    own += w;
+    own_seen = 1;
+    key = kEmpty;
+  }
+  if (warp_combine(key, w, lane)) tab.insert(lg, key, w);
+}
+
 __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32 c, u32 lg, double* red,
                              u32* red_seen, u32* cursor) {
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int W = kBlockThreads / 32;
   const u64 mlo = x.coff[c], mhi = x.coff[c + 1];
   const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
@@ -181,11 +194,31 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32 c, u32 lg, do
   __syncthreads();
   double own = 0.0;
   u32 own_seen = 0;
-  if (budget >= (mhi - mlo) * 16) {  // warp per member
-    for (u64 k = mlo + wid; k < mhi; k += W) merge_row(x, tab, lg, c, x.members[k], lane, 32, own, own_seen);
-  } else {  // thread per member
-    for (u64 k = mlo + threadIdx.x; k < mhi; k += kBlockThreads)
-      merge_row(x, tab, lg, c, x.members[k], 0, 1, own, own_seen);
+  if (budget >= (mhi - mlo) * 16) {  // warp per member, lanes across its row
+    for (u64 k = mlo + wid; k < mhi; k += W) {
+      const u32 v = x.members[k];
+      const u64 lo = x.g.off[v], hi = x.g.off[v + 1];
+      for (u64 a0 = lo; a0 < hi; a0 += 32) {
+        const u64 a = a0 + lane;
+        const u32 key = a < hi ? x.C[__ldcs(x.g.tgt + a)] : kEmpty;
+        const double w = a < hi ? double(__ldcs(x.g.w + a)) : 0.0;
+        ag_merge_round(tab, lg, c, key, w, lane, own, own_seen);
+      }
+    }
+  } else {  // lane per member, one arc per lane per round
+    for (u64 k0 = mlo + u64(wid) * 32; k0 < mhi; k0 += u64(W) * 32) {
+      const u64 k = k0 + lane;
+      u64 a = 0, hi = 0;
+      if (k < mhi) {
+        const u32 v = x.members[k];
+        a = x.g.off[v], hi = x.g.off[v + 1];
+      }
+      for (; __any_sync(0xffffffffu, a < hi); ++a) {
+        const u32 key = a < hi ? x.C[x.g.tgt[a]] : kEmpty;
+        const double w = a < hi ? double(x.g.w[a]) : 0.0;
+        ag_merge_round(tab, lg, c, key, w, lane, own, own_seen);
+      }
+    }
   }
   own = warp_sum(own);
   own_seen = __any_sync(0xffffffffu, own_seen);
@@ -337,20 +370,33 @@ __global__ void __launch_bounds__(256) ag_big_arcs(AggArgs x, const u32* __restr
       }
       const u64 owner = i0 + k;
       i0 += __shfl_sync(0xffffffffu, k, 31);
-      if (a >= hi) continue;
-      const u32 v = L[owner];
-      const u32 c = x.C[v];
-      const u32 pi = index[c];
-      const u64 ga = x.g.off[v] + (a - P[owner]);
-      const u32 key = x.C[__ldcs(x.g.tgt + ga)];
-      const double wt = double(__ldcs(x.g.w + ga));
-      if (key == c) {
-        if (pi != own_pi) {
-          if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
-          own_pi = pi, own = 0.0;
+      u32 key = kEmpty, c = 0, pi = 0;
+      double wt = 0.0;
+      if (a < hi) {
+        const u32 v = L[owner];
+        c = x.C[v];
+        pi = index[c];
+        const u64 ga = x.g.off[v] + (a - P[owner]);
+        key = x.C[__ldcs(x.g.tgt + ga)];
+        wt = double(__ldcs(x.g.w + ga));
+        if (key == c) {
+          if (pi != own_pi) {
+            if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
+            own_pi = pi, own = 0.0;
+          }
+          own += wt;
+          seen = 1;
+          key = kEmpty;
         }
-        own += wt;
-        seen = 1;
+      }
+      // a batch inside one community (the usual case): one insert per distinct key
+      const u32 phi = __reduce_max_sync(0xffffffffu, key != kEmpty ? pi : 0u);
+      const u32 plo = __reduce_min_sync(0xffffffffu, key != kEmpty ? pi : ~0u);
+      if (phi == plo) {
+        const u32 cc = __reduce_max_sync(0xffffffffu, key != kEmpty ? c : 0u);
+        if (!warp_combine(key, wt, lane)) continue;
+        c = cc, pi = phi;
+      } else if (key == kEmpty) {
         continue;
       }
       const u64 slots = big_slots(x.hoff[c + 1] - x.hoff[c]);

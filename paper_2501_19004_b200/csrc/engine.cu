@@ -497,6 +497,11 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   }
   Bins ab;
   compute_bins(boff.p + c0, c1 - c0, e, ab, s, ~u64(0), c0);  // synchronises
+  if (verbose()) {
+    std::fprintf(stderr, "[lvn] aggregate %u communities, budget bins:", count);
+    for (int b = 0; b < kBins; ++b) std::fprintf(stderr, " %llu", (unsigned long long)ab.count(b));
+    std::fprintf(stderr, " (max budget %llu)\n", (unsigned long long)ab.max_degree);
+  }
   const u64 H = read_scalar(hoff.p + count, s);
   DBuf<u32> htgt(H ? H : 1), fill(count ? count : 1);
   DBuf<float> hw(H ? H : 1);

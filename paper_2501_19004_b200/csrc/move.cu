@@ -83,13 +83,25 @@ __device__ __forceinline__ double score(const MoveArgs& x, double k_to_c, double
   return (k_to_c - own) * x.inv_m - ku * (ku + sigma_c - sigma_d) * x.inv_2m2;
 }
 
+// Sigma-free upper bound of Eq. 2: with Sigma_c >= 0 the gain of c is at most
+// (K_{u->c} - K_{u->d})/m - K_u (K_u - Sigma_d)/(2m^2). A candidate whose bound
+// is not positive can never be the move target (a move needs gain > 0,
+// louvain_compact.cpp:151), so its Sigma gather is skipped. Once communities
+// form, most candidates fall under the weight to the own community, and the
+// random Sigma gathers (one L1TEX wavefront per lane) are what limits the sweep.
+// The margin covers rounding (the bound and the score are evaluated alike).
+__device__ __forceinline__ bool may_gain(const MoveArgs& x, double k_to_c, double own, double ku, double sf) {
+  const double a = (k_to_c - own) * x.inv_m, b = ku * (ku - sf) * x.inv_2m2;
+  return a - b >= -1e-12 * (fabs(a) + fabs(b));
+}
+
 // Move decision shared by every kernel; called by exactly one thread per vertex.
 // bk = K_{u->bc}, own = K_{u->from}.
 //
 // Applying a move validates it against the true Sigma at the instant it
 // lands: the join is one fp64 atomicAdd that returns Sigma_bc as it stood
-// (all earlier joiners included), the gain is re-scored exactly with that
-// value and the current Sigma_from, and the join is undone if it is no
+// (all earlier joiners included), the gain is re-scored with that value (the
+// reciprocal form of Eq. 2) and the current Sigma_from, and the join is undone if it is no
 // longer positive. This is the reference's asynchronous semantics (every
 // decision sees the moves applied before it, louvain_mc.hpp:80-86) kept under
 // massive concurrency, where thousands of deciders would otherwise read the
@@ -116,7 +128,7 @@ __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, doubl
   if (mv) {
     const double sigma_c = atomicAdd(&x.sigma[bc], ku);
     const double sigma_d = *reinterpret_cast<volatile double*>(&x.sigma[from]);
-    const double g = delta_q(bk, own, ku, sigma_c, sigma_d, x.m);
+    const double g = score<false>(x, bk, own, ku, sigma_c, sigma_d);
     if (g > 0.0) {
       atomicAdd(&x.sigma[from], -ku);
       x.C[u] = bc;
@@ -185,11 +197,11 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
       bool first = ck != kEmpty && ck != from && key_ok(x, ck);
 #pragma unroll
       for (int j = 0; j < k; ++j) first = first && c[j] != ck;
-      if (first) {
-        V sum = V(0);  // row order, like the reference's serial scan
+      V sum = V(0);  // row order, like the reference's serial scan
 #pragma unroll
-        for (int j = k; j < kThreadMaxD; ++j)
-          if (c[j] == ck) sum += wv[j];
+      for (int j = k; j < kThreadMaxD; ++j)
+        if (c[j] == ck) sum += wv[j];
+      if (first && (DRY || may_gain(x, double(sum), double(own), ku, sf))) {
         const double g = score<DRY>(x, double(sum), double(own), ku, x.sigma[ck], sf);
         if (better(g, ck, bg, bc)) bg = g, bc = ck, bk = double(sum);
       }
@@ -269,7 +281,9 @@ __device__ __forceinline__ void rank_live(const MoveArgs& x, const Tab& tab, con
       const u32 j = j0 + k * stride;
       key[k] = kEmpty;
       val[k] = 0.0;
-      if (j < n && !(tab.read(live[j], key[k], val[k]) && key_ok(x, key[k]))) key[k] = kEmpty;
+      if (j < n && !(tab.read(live[j], key[k], val[k]) && key_ok(x, key[k]) &&
+                     (DRY || may_gain(x, val[k], own, ku, sf))))
+        key[k] = kEmpty;
     }
 #pragma unroll
     for (int k = 0; k < B; ++k) sc[k] = key[k] != kEmpty ? x.sigma[key[k]] : 0.0;
@@ -448,7 +462,7 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
     double sc[K];
 #pragma unroll
     for (int r = 0; r < K; ++r) {
-      if (cand[r]) cand[r] = key_ok(x, key[r]);
+      if (cand[r]) cand[r] = key_ok(x, key[r]) && (DRY || may_gain(x, double(run[r]), double(own), ku, sf));
       sc[r] = cand[r] ? ld_keep(x.sigma + key[r], keep) : 0.0;
     }
 
@@ -510,14 +524,21 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
 }
 
 // ---- sort bins, packed keys (psort.cuh): the default when n < 2^(32 - LB) -------
-// Same schedule as lm_sort (G lanes x K registers per vertex, pipelined one
-// vertex deep), with fewer instructions per vertex: the network sorts 32-bit
-// (community << LB | row position) keys and the weights are fetched once
-// afterwards; run starts come from a ballot; the group argmax is three
-// redux.sync for G = 32; the lane holding the winning candidate decides
-// (no broadcast of gain and weight); targets are re-read only when u moves.
+// Same work split as lm_sort (G lanes x K registers per vertex) with fewer
+// instructions per vertex: the network sorts 32-bit (community << LB | row
+// position) keys and the weights are fetched once afterwards; run starts come
+// from a ballot; the group argmax is three redux.sync for G = 32; the lane
+// holding the winning candidate decides (no broadcast of gain and weight).
+//
+// Software pipeline, three vertices per group in flight. Iteration i:
+//   targets + weights of i+1 | list entry of i+2 | sort i | C[t] of i+1 |
+//   own weight + Sigma of i | row bounds of i+2 | rank, decide, mark i
+// so every dependent load (list -> offsets -> targets -> communities) has a
+// compute step of its own between issue and use. The targets of i and i+1 stay
+// in registers for the neighbour marks. Gathers for i+1 may miss the move of
+// i (asynchrony the validated join tolerates); DRY writes no state.
 template <int G, int K, class V, bool DRY>
-__global__ void __launch_bounds__(256) lm_psort(MoveArgs x, const u32* __restrict__ list, u64 count) {
+__global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(MoveArgs x, const u32* __restrict__ list, u64 count) {
   constexpr int GPB = 256 / G;
   constexpr int N = G * K;
   constexpr int LB = ilog2<N>();
@@ -532,12 +553,29 @@ __global__ void __launch_bounds__(256) lm_psort(MoveArgs x, const u32* __restric
   const u64 stride = u64(gridDim.x) * GPB;
   const ull keep = l2_keep_policy();
   Tally tl;
+
+  auto load_row = [&](u32 v, u64 rlo, u64 rhi, u32 (&t)[K], V (&w)[K]) {
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      const u64 a = rlo + u64(r) * G + lane;
+      const bool ok = a < rhi;
+      t[r] = ok ? __ldcs(x.g.tgt + a) : kEmpty;
+      w[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+    }
+  };
+  auto gather = [&](u32 v, const u32 (&t)[K], u32 (&key)[K]) {
+#pragma unroll
+    for (int r = 0; r < K; ++r)  // self-loops and padding carry no key
+      key[r] = (t[r] != v && t[r] != kEmpty) ? (ld_keep(x.C + t[r], keep) << LB) | u32(r * G + lane) : kNoKey;
+  };
+
+  // prologue: vertex i fully loaded, vertex i+1's header
   u64 i0 = u64(blockIdx.x) * GPB;
   bool have = i0 + gi < count;
   u32 u = 0, from = kEmpty;
   u64 lo = 0, hi = 0;
   double ku = 0.0, sf = 0.0;
-  u32 key[K];
+  u32 key[K], t[K];
   V val[K];
   if (have) {
     u = list[i0 + gi];
@@ -546,28 +584,31 @@ __global__ void __launch_bounds__(256) lm_psort(MoveArgs x, const u32* __restric
     from = x.C[u];
     ku = x.K[u];
   }
-  {
-    u32 t[K];
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
-      const u64 a = lo + u64(r) * G + lane;
-      const bool ok = a < hi;
-      t[r] = ok ? __ldcs(x.g.tgt + a) : u;
-      val[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
-    }
-    if (have) sf = x.sigma[from];
-#pragma unroll
-    for (int r = 0; r < K; ++r)
-      key[r] = t[r] != u ? (ld_keep(x.C + t[r], keep) << LB) | u32(r * G + lane) : kNoKey;
+  load_row(u, lo, hi, t, val);
+  if (have) sf = x.sigma[from];
+  gather(u, t, key);
+  bool have1 = i0 + stride + gi < count;
+  u32 u1 = 0, from1 = kEmpty;
+  u64 lo1 = 0, hi1 = 0;
+  double ku1 = 0.0;
+  if (have1) {
+    u1 = list[i0 + stride + gi];
+    lo1 = x.g.off[u1];
+    hi1 = x.g.off[u1 + 1];
+    from1 = x.C[u1];
+    ku1 = x.K[u1];
   }
 
   for (; i0 < count; i0 += stride) {
-    // stage 1 (next): list entry
-    const u64 in = i0 + stride + gi;
-    const bool nhave = in < count;
-    const u32 nu = nhave ? list[in] : 0u;
+    // (i+1) targets and weights; (i+2) list entry
+    u32 t1[K], key1[K];
+    V val1[K];
+    load_row(u1, lo1, hi1, t1, val1);
+    const u64 in2 = i0 + 2 * stride + gi;
+    const bool have2 = in2 < count;
+    const u32 u2 = have2 ? list[in2] : 0u;
 
-    // current: group the arcs by community, fetch the weights in sorted order
+    // (i) group the arcs by community, fetch the weights in sorted order
     if (K > 1) {
       __syncwarp();
 #pragma unroll
@@ -589,18 +630,11 @@ __global__ void __launch_bounds__(256) lm_psort(MoveArgs x, const u32* __restric
     bool tail[K];
     prun_sums<G, K, V>(ck, run, tail, lane, gshift);
 
-    // stage 2 (next): row bounds, own community, vertex weight
-    u64 nlo = 0, nhi = 0;
-    u32 nfrom = kEmpty;
-    double nku = 0.0;
-    if (nhave) {
-      nlo = x.g.off[nu];
-      nhi = x.g.off[nu + 1];
-      nfrom = x.C[nu];
-      nku = x.K[nu];
-    }
+    // (i+1) communities of its arcs, Sigma of its community
+    gather(u1, t1, key1);
+    const double sf1 = have1 ? x.sigma[from1] : 0.0;
 
-    // current: weight to the own community (one run tail in the group holds it),
+    // (i) weight to the own community (one run tail in the group holds it),
     // Sigma of the candidates
     V own_l = V(0);
     bool has_own = false, cand[K];
@@ -615,22 +649,23 @@ __global__ void __launch_bounds__(256) lm_psort(MoveArgs x, const u32* __restric
     double sc[K];
 #pragma unroll
     for (int r = 0; r < K; ++r) {
-      if (cand[r]) cand[r] = key_ok(x, ck[r]);
+      if (cand[r]) cand[r] = key_ok(x, ck[r]) && (DRY || may_gain(x, double(run[r]), double(own), ku, sf));
       sc[r] = cand[r] ? ld_keep(x.sigma + ck[r], keep) : 0.0;
     }
 
-    // stage 3 (next): arcs
-    u32 nt[K];
-    V nval[K];
-#pragma unroll
-    for (int r = 0; r < K; ++r) {
-      const u64 a = nlo + u64(r) * G + lane;
-      const bool ok = a < nhi;
-      nt[r] = ok ? __ldcs(x.g.tgt + a) : nu;
-      nval[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
+    // (i+2) row bounds, community, vertex weight
+    u64 lo2 = 0, hi2 = 0;
+    u32 from2 = kEmpty;
+    double ku2 = 0.0;
+    if (have2) {
+      lo2 = x.g.off[u2];
+      hi2 = x.g.off[u2 + 1];
+      from2 = x.C[u2];
+      ku2 = x.K[u2];
     }
 
-    // current: rank the candidates, group argmax
+    // (i) rank the candidates, group argmax; the lane holding the best
+    // candidate (lane 0 if none) decides
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
 #pragma unroll
@@ -640,15 +675,6 @@ __global__ void __launch_bounds__(256) lm_psort(MoveArgs x, const u32* __restric
       if (better(g, ck[r], bg, bc)) bg = g, bc = ck[r], bk = double(run[r]);
     }
     const u32 best = group_best<G>(bg, bc);
-
-    // stage 4 (next): communities of the arcs, Sigma of the own community
-    u32 nkey[K];
-#pragma unroll
-    for (int r = 0; r < K; ++r)
-      nkey[r] = nt[r] != nu ? (ld_keep(x.C + nt[r], keep) << LB) | u32(r * G + lane) : kNoKey;
-    const double nsf = nhave ? x.sigma[nfrom] : 0.0;
-
-    // current: the lane holding the best candidate (lane 0 if none) decides
     const bool decider = have && (best == kEmpty ? lane == 0 : bc == best);
     bool moved = false;
     if (decider) {
@@ -657,13 +683,17 @@ __global__ void __launch_bounds__(256) lm_psort(MoveArgs x, const u32* __restric
       tl.arcs += hi - lo;
       moved = decide<DRY>(x, u, from, ku, best, best == kEmpty ? -INFINITY : bg, bk, double(own), tl);
     }
-    if (!DRY && x.prune && ((__ballot_sync(FULL, moved) >> gshift) & GMASK))
-      for (u64 a = lo + lane; a < hi; a += G) x.flags[x.g.tgt[a]] = 1;
-
-    // rotate
-    have = nhave, u = nu, lo = nlo, hi = nhi, from = nfrom, ku = nku, sf = nsf;
+    if (!DRY && x.prune && ((__ballot_sync(FULL, moved) >> gshift) & GMASK)) {
 #pragma unroll
-    for (int r = 0; r < K; ++r) key[r] = nkey[r], val[r] = nval[r];
+      for (int r = 0; r < K; ++r)  // every arc target, u itself on a self-loop (louvain_compact.cpp:160-161)
+        if (t[r] != kEmpty) x.flags[t[r]] = 1;
+    }
+
+    // rotate: i <- i+1 <- i+2
+    have = have1, u = u1, lo = lo1, hi = hi1, from = from1, ku = ku1, sf = sf1;
+    have1 = have2, u1 = u2, lo1 = lo2, hi1 = hi2, from1 = from2, ku1 = ku2;
+#pragma unroll
+    for (int r = 0; r < K; ++r) key[r] = key1[r], val[r] = val1[r], t[r] = t1[r];
   }
   tl.flush(x);
 }

@@ -90,6 +90,28 @@ __device__ __forceinline__ void segmented_runs(const u32 (&key)[K], V (&val)[K],
   for (int r = 0; r < K; ++r) tail[r] = r + 1 < K ? head[r + 1] : (lane == G - 1 || next_head);
 }
 
+// Warp-level pre-combine of one (key, value) per lane before a table insert:
+// when a key other than kEmpty repeats across the warp, the 32 pairs are
+// sorted by key and each run summed. Returns true on the lanes that hold a
+// distinct key's total (never for kEmpty), so each key is inserted once per
+// round instead of once per arc (shared-memory atomics serialise per lane,
+// and same-key CAS loops serialise per address).
+template <class V>
+__device__ __forceinline__ bool warp_combine(u32& key, V& val, u32 lane) {
+  constexpr u32 FULL = 0xffffffffu;
+  const u32 peers = __match_any_sync(FULL, key);
+  if (__any_sync(FULL, key != kEmpty && peers != (1u << lane))) {
+    u32 kk[1] = {key};
+    V vv[1] = {val};
+    bitonic_sort<32, 1, V>(kk, vv, lane);
+    bool tl[1];
+    segmented_runs<32, 1, V>(kk, vv, tl, lane);
+    key = kk[0], val = vv[0];
+    return tl[0] && key != kEmpty;
+  }
+  return key != kEmpty;
+}
+
 // exclusive prefix count of `n` over the G lanes of a group, and the group total
 template <int G>
 __device__ __forceinline__ u32 group_exclusive(u32 n, u32 lane, u32& total) {

@@ -13,4 +13,5 @@ dg = lvn.generate(c["kind"], **{k: v for k, v in c.items() if k not in ("kind", 
 for i in range(runs):
     r = lvn.louvain_compact(dg, None, opts, membership_on_device=True)
     print(cfg, round(r.modularity, 5), r.passes, r.iterations_per_pass, "V", r.vertices_per_pass, "A", r.arcs_per_pass,
-          {k: round(s.seconds * 1e3, 2) for k, s in r.stats.items()}, "pass_ms", [round(x * 1e3, 1) for x in r.pass_seconds], flush=True)
+          {k: round(s.seconds * 1e3, 2) for k, s in r.stats.items()}, "pass_ms", [round(x * 1e3, 1) for x in r.pass_seconds],
+          "move_GBps", round(r.stats["move"].gbps, 1), "move_arcs", r.stats["move"].arcs, "total_ms", round(r.wall_seconds * 1e3, 1), flush=True)
