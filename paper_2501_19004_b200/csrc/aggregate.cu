@@ -181,23 +181,79 @@ __device__ __forceinline__ void ag_merge_round(const Tab& tab, u32 lg, u32 c, u3
   if (warp_combine(key, w, lane)) tab.insert(lg, key, w);
 }
 
-__device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32 c, u32 lg, double* red,
+// Block per community (budget <= block_max): the community's member arcs are
+// enumerated flat, thread t taking arcs t, t + 512, ... of the concatenated
+// member rows (member found by binary search in an smem prefix of member
+// degrees), so a hub member is spread over the whole block instead of one
+// warp while the others wait at the barrier. Communities with more members
+// than the prefix holds (many arc-less members) take the member loops.
+constexpr u32 kPrefixCap = 4096;
+
+__device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, u32 lg, double* red,
                              u32* red_seen, u32* cursor) {
   const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   constexpr int W = kBlockThreads / 32;
-  const u64 mlo = x.coff[c], mhi = x.coff[c + 1];
+  const u64 mlo = x.coff[c], mhi = x.coff[c + 1], nm = mhi - mlo;
   const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
-  const u64 budget = x.boff[c + 1] - x.boff[c];
   const u32 S = 1u << lg;
   for (u32 s = threadIdx.x; s < S; s += kBlockThreads) tab.clear(s);
   if (threadIdx.x == 0) *cursor = 0;
-  __syncthreads();
   double own = 0.0;
   u32 own_seen = 0;
-  if (budget >= (mhi - mlo) * 16) {  // warp per member, lanes across its row
+  if (nm <= kPrefixCap) {
+    // pre[k] = arcs of members [0, k): block-wide exclusive scan in chunks
+    u32 run = 0;
+    for (u64 k0 = 0; k0 < nm; k0 += kBlockThreads) {
+      const u64 k = k0 + threadIdx.x;
+      u32 d = 0;
+      if (k < nm) {
+        const u32 v = x.members[mlo + k];
+        d = u32(x.g.off[v + 1] - x.g.off[v]);
+      }
+      u32 inc = d;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const u32 y = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= u32(o)) inc += y;
+      }
+      if (lane == 31) red_seen[wid] = inc;
+      __syncthreads();
+      u32 before = run;
+      for (u32 w = 0; w < wid; ++w) before += red_seen[w];
+      if (k < nm) pre[k] = before + inc - d;
+      u32 tot = 0;
+      for (int w = 0; w < W; ++w) tot += red_seen[w];
+      run += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) pre[nm] = run;
+    __syncthreads();
+    const u32 E = run;
+    // uniform trip count over the block: every warp runs every round
+    for (u32 e0 = 0; e0 < E; e0 += kBlockThreads) {
+      const u32 e = e0 + threadIdx.x;
+      u32 key = kEmpty;
+      double w = 0.0;
+      if (e < E) {
+        u32 lo = 0, hi = u32(nm);  // last k with pre[k] <= e
+        while (hi - lo > 1) {
+          const u32 mid = (lo + hi) >> 1;
+          if (pre[mid] <= e) lo = mid; else hi = mid;
+        }
+        const u32 v = x.members[mlo + lo];
+        const u64 a = x.g.off[v] + (e - pre[lo]);
+        key = x.C[__ldcs(x.g.tgt + a)];
+        w = double(__ldcs(x.g.w + a));
+      }
+      ag_merge_round(tab, lg, c, key, w, lane, own, own_seen);
+    }
+  } else {
+    __syncthreads();
+    // rows of >= 32 arcs: a warp across each row; shorter rows: a lane each
     for (u64 k = mlo + wid; k < mhi; k += W) {
       const u32 v = x.members[k];
       const u64 lo = x.g.off[v], hi = x.g.off[v + 1];
+      if (hi - lo < 32) continue;
       for (u64 a0 = lo; a0 < hi; a0 += 32) {
         const u64 a = a0 + lane;
         const u32 key = a < hi ? x.C[__ldcs(x.g.tgt + a)] : kEmpty;
@@ -205,13 +261,13 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32 c, u32 lg, do
         ag_merge_round(tab, lg, c, key, w, lane, own, own_seen);
       }
     }
-  } else {  // lane per member, one arc per lane per round
     for (u64 k0 = mlo + u64(wid) * 32; k0 < mhi; k0 += u64(W) * 32) {
       const u64 k = k0 + lane;
       u64 a = 0, hi = 0;
       if (k < mhi) {
         const u32 v = x.members[k];
         a = x.g.off[v], hi = x.g.off[v + 1];
+        if (hi - a >= 32) hi = a;  // taken by the warp loop above
       }
       for (; __any_sync(0xffffffffu, a < hi); ++a) {
         const u32 key = a < hi ? x.C[x.g.tgt[a]] : kEmpty;
@@ -222,6 +278,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32 c, u32 lg, do
   }
   own = warp_sum(own);
   own_seen = __any_sync(0xffffffffu, own_seen);
+  __syncthreads();  // red_seen doubled as scan scratch
   if (lane == 0) red[wid] = own, red_seen[wid] = own_seen;
   __syncthreads();
   for (u32 s = threadIdx.x; s < S; s += kBlockThreads) {
@@ -257,6 +314,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_block(AggArgs x, const u32* 
   __shared__ u32 red_seen[kBlockThreads / 32];
   __shared__ u32 cursor;
   const Tab stab(smem, u64(1) << kBlockCapLog);
+  u32* pre = reinterpret_cast<u32*>(smem + (size_t(1) << kBlockCapLog) * Tab::kSlotBytes);
   for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
     const u32 c = list[i];
     const u64 hcap = x.hoff[c + 1] - x.hoff[c];
@@ -265,7 +323,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_block(AggArgs x, const u32* 
       if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
       continue;
     }
-    ag_block_one(x, stab, c, lg, red, red_seen, &cursor);
+    ag_block_one(x, stab, pre, c, lg, red, red_seen, &cursor);
   }
 }
 
@@ -507,7 +565,7 @@ void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
     LVN_LAUNCH();
   }
   if (b.count(kBinBlock)) {
-    const size_t smem = (size_t(1) << kBlockCapLog) * Tab::kSlotBytes;
+    const size_t smem = (size_t(1) << kBlockCapLog) * Tab::kSlotBytes + (kPrefixCap + 1) * sizeof(u32);
     static const int occ = occupancy(ag_block, kBlockThreads, smem);
     const u64 blocks = std::min<u64>(b.count(kBinBlock), u64(sms) * occ);
     ag_block<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(kBinBlock), b.count(kBinBlock));
