@@ -21,6 +21,7 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+#include <string>
 #include <cooperative_groups/reduce.h>
 
 #include "kernels.cuh"
@@ -331,20 +332,54 @@ __global__ void __launch_bounds__(kBlockThreads) ag_block(AggArgs x, const u32* 
 // The members of the big communities (grouped by community, vertices without
 // arcs dropped) form a list L whose arcs are cut into fixed chunks of kBigChunk
 // arcs, one chunk per warp task: a hub row is split across many warps and the
-// warps of one community run together, so its HBM table stays hot in L2. Every
-// arc merges into its community's table (claim by CAS, fp64 reductions, a
-// live-slot list); the weight to the community itself (the super-vertex
-// self-loop, usually the dominant key) is summed per lane while the lane stays
-// in one community and added once per run. Then one block per community emits
-// the row.
+// warps of one community run together, so its HBM region stays hot in L2. The
+// weight to the community itself (the super-vertex self-loop, usually the
+// dominant key) is summed per lane while the lane stays in one community and
+// added once per run; the other arcs are pre-combined across the warp and
+// merged into the community's region:
+//   hash  : 16-byte slots {key, fp64 value} (one sector per probe), claimed by
+//           CAS (one L2 round trip per probe), fp64 L2 reductions, a live list;
+//   dense : when the hash table would outgrow a dense fp64 array over all
+//           `count` target communities, the array itself (no keys, no probing:
+//           one reduction per arc; present entries are the ones no longer -0.0).
+// Then one block per community emits the row.
 constexpr u64 kBigChunk = 1024;
+constexpr ull kDenseEmpty = 0x8000000000000000ull;  // -0.0: never produced by adding a weight
+
+struct BigSlot {
+  u32 key;
+  u32 pad;
+  double val;
+};
 
 __device__ __forceinline__ u64 big_slots(u64 hcap) {
   const u32 l = ceil_log2_u64(2 * (hcap ? hcap : 1));
   return u64(1) << (l > 5 ? l : 5);
 }
-__device__ __forceinline__ u64 big_region_bytes(u64 slots) {
-  return (slots * Tab::kSlotBytes + slots / 2 * 4 + 15) & ~u64(15);
+__device__ __forceinline__ bool big_dense(u64 hcap, u32 count, int mode) {
+  if (mode) return mode == 2;
+  return big_slots(hcap) * sizeof(BigSlot) >= u64(count) * sizeof(double);
+}
+__device__ __forceinline__ u64 big_region_bytes(u64 hcap, u32 count, int mode) {
+  if (big_dense(hcap, count, mode)) return (u64(count) * sizeof(double) + 15) & ~u64(15);
+  const u64 slots = big_slots(hcap);
+  return (slots * sizeof(BigSlot) + slots / 2 * 4 + 15) & ~u64(15);
+}
+// claim-or-find by CAS (one round trip per probe); returns the slot, and
+// whether this call claimed it
+__device__ __forceinline__ u32 big_insert(BigSlot* t, u64 slots, u32 key, double w, bool& fresh) {
+  const u32 lg = ceil_log2_u64(slots);
+  const u32 mask = u32(slots - 1);
+  u32 h = slot_hash(key, lg);
+  while (true) {
+    const u32 cur = atomicCAS(&t[h].key, kEmpty, key);
+    if (cur == kEmpty || cur == key) {
+      atomicAdd(&t[h].val, w);
+      fresh = cur == kEmpty;
+      return h;
+    }
+    h = (h + 1) & mask;
+  }
 }
 // largest i in [0, n) with p[i] <= x (p ascending, p[0] <= x)
 __device__ __forceinline__ u64 last_le(const u64* __restrict__ p, u64 n, u64 x) {
@@ -356,24 +391,31 @@ __device__ __forceinline__ u64 last_le(const u64* __restrict__ p, u64 n, u64 x) 
   return lo;
 }
 
-__global__ void ag_big_plan(const u32* __restrict__ big, u64 nbig, const u64* __restrict__ hoff,
+__global__ void ag_big_plan(const u32* __restrict__ big, u64 nbig, u32 count, int mode, const u64* __restrict__ hoff,
                             const u64* __restrict__ coff, u32* __restrict__ index, u64* __restrict__ bytes,
                             u32* __restrict__ mcount) {
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < nbig; i += u64(gridDim.x) * blockDim.x) {
     const u32 c = big[i];
     index[c] = u32(i);
-    bytes[i] = big_region_bytes(big_slots(hoff[c + 1] - hoff[c]));
+    bytes[i] = big_region_bytes(hoff[c + 1] - hoff[c], count, mode);
     mcount[i] = u32(coff[c + 1] - coff[c]);
   }
 }
 
-__global__ void ag_big_clear(const u32* __restrict__ big, u64 nbig, const u64* __restrict__ hoff,
+__global__ void ag_big_clear(const u32* __restrict__ big, u64 nbig, u32 count, int mode, const u64* __restrict__ hoff,
                              const u64* __restrict__ tab_off, unsigned char* tables) {
   for (u64 i = blockIdx.x; i < nbig; i += gridDim.x) {
     const u32 c = big[i];
-    const u64 slots = big_slots(hoff[c + 1] - hoff[c]);
-    const Tab tab(tables + tab_off[i], slots);
-    for (u64 s = threadIdx.x; s < slots; s += blockDim.x) tab.clear(u32(s));
+    const u64 hcap = hoff[c + 1] - hoff[c];
+    unsigned char* base = tables + tab_off[i];
+    if (big_dense(hcap, count, mode)) {
+      ull* d = reinterpret_cast<ull*>(base);
+      for (u64 j = threadIdx.x; j < count; j += blockDim.x) d[j] = kDenseEmpty;
+    } else {
+      BigSlot* t = reinterpret_cast<BigSlot*>(base);
+      const u64 slots = big_slots(hcap);
+      for (u64 j = threadIdx.x; j < slots; j += blockDim.x) t[j] = BigSlot{kEmpty, 0u, 0.0};
+    }
   }
 }
 
@@ -447,7 +489,7 @@ __global__ void __launch_bounds__(256) ag_big_arcs(AggArgs x, const u32* __restr
           key = kEmpty;
         }
       }
-      // a batch inside one community (the usual case): one insert per distinct key
+      // a batch inside one community (the usual case): one merge per distinct key
       const u32 phi = __reduce_max_sync(0xffffffffu, key != kEmpty ? pi : 0u);
       const u32 plo = __reduce_min_sync(0xffffffffu, key != kEmpty ? pi : ~0u);
       if (phi == plo) {
@@ -457,11 +499,16 @@ __global__ void __launch_bounds__(256) ag_big_arcs(AggArgs x, const u32* __restr
       } else if (key == kEmpty) {
         continue;
       }
-      const u64 slots = big_slots(x.hoff[c + 1] - x.hoff[c]);
+      const u64 hcap = x.hoff[c + 1] - x.hoff[c];
       unsigned char* base = tables + tab_off[pi];
-      const Tab tab(base, slots);
-      const int s = tab.insert(ceil_log2_u64(slots), key, wt);
-      if (s >= 0) reinterpret_cast<u32*>(base + slots * Tab::kSlotBytes)[atomicAdd(&live_n[pi], 1u)] = u32(s);
+      if (big_dense(hcap, x.count, x.big_mode)) {
+        atomicAdd(reinterpret_cast<double*>(base) + key, wt);
+      } else {
+        const u64 slots = big_slots(hcap);
+        bool fresh;
+        const u32 sl = big_insert(reinterpret_cast<BigSlot*>(base), slots, key, wt, fresh);
+        if (fresh) reinterpret_cast<u32*>(base + slots * sizeof(BigSlot))[atomicAdd(&live_n[pi], 1u)] = sl;
+      }
     }
     if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
   }
@@ -469,35 +516,61 @@ __global__ void __launch_bounds__(256) ag_big_arcs(AggArgs x, const u32* __restr
 
 __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, const u32* __restrict__ big, u64 nbig,
                                                              const u64* __restrict__ tab_off,
-                                                             unsigned char* tables, const u32* __restrict__ live_n,
+                                                             unsigned char* tables, u32* __restrict__ live_n,
                                                              const double* __restrict__ own_sum,
                                                              const u32* __restrict__ own_seen) {
+  __shared__ u32 cursor;
   for (u64 i = blockIdx.x; i < nbig; i += gridDim.x) {
     const u32 c = big[i];
     const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
-    const u64 slots = big_slots(hcap);
     unsigned char* base = tables + tab_off[i];
-    const Tab tab(base, slots);
-    const u32* live = reinterpret_cast<const u32*>(base + slots * Tab::kSlotBytes);
-    const u32 n = live_n[i];
     const u32 self = own_seen[i] ? 1u : 0u;
-    if (n + self > hcap) {
-      if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
-      continue;
-    }
-    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) {
-      u32 key;
-      double val;
-      tab.read(live[j], key, val);
-      x.htgt[hbase + j] = key;
-      x.hw[hbase + j] = float(val);  // fp64 sum narrowed once
+    u32 n = 0;
+    if (big_dense(hcap, x.count, x.big_mode)) {
+      // present entries of the dense array, compacted through a block cursor
+      if (threadIdx.x == 0) cursor = 0;
+      __syncthreads();
+      const ull* d = reinterpret_cast<const ull*>(base);
+      for (u64 j0 = 0; j0 < x.count; j0 += kBlockThreads) {
+        const u64 j = j0 + threadIdx.x;
+        const ull bits = j < x.count ? d[j] : kDenseEmpty;
+        const bool live = bits != kDenseEmpty;
+        const u32 bal = __ballot_sync(0xffffffffu, live);
+        u32 wbase = 0;
+        if ((threadIdx.x & 31) == 0 && bal) wbase = atomicAdd(&cursor, __popc(bal));
+        wbase = __shfl_sync(0xffffffffu, wbase, 0);
+        if (live) {
+          const u32 o = wbase + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
+          if (o < hcap) {
+            x.htgt[hbase + o] = u32(j);
+            x.hw[hbase + o] = float(__longlong_as_double((long long)bits));  // fp64 sum narrowed once
+          }
+        }
+      }
+      __syncthreads();
+      n = cursor;
+      __syncthreads();
+    } else {
+      const u64 slots = big_slots(hcap);
+      const BigSlot* t = reinterpret_cast<const BigSlot*>(base);
+      const u32* live = reinterpret_cast<const u32*>(base + slots * sizeof(BigSlot));
+      n = live_n[i];
+      for (u32 j = threadIdx.x; j < n && j < hcap; j += kBlockThreads) {
+        const BigSlot e = t[live[j]];
+        x.htgt[hbase + j] = e.key;
+        x.hw[hbase + j] = float(e.val);  // fp64 sum narrowed once
+      }
     }
     if (threadIdx.x == 0) {
-      if (self) {
-        x.htgt[hbase + n] = c;
-        x.hw[hbase + n] = float(own_sum[i]);
+      if (n + self > hcap) {
+        atomicOr(x.err, u32(kErrTable));
+      } else {
+        if (self) {
+          x.htgt[hbase + n] = c;
+          x.hw[hbase + n] = float(own_sum[i]);
+        }
+        x.fill[c] = n + self;
       }
-      x.fill[c] = n + self;
     }
   }
 }
@@ -535,8 +608,10 @@ int occupancy(K kernel, int threads, size_t smem) {
 }  // namespace
 
 
-void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
+void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
   const int sms = sm_count();
+  AggArgs a = a0;
+  if (const char* e = std::getenv("LVN_BIG_MODE")) a.big_mode = std::string(e) == "hash" ? 1 : std::string(e) == "dense" ? 2 : 0;
   if (b.edges.thread_max > 8 || b.edges.group_max > 256 || b.edges.warp_max > 256 ||
       b.edges.block_max > 4096)
     fail(kInvalid, "aggregation bin edges exceed the device table capacities");
@@ -581,7 +656,7 @@ void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
     LVN_CUDA(cudaMemsetAsync(own_seen.p, 0, nbig * sizeof(u32), s));
     LVN_CUDA(cudaMemsetAsync(own.p, 0, nbig * sizeof(double), s));
     const unsigned pg = unsigned(std::min<u64>((nbig + 255) / 256, u64(sms) * 4));
-    ag_big_plan<<<pg, 256, 0, s>>>(big, nbig, a.hoff, a.coff, index.p, bytes.p, mcount.p);
+    ag_big_plan<<<pg, 256, 0, s>>>(big, nbig, a.count, a.big_mode, a.hoff, a.coff, index.p, bytes.p, mcount.p);
     LVN_LAUNCH();
     exclusive_scan_u64(bytes.p, tab_off.p, nbig, s);
     exclusive_scan_u32_to_u64(mcount.p, moff.p, nbig, s);
@@ -629,8 +704,8 @@ void aggregate_rows(const AggArgs& a, const Bins& b, cudaStream_t s) {
       if (!nb) continue;
       // regions of this batch start at the buffer's base
       unsigned char* base = tables.p - h_tab[b0];
-      ag_big_clear<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), 256, 0, s>>>(big + b0, nb, a.hoff, tab_off.p + b0,
-                                                                              base);
+      ag_big_clear<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), 256, 0, s>>>(big + b0, nb, a.count, a.big_mode, a.hoff,
+                                                                              tab_off.p + b0, base);
       LVN_LAUNCH();
       // arc range of the batch: members [moff[b0], moff[b1]) -> kept L entries -> P
       u64 arc_lo = 0, arc_hi = ~u64(0);

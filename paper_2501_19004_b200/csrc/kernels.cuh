@@ -161,6 +161,7 @@ struct AggArgs {
   float* hw = nullptr;
   u32* fill = nullptr;           // entries written per row
   u32* err = nullptr;
+  int big_mode = 0;              // giant-community regions: 0 by size, 1 hash, 2 dense (LVN_BIG_MODE)
 };
 // Synchronises once when the kBinGlobal bin is non-empty (sizes its HBM tables).
 void aggregate_rows(const AggArgs& a, const Bins& bins, cudaStream_t s);

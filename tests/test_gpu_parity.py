@@ -199,6 +199,20 @@ def test_aggregate_member_parallel_batched(lvn, port, monkeypatch):
     agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
 
 
+@pytest.mark.parametrize("mode", ["hash", "dense"])
+def test_aggregate_member_parallel_modes(lvn, port, monkeypatch, mode):
+    # giant-community regions: 16-byte-slot hash tables or dense fp64 arrays
+    monkeypatch.setenv("LVN_BIG_MODE", mode)
+    g = hubs_graph(30000, 4, 20000, 100000, 6)
+    for m in ((np.arange(g.n) % 2).astype(np.uint32), random_membership(g.n, 50, 4)):
+        agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
+    g = random_graph(40000, 400000, 95)
+    m = random_membership(g.n, 3000, 9).astype(np.int64)
+    m[: 24000] = np.arange(24000) % 3
+    m = np.unique(m, return_inverse=True)[1].astype(np.uint32)
+    agg_equal(lvn.compact_aggregate(G_(g, lvn), m), port.aggregate(g, m))
+
+
 def test_aggregate_member_parallel_hubs(lvn, port):
     g = hubs_graph(30000, 4, 20000, 100000, 5)
     for m in (np.zeros(g.n, np.uint32), (np.arange(g.n) % 2).astype(np.uint32),
