@@ -13,9 +13,9 @@ louvain_mc.cpp:163-247) over one synthetic graph.
 Inputs are far larger than L2 (C2: 2.6 GB of CSR vs 126 MB L2), so no flush
 is needed between steps.
 
-N > 1 (torchrun, one process per GPU): every rank runs its own replica of the
-workload (the vertex-sharded multi-GPU engine is SURVEY 8(e), not built yet);
-value = total arcs processed by all ranks / max-over-ranks time.
+N > 1 (torchrun, one process per GPU): the row-sharded engine
+(lvn_louvain_sharded, SURVEY 8(e)) over NCCL, one graph for the whole job;
+value = arcs / max-over-ranks time (strong scaling).
 """
 
 from __future__ import annotations
@@ -114,6 +114,15 @@ def measured_peaks():
         return float(d["hbm_gbs"]), "measured"
     except Exception:
         return 6650.0, "fallback"
+
+
+def gather_peak():
+    """measured whole-GPU rate of random 4-byte loads (profiles/gather_peak.json)"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "gather_peak.json")) as f:
+            return float(json.load(f)["gathers_per_s"])
+    except Exception:
+        return None
 
 
 def traffic_from_profile(config):
@@ -299,6 +308,7 @@ def main():
     move_gbps = mv.bytes / mv.seconds / 1e9 if mv.seconds else 0.0
     per_launch_bytes = mv.bytes / max(mv.launches, 1)
     traffic = traffic_from_profile(args.config)
+    gpeak = gather_peak()
 
     # ---- e2e: host (pinned) buffers through the public API ------------------------
     e2e = None
@@ -342,6 +352,8 @@ def main():
             "modularity": r.modularity, "num_communities": r.num_communities, "passes": r.passes,
             "sharded_passes": r.sharded_passes, "exchange_seconds": r.exchange_seconds,
             "iterations_per_pass": r.iterations_per_pass,
+            "pass_ms": [round(x * 1e3, 2) for x in r.pass_seconds],
+            "step_ms": [round(x.wall_seconds * 1e3, 2) for x in results],
             "phase_seconds": {"local_moving": r.phase.local_moving, "aggregation": r.phase.aggregation,
                               "other": r.phase.other},
             "kernel_seconds": {k: s.seconds for k, s in r.stats.items()},
@@ -352,7 +364,13 @@ def main():
                          "achieved": move_gbps, "peak": peak, "peak_kind": peak_kind, "unit": "GB/s",
                          "frac": move_gbps / peak if peak else None,
                          "bytes_per_launch": per_launch_bytes,
-                         "traffic": traffic},
+                         "traffic": traffic,
+                         # the ceiling that binds a sweep: random element accesses
+                         # (C[t], Sigma[c] gathers, neighbour marks) against the
+                         # measured random-gather rate of the L1TEX path
+                         "gather": {"achieved": mv.gathers_per_second, "peak": gpeak, "unit": "random accesses/s",
+                                    "frac": mv.gathers_per_second / gpeak if gpeak else None,
+                                    "per_arc": mv.gathers / mv.arcs if mv.arcs else None}},
             "cpu_baseline": cpu, "cpu_modularity": cpu_q,
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }

@@ -128,6 +128,7 @@ typedef struct lvn_phase_stats {
   uint64_t launches;
   uint64_t items;        /* vertices processed */
   uint64_t arcs;         /* arcs scanned */
+  uint64_t gathers;      /* random element accesses: C[t] and Sigma[c] gathers, neighbour marks */
 } lvn_phase_stats;
 
 enum { LVN_STAT_MOVE = 0, LVN_STAT_AGGREGATE = 1, LVN_STAT_RENUMBER = 2, LVN_STAT_RESET = 3,

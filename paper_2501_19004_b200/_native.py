@@ -79,6 +79,7 @@ class lvn_phase_stats(C.Structure):
         ("launches", C.c_uint64),
         ("items", C.c_uint64),
         ("arcs", C.c_uint64),
+        ("gathers", C.c_uint64),
     ]
 
 

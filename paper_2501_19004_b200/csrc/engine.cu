@@ -331,7 +331,7 @@ struct Timing {
     cudaEvent_t a, b;
     int fam;
     double bytes;
-    ull items, arcs;
+    ull items, arcs, gathers;
   };
   std::vector<Span> spans;
   std::vector<cudaEvent_t> free_events;
@@ -346,7 +346,7 @@ struct Timing {
     return e;
   }
   size_t begin(int fam, cudaStream_t s) {
-    Span sp{ev(), ev(), fam, 0.0, 0, 0};
+    Span sp{ev(), ev(), fam, 0.0, 0, 0, 0};
     LVN_CUDA(cudaEventRecord(sp.a, s));
     spans.push_back(sp);
     return spans.size() - 1;
@@ -357,8 +357,8 @@ struct Timing {
     spans[i].items = items;
     spans[i].arcs = arcs;
   }
-  void set_bytes(size_t i, double bytes, ull items, ull arcs) {
-    spans[i].bytes = bytes, spans[i].items = items, spans[i].arcs = arcs;
+  void set_bytes(size_t i, double bytes, ull items, ull arcs, ull gathers = 0) {
+    spans[i].bytes = bytes, spans[i].items = items, spans[i].arcs = arcs, spans[i].gathers = gathers;
   }
   void collect(lvn_phase_stats* st) {
     for (auto& sp : spans) {
@@ -371,6 +371,7 @@ struct Timing {
       f.launches += 1;
       f.items += sp.items;
       f.arcs += sp.arcs;
+      f.gathers += sp.gathers;
       free_events.push_back(sp.a);
       free_events.push_back(sp.b);
     }
@@ -386,7 +387,7 @@ constexpr int kMaxRanges = 64;
 
 struct IterRecord {  // device scratch read back once per iteration
   double gain;
-  ull verts, arcs, moves;
+  ull verts, arcs, moves, gathers;
   ull active[kMaxRanges * kBins];  // per-(range, bin) sizes of the next active lists
 };
 
@@ -804,7 +805,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       sp = sp0;
       if (shard) {
         cm.allreduce(&rec.p->gain, 1, LVN_F64, LVN_SUM, s);
-        cm.allreduce(&rec.p->verts, 3, LVN_U64, LVN_SUM, s);
+        cm.allreduce(&rec.p->verts, 4, LVN_U64, LVN_SUM, s);
       }
       if (p.prune)
         for (int k = 0; k < R; ++k)
@@ -812,7 +813,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       IterRecord* h = reinterpret_cast<IterRecord*>(c.pinned);
       LVN_CUDA(cudaMemcpyAsync(h, rec.p, sizeof(IterRecord), cudaMemcpyDeviceToHost, s));
       LVN_CUDA(cudaStreamSynchronize(s));
-      tm.set_bytes(sp, 12.0 * double(h->arcs) + 32.0 * double(h->verts), h->verts, h->arcs);
+      tm.set_bytes(sp, 12.0 * double(h->arcs) + 32.0 * double(h->verts), h->verts, h->arcs, h->gathers);
       if (verbose())
         std::fprintf(stderr, "[lvn] pass %d it %d: %llu vertices, %llu arcs, %llu moves, gain %.6g\n", pass, it,
                      (unsigned long long)h->verts, (unsigned long long)h->arcs, (unsigned long long)h->moves,

@@ -87,7 +87,7 @@ struct MoveArgs {
   u32* out_to = nullptr;
   double* out_gain = nullptr;
   double* gain_acc = nullptr;  // summed gain of applied moves
-  ull* counters = nullptr;     // [0] vertices processed, [1] arcs scanned, [2] moves
+  ull* counters = nullptr;     // [0] vertices processed, [1] arcs scanned, [2] moves, [3] random accesses
   u32* err = nullptr;
   u64 chunk = ~u64(0);         // max vertices of one bin decided per launch
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep

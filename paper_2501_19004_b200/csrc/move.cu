@@ -55,15 +55,16 @@ constexpr int kBatch = 4;          // arcs (and ranked entries) in flight per la
 // ---- per-thread accounting, flushed once per thread at kernel exit ----------
 struct Tally {
   double gain = 0.0;
-  ull verts = 0, arcs = 0, moves = 0;
+  ull verts = 0, arcs = 0, moves = 0, rand = 0;  // rand: random element accesses of this lane
   __device__ void flush(const MoveArgs& x) {
     const double g = warp_sum(gain);
-    const ull v = warp_sum(verts), a = warp_sum(arcs), m = warp_sum(moves);
+    const ull v = warp_sum(verts), a = warp_sum(arcs), m = warp_sum(moves), r = warp_sum(rand);
     if ((threadIdx.x & 31) == 0) {
       if (g != 0.0) atomicAdd(x.gain_acc, g);
       if (v) atomicAdd(&x.counters[0], v);
       if (a) atomicAdd(&x.counters[1], a);
       if (m) atomicAdd(&x.counters[2], m);
+      if (r) atomicAdd(&x.counters[3], r);
     }
   }
 };
@@ -203,12 +204,15 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
         if (c[j] == ck) sum += wv[j];
       if (first && (DRY || may_gain(x, double(sum), double(own), ku, sf))) {
         const double g = score<DRY>(x, double(sum), double(own), ku, x.sigma[ck], sf);
+        ++tl.rand;
         if (better(g, ck, bg, bc)) bg = g, bc = ck, bk = double(sum);
       }
     }
     ++tl.verts;
     tl.arcs += d;
+    tl.rand += d;
     if (decide<DRY>(x, u, from, ku, bc, bg, bk, double(own), tl) && x.prune) {
+      tl.rand += d;
 #pragma unroll
       for (int k = 0; k < kThreadMaxD; ++k)
         if (k < d) x.flags[t[k]] = 1;
@@ -361,10 +365,11 @@ __global__ void __launch_bounds__(THREADS, 4) lm_group(MoveArgs x, const u32* __
       *nlive = 0;
       ++tl.verts;
       tl.arcs += d;
+      tl.rand += d + n;
       moved = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own), tl);
     }
     if (!DRY && tile.shfl(moved, 0) && x.prune)
-      for (u64 a = lo + lane; a < lo + d; a += G) x.flags[x.g.tgt[a]] = 1;
+      for (u64 a = lo + lane; a < lo + d; a += G) x.flags[x.g.tgt[a]] = 1, ++tl.rand;
     tile.sync();
   }
   tl.flush(x);
@@ -432,6 +437,8 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
 
     // current: sort by community (padding and self-loops carry kEmpty and
     // sort last); K_{u->c} lands on the last element of each run
+#pragma unroll
+    for (int r = 0; r < K; ++r) tl.rand += key[r] != kEmpty ? 1 : 0;
     bitonic_sort<G, K, V>(key, val, lane);
     bool tail[K];
     segmented_runs<G, K, V>(key, val, tail, lane);
@@ -464,6 +471,7 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
     for (int r = 0; r < K; ++r) {
       if (cand[r]) cand[r] = key_ok(x, key[r]) && (DRY || may_gain(x, double(run[r]), double(own), ku, sf));
       sc[r] = cand[r] ? ld_keep(x.sigma + key[r], keep) : 0.0;
+      tl.rand += cand[r] ? 1 : 0;
     }
 
     // stage 3 (next): arcs
@@ -512,7 +520,7 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
     if (!DRY && moved && x.prune) {
 #pragma unroll
       for (int r = 0; r < K; ++r)
-        if (t[r] != kEmpty) x.flags[t[r]] = 1;
+        if (t[r] != kEmpty) x.flags[t[r]] = 1, ++tl.rand;
     }
 
     // rotate
@@ -615,6 +623,8 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
       for (int r = 0; r < K; ++r) gbuf[r * G + lane] = val[r];
       __syncwarp();
     }
+#pragma unroll
+    for (int r = 0; r < K; ++r) tl.rand += key[r] != kNoKey ? 1 : 0;
     psort<G, K>(key, dirs);
     u32 ck[K];
     V run[K];
@@ -651,6 +661,7 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
     for (int r = 0; r < K; ++r) {
       if (cand[r]) cand[r] = key_ok(x, ck[r]) && (DRY || may_gain(x, double(run[r]), double(own), ku, sf));
       sc[r] = cand[r] ? ld_keep(x.sigma + ck[r], keep) : 0.0;
+      tl.rand += cand[r] ? 1 : 0;
     }
 
     // (i+2) row bounds, community, vertex weight
@@ -686,7 +697,7 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
     if (!DRY && x.prune && ((__ballot_sync(FULL, moved) >> gshift) & GMASK)) {
 #pragma unroll
       for (int r = 0; r < K; ++r)  // every arc target, u itself on a self-loop (louvain_compact.cpp:160-161)
-        if (t[r] != kEmpty) x.flags[t[r]] = 1;
+        if (t[r] != kEmpty) x.flags[t[r]] = 1, ++tl.rand;
     }
 
     // rotate: i <- i+1 <- i+2
@@ -858,13 +869,14 @@ __global__ void __launch_bounds__(256) lm_match(MoveArgs x, const u32* __restric
       if (!DRY) x.flags[u] = 0;
       ++tl.verts;
       tl.arcs += hi - lo;
+      tl.rand += hi - lo + n;
       moved = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own), tl);
     }
     moved = __shfl_sync(FULL, moved, 0);
     if (!DRY && moved && x.prune) {
 #pragma unroll
       for (int r = 0; r < K; ++r)
-        if (t[r] != kEmpty) x.flags[t[r]] = 1;
+        if (t[r] != kEmpty) x.flags[t[r]] = 1, ++tl.rand;
     }
 
     have = nhave, u = nu, lo = nlo, hi = nhi, from = nfrom, ku = nku, sf = nsf;
@@ -948,11 +960,12 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
       nlive = 0;
       ++tl.verts;
       tl.arcs += d;
+      tl.rand += d + n;
       bcast = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own_all), tl);
     }
     __syncthreads();
     if (!DRY && bcast && x.prune)
-      for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) x.flags[x.g.tgt[a]] = 1;
+      for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) x.flags[x.g.tgt[a]] = 1, ++tl.rand;
     __syncthreads();
   }
   tl.flush(x);
@@ -1110,11 +1123,12 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_decide(MoveArgs x, const
       if (!DRY) x.flags[u] = 0;
       ++tl.verts;
       tl.arcs += d;
+      tl.rand += d + n;
       bcast = decide<DRY>(x, u, from, ku, bc, bg, bk, own, tl);
     }
     __syncthreads();
     if (!DRY && bcast && x.prune)
-      for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) x.flags[x.g.tgt[a]] = 1;
+      for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) x.flags[x.g.tgt[a]] = 1, ++tl.rand;
     __syncthreads();
   }
   tl.flush(x);

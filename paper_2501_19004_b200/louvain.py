@@ -148,10 +148,15 @@ class KernelStats:
     launches: int
     items: int
     arcs: int
+    gathers: int = 0  # random element accesses (local moving: C[t], Sigma[c], neighbour marks)
 
     @property
     def gbps(self) -> float:
         return self.bytes / self.seconds / 1e9 if self.seconds > 0 else 0.0
+
+    @property
+    def gathers_per_second(self) -> float:
+        return self.gathers / self.seconds if self.seconds > 0 else 0.0
 
 
 @dataclass
@@ -413,7 +418,7 @@ def _result(out) -> LouvainResult:
             arcs_per_pass=lst(r.arcs_per_pass),
             h2d_seconds=r.h2d_seconds,
             d2h_seconds=r.d2h_seconds,
-            stats={name: KernelStats(s.seconds, s.bytes, s.launches, s.items, s.arcs)
+            stats={name: KernelStats(s.seconds, s.bytes, s.launches, s.items, s.arcs, s.gathers)
                    for name, s in zip(N.STAT_NAMES, r.stats)},
             num_shards=max(r.num_shards, 1),
             sharded_passes=r.sharded_passes,
