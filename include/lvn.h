@@ -192,6 +192,16 @@ int lvn_community_csr(const uint32_t* membership, uint32_t n, uint32_t count, in
 /* compact_aggregate / louvain_aggregate (louvain_compact.hpp:76-77, louvain_mc.hpp:96-97):
  * contiguous membership required; fp64 accumulation narrowed once to f32;
  * canonical != 0 sorts each row by target. */
+/* build_csr (graph.cpp:15-87) on the device: num_triples host triples
+ * (sources[i], targets[i], weights[i]) -> CSR with every row sorted by target,
+ * parallel arcs merged (fp64 sum in (target, weight) order, one f32 narrowing)
+ * and, when symmetrize != 0, the reverse arc of every non-loop triple added.
+ * Errors: LVN_INVALID for endpoints >= num_vertices or weights that are not
+ * finite and non-negative (std::invalid_argument in the reference).
+ * Replaces build_csr(const EdgeList&, bool) (graph.hpp / graph.cpp:15). */
+int lvn_build_csr(uint32_t num_vertices, uint64_t num_triples, const uint32_t* sources,
+                  const uint32_t* targets, const double* weights, int symmetrize, lvn_graph_out** out);
+
 int lvn_aggregate(const lvn_csr* g, const uint32_t* membership, int membership_location,
                   int canonical, const lvn_params* p, lvn_graph_out** out);
 /* compact_evaluate_move (louvain_compact.hpp:65-72), batched over all vertices on

@@ -24,6 +24,7 @@ from .louvain import (  # noqa: F401
     Probing,
     SwitchDegrees,
     build_community_csr,
+    build_csr,
     compact_aggregate,
     compact_evaluate_move,
     count_communities,

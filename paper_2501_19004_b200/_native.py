@@ -150,7 +150,7 @@ EXPORTS = (
     "lvn_count_communities", "lvn_renumber", "lvn_lookup_dendrogram", "lvn_community_csr",
     "lvn_aggregate", "lvn_evaluate_moves", "lvn_generate", "lvn_dgraph_upload", "lvn_dgraph_view",
     "lvn_dgraph_download", "lvn_dgraph_free", "lvn_device_alloc", "lvn_device_free", "lvn_memcpy",
-    "lvn_louvain_sharded", "lvn_partition_rows",
+    "lvn_louvain_sharded", "lvn_partition_rows", "lvn_build_csr",
 )
 
 _lib = None
@@ -197,6 +197,7 @@ def lib() -> C.CDLL:
     L.lvn_community_csr.argtypes = [vp, C.c_uint32, C.c_uint32, i, vp, vp]
     L.lvn_aggregate.argtypes = [C.POINTER(lvn_csr), vp, i, i, C.POINTER(lvn_params),
                                 C.POINTER(C.POINTER(lvn_graph_out))]
+    L.lvn_build_csr.argtypes = [C.c_uint32, C.c_uint64, vp, vp, vp, i, C.POINTER(C.POINTER(lvn_graph_out))]
     L.lvn_evaluate_moves.argtypes = [C.POINTER(lvn_csr), vp, vp, vp, C.c_double, C.POINTER(lvn_params), i,
                                      vp, vp]
     L.lvn_generate.argtypes = [C.POINTER(lvn_gen_params), C.POINTER(vp)]

@@ -1045,6 +1045,49 @@ void lvn_result_free(lvn_result* r) {
   delete r;
 }
 
+int lvn_build_csr(uint32_t num_vertices, uint64_t num_triples, const uint32_t* sources, const uint32_t* targets,
+                  const double* weights, int symmetrize, lvn_graph_out** out) {
+  if (!out) {
+    t_err = "null output";
+    return kInvalid;
+  }
+  *out = nullptr;
+  lvn_graph_out* res = nullptr;
+  const int rc = guard([&](Context& c) {
+    if (num_triples && (!sources || !targets || !weights)) fail(kInvalid, "null triple arrays");
+    cudaStream_t s = c.stream;
+    DBuf<u32> src(num_triples ? num_triples : 1), dst(num_triples ? num_triples : 1);
+    DBuf<double> w(num_triples ? num_triples : 1);
+    if (num_triples) {
+      LVN_CUDA(cudaMemcpyAsync(src.p, sources, num_triples * 4, cudaMemcpyHostToDevice, s));
+      LVN_CUDA(cudaMemcpyAsync(dst.p, targets, num_triples * 4, cudaMemcpyHostToDevice, s));
+      LVN_CUDA(cudaMemcpyAsync(w.p, weights, num_triples * 8, cudaMemcpyHostToDevice, s));
+    }
+    OwnedCsr o;
+    build_csr_device(num_vertices, num_triples, src.p, dst.p, w.p, symmetrize, o, s);
+    res = new lvn_graph_out;
+    res->num_vertices = o.n;
+    res->num_arcs = o.arcs;
+    res->total_weight = o.total_weight;
+    res->offsets = static_cast<u64*>(std::malloc((u64(o.n) + 1) * sizeof(u64)));
+    res->targets = static_cast<u32*>(std::malloc((o.arcs ? o.arcs : 1) * sizeof(u32)));
+    res->weights = static_cast<float*>(std::malloc((o.arcs ? o.arcs : 1) * sizeof(float)));
+    if (!res->offsets || !res->targets || !res->weights) fail(kOom, "host allocation failed");
+    LVN_CUDA(cudaMemcpyAsync(res->offsets, o.off.p, (u64(o.n) + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    if (o.arcs) {
+      LVN_CUDA(cudaMemcpyAsync(res->targets, o.tgt.p, o.arcs * sizeof(u32), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaMemcpyAsync(res->weights, o.w.p, o.arcs * sizeof(float), cudaMemcpyDeviceToHost, s));
+    }
+    LVN_CUDA(cudaStreamSynchronize(s));
+  });
+  if (rc) {
+    lvn_graph_free(res);
+    return rc;
+  }
+  *out = res;
+  return kOk;
+}
+
 void lvn_graph_free(lvn_graph_out* g) {
   if (!g) return;
   std::free(g->offsets);

@@ -195,6 +195,10 @@ struct GenSpec {
   u64 seed = 1;
 };
 void generate(const GenSpec& g, OwnedCsr& out, cudaStream_t s);
+// build.cu: build_csr (graph.cpp:15-87) on the device from device triples;
+// throws kInvalid on bad endpoints / weights
+void build_csr_device(u32 n, u64 T, const u32* src, const u32* dst, const double* w, int symmetrize,
+                      OwnedCsr& out, cudaStream_t s);
 // sorted arc keys (source<<32 | target, ~0 = dropped) -> deduplicated unit-weight CSR
 void keys_to_csr(DBuf<ull>& keys, u64 nkeys, u64 n, OwnedCsr& out, cudaStream_t s);
 

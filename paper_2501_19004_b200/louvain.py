@@ -504,6 +504,24 @@ def compact_aggregate(g, membership, params: LouvainParams | None = None,
 louvain_aggregate = compact_aggregate
 
 
+def build_csr(num_vertices: int, sources, targets, weights=None, symmetrize: bool = True) -> CsrGraph:
+    """build_csr (graph.cpp:15-87) on the device: rows sorted by target, parallel
+    arcs merged in fp64 (one f32 narrowing), reverse arcs added when
+    symmetrizing. Missing weights default to 1 (io.hpp). Raises ValueError for
+    endpoints out of range or weights that are not finite and non-negative."""
+    src = _u32(sources)
+    dst = _u32(targets)
+    if len(src) != len(dst):
+        raise ValueError("sources and targets differ in length")
+    w = np.ones(len(src)) if weights is None else np.ascontiguousarray(weights, dtype=np.float64)
+    if len(w) != len(src):
+        raise ValueError("weights differ in length")
+    out = C.POINTER(N.lvn_graph_out)()
+    _check(N.lib().lvn_build_csr(int(num_vertices), len(src), src.ctypes.data, dst.ctypes.data, w.ctypes.data,
+                                 int(bool(symmetrize)), C.byref(out)))
+    return _graph_out(out)
+
+
 def evaluate_moves(g, membership, vertex_w, community_w, m: float, options: CompactOptions | None = None,
                    force_kernel: int = -1):
     """Decision of every vertex on one fixed snapshot, nothing applied
