@@ -19,6 +19,7 @@
 // per-community HBM tables filled arc-parallel (ag_big_*).
 // Bytes: 12 B x A_in + 16 B x V_in + 8 B x A_out + 8 B x (count+1).
 #include <cooperative_groups.h>
+#include <chrono>
 #include <cstdio>
 #include <cstdlib>
 #include <string>
@@ -670,8 +671,7 @@ void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
     // approaches 28 B per arc); communities are processed in batches whose
     // regions fit a budget of a quarter of the free memory (at least the
     // largest single region).
-    size_t free_b = 0, total_b = 0;
-    LVN_CUDA(cudaMemGetInfo(&free_b, &total_b));
+    const size_t free_b = ctx().pool.available();
     u64 largest = 0;
     for (u64 i = 0; i < nbig; ++i) largest = std::max(largest, h_tab[i + 1] - h_tab[i]);
     u64 budget = std::min<u64>(h_tab[nbig], u64(free_b / 4));

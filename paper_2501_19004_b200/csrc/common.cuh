@@ -79,6 +79,10 @@ class Pool {
   void trim();         // return cached memory to the driver
   void release_all();  // free every outstanding allocation (context teardown)
   void report();       // pool occupancy on stderr (LVN_VERBOSE)
+  // device memory this pool can still hand out: device total minus the pool's
+  // live allocations, plus its cached big blocks (no cudaMemGetInfo, which can
+  // stall the host for tens of ms while kernels are in flight)
+  size_t available();
 
  private:
   void* raw(size_t bytes);
@@ -88,6 +92,7 @@ class Pool {
   std::unordered_map<void*, size_t> big_used_;
   std::multimap<size_t, void*> big_free_;
   size_t cache_budget_ = size_t(16) << 30;  // bytes of free big blocks kept across a miss
+  size_t total_ = 0;                        // device memory (at bind)
 };
 
 // Pinned host blocks for results handed to the caller (membership): device

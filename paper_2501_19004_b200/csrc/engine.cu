@@ -38,6 +38,15 @@ void Pool::bind(int device, cudaStream_t s) {
   size_t free_b = 0, total_b = 0;
   LVN_CUDA(cudaMemGetInfo(&free_b, &total_b));
   cache_budget_ = total_b / 4;
+  total_ = total_b;
+}
+
+size_t Pool::available() {
+  std::uint64_t used = 0;
+  (void)cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemCurrent, &used);
+  size_t cached = 0;
+  for (auto& kv : big_free_) cached += kv.first;
+  return used + (size_t(1) << 30) < total_ + cached ? total_ + cached - used - (size_t(1) << 30) : 0;
 }
 
 void* Pool::raw(size_t bytes) {
