@@ -90,6 +90,7 @@ struct MoveArgs {
   ull* counters = nullptr;     // [0] vertices processed, [1] arcs scanned, [2] moves, [3] random accesses
   u32* err = nullptr;
   u64 chunk = ~u64(0);         // max vertices of one bin decided per launch
+  u64 hub_chunk = ~u64(0);     // max vertices of the block / hub bins decided per launch
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
   int hubs_first = 0;          // bin order of a sweep: highest degree class first
   u32* csize = nullptr;        // community member counts (singleton-pair rule), or null

@@ -1242,26 +1242,33 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         auto k = lm_block<Tab, DRY>;
         constexpr size_t smem = block_smem<Tab>();
         static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
-        launch_chunks(k, a, b.of(bin), b.count(bin), kBlockThreads, 1, u64(sms) * occ, smem, s);
+        MoveArgs ab = a;
+        ab.chunk = std::min(a.chunk, a.hub_chunk);
+        launch_chunks(k, ab, b.of(bin), b.count(bin), kBlockThreads, 1, u64(sms) * occ, smem, s);
         break;
       }
       case kBinGlobal: {
+        // hubs in groups of hub_chunk: a later group sees the moves of the earlier ones
         if (!a.hub_tables) fail(kInternal, "hub plan not provisioned");
-        const u64 cnt = b.count(bin);
-        const u32* hubs = b.of(bin);
-        DBuf<u32> chunks(cnt);
-        DBuf<u64> coff(cnt + 1);
-        hub_chunk_counts_k<<<unsigned(std::min<u64>((cnt + 255) / 256, u64(sms) * 4)), 256, 0, s>>>(
-            hubs, cnt, a.g.off, chunks.p);
-        LVN_LAUNCH();
-        exclusive_scan_u32_to_u64(chunks.p, coff.p, cnt, s);
+        const u64 all = b.count(bin);
+        const u64 step = std::max<u64>(1, std::min(a.hub_chunk, all));
+        DBuf<u32> chunks(std::min(step, all));
+        DBuf<u64> coff(std::min(step, all) + 1);
         auto kc = lm_hub_chunks<Tab>;
         constexpr size_t smem = block_smem<Tab>();
         static const int occ = (set_smem(kc, smem), occupancy(kc, kBlockThreads, smem));
-        kc<<<unsigned(sms * occ), kBlockThreads, smem, s>>>(a, hubs, cnt, coff.p);
-        LVN_LAUNCH();
-        lm_hub_decide<Tab, DRY><<<unsigned(std::min<u64>(cnt, u64(sms) * 4)), kBlockThreads, 0, s>>>(a, hubs, cnt);
-        LVN_LAUNCH();
+        for (u64 h0 = 0; h0 < all; h0 += step) {
+          const u64 cnt = std::min(step, all - h0);
+          const u32* hubs = b.of(bin) + h0;
+          hub_chunk_counts_k<<<unsigned(std::min<u64>((cnt + 255) / 256, u64(sms) * 4)), 256, 0, s>>>(
+              hubs, cnt, a.g.off, chunks.p);
+          LVN_LAUNCH();
+          exclusive_scan_u32_to_u64(chunks.p, coff.p, cnt, s);
+          kc<<<unsigned(sms * occ), kBlockThreads, smem, s>>>(a, hubs, cnt, coff.p);
+          LVN_LAUNCH();
+          lm_hub_decide<Tab, DRY><<<unsigned(std::min<u64>(cnt, u64(sms) * 4)), kBlockThreads, 0, s>>>(a, hubs, cnt);
+          LVN_LAUNCH();
+        }
         break;
       }
       default: break;
