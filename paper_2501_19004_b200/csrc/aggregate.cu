@@ -26,6 +26,7 @@
 #include <cooperative_groups/reduce.h>
 
 #include "kernels.cuh"
+#include "psort.cuh"
 #include "sortnet.cuh"
 #include "tables.cuh"
 
@@ -95,6 +96,82 @@ __global__ void __launch_bounds__(256) ag_sort(AggArgs x, const u32* __restrict_
         if (lane == 0) x.fill[c] = total;
       }
     }
+  }
+}
+
+// Packed-key variant (psort.cuh): keys (C[t] << LB) | position, the f32
+// weights staged per group in smem and fetched by position after the sort,
+// runs summed in fp64 (sequence starts from a ballot). Needs count < 2^(32-LB).
+template <int G, int K>
+__global__ void __launch_bounds__(256) ag_psort(AggArgs x, const u32* __restrict__ list, u64 count) {
+  constexpr int GPB = 256 / G;
+  constexpr int N = G * K;
+  constexpr int LB = ilog2<N>();
+  constexpr u32 FULL = 0xffffffffu;
+  __shared__ float wbuf[256 * K];
+  const u32 lane = threadIdx.x & (G - 1);
+  const u32 gi = threadIdx.x / G;
+  const u32 gshift = (threadIdx.x & 31u) & ~u32(G - 1);
+  float* gw = wbuf + gi * N;
+  const ull dirs = psort_dirs<G, K>(lane);
+  for (u64 i0 = u64(blockIdx.x) * GPB; i0 < count; i0 += u64(gridDim.x) * GPB) {
+    const u64 i = i0 + gi;
+    const bool have = i < count;
+    const u32 c = have ? list[i] : 0;
+    u32 key[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) key[r] = kNoKey;
+    u64 mlo = 0, mhi = 0;
+    if (have) mlo = x.coff[c], mhi = x.coff[c + 1];
+    __syncwarp();
+    u64 base = 0;
+    for (u64 k = mlo; k < mhi; ++k) {
+      const u32 v = x.members[k];
+      const u64 lo = x.g.off[v], d = x.g.off[v + 1] - lo;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const u64 e = u64(r) * G + lane;
+        if (e >= base && e < base + d) {
+          const u64 a = lo + (e - base);
+          key[r] = (x.C[__ldcs(x.g.tgt + a)] << LB) | u32(e);
+          gw[e] = __ldcs(x.g.w + a);
+        }
+      }
+      base += d;
+    }
+    __syncwarp();
+    psort<G, K>(key, dirs);
+    u32 ck[K];
+    double val[K];
+#pragma unroll
+    for (int r = 0; r < K; ++r) {
+      ck[r] = key[r] == kNoKey ? kEmpty : key[r] >> LB;
+      val[r] = key[r] == kNoKey ? 0.0 : double(gw[key[r] & u32(N - 1)]);
+    }
+    bool tail[K];
+    prun_sums<G, K, double>(ck, val, tail, lane, gshift);
+    u32 mine = 0;
+#pragma unroll
+    for (int r = 0; r < K; ++r) mine += (tail[r] && ck[r] != kEmpty) ? 1u : 0u;
+    u32 total;
+    u32 pos = group_exclusive<G>(mine, lane, total);
+    if (have) {
+      const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
+      if (total > hcap) {
+        if (lane == 0) atomicOr(x.err, u32(kErrTable));
+      } else {
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          if (tail[r] && ck[r] != kEmpty) {
+            x.htgt[hbase + pos] = ck[r];
+            x.hw[hbase + pos] = float(val[r]);  // fp64 sum narrowed once
+            ++pos;
+          }
+        }
+        if (lane == 0) x.fill[c] = total;
+      }
+    }
+    (void)FULL;
   }
 }
 
@@ -624,13 +701,16 @@ void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
     kernel<<<unsigned(blocks), 256, 0, s>>>(a, b.of(bin), b.count(bin));
     LVN_LAUNCH();
   };
-  sort_bin(kBinThread, ag_sort<8, 1>, 8);
-  sort_bin(kBinSort8, ag_sort<8, 1>, 8);
-  sort_bin(kBinSort16, ag_sort<16, 1>, 16);
-  sort_bin(kBinSort32, ag_sort<32, 1>, 32);
-  sort_bin(kBinSort64, ag_sort<32, 2>, 32);
-  sort_bin(kBinSort128, ag_sort<32, 4>, 32);
-  sort_bin(kBinSort256, ag_sort<32, 8>, 32);
+  // packed keys when the community ids leave room for the row position
+  const bool pk = !std::getenv("LVN_AGG_UNPACKED");
+  auto fits = [&](int lb) { return pk && u64(a.count) < (u64(1) << (32 - lb)); };
+  if (fits(3)) sort_bin(kBinThread, ag_psort<8, 1>, 8); else sort_bin(kBinThread, ag_sort<8, 1>, 8);
+  if (fits(3)) sort_bin(kBinSort8, ag_psort<8, 1>, 8); else sort_bin(kBinSort8, ag_sort<8, 1>, 8);
+  if (fits(4)) sort_bin(kBinSort16, ag_psort<16, 1>, 16); else sort_bin(kBinSort16, ag_sort<16, 1>, 16);
+  if (fits(5)) sort_bin(kBinSort32, ag_psort<32, 1>, 32); else sort_bin(kBinSort32, ag_sort<32, 1>, 32);
+  if (fits(6)) sort_bin(kBinSort64, ag_psort<32, 2>, 32); else sort_bin(kBinSort64, ag_sort<32, 2>, 32);
+  if (fits(7)) sort_bin(kBinSort128, ag_psort<32, 4>, 32); else sort_bin(kBinSort128, ag_sort<32, 4>, 32);
+  if (fits(8)) sort_bin(kBinSort256, ag_psort<32, 8>, 32); else sort_bin(kBinSort256, ag_sort<32, 8>, 32);
   if (b.count(kBinWarp)) {
     constexpr int T = 256;
     auto k = ag_group<32, kWarpCapLog, T>;
