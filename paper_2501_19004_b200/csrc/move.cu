@@ -571,10 +571,16 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
       w[r] = ok ? V(__ldcs(x.g.w + a)) : V(0);
     }
   };
-  auto gather = [&](u32 v, const u32 (&t)[K], u32 (&key)[K]) {
+  // padding carries no key; a self-loop keeps its place in the row as a
+  // zero-weight element of u's own community (K_{u->c} excludes self-loops,
+  // louvain_compact.cpp:46), so rows stored sorted by target stay sorted
+  auto gather = [&](u32 v, u32 vfrom, const u32 (&t)[K], u32 (&key)[K], V (&w)[K]) {
 #pragma unroll
-    for (int r = 0; r < K; ++r)  // self-loops and padding carry no key
-      key[r] = (t[r] != v && t[r] != kEmpty) ? (ld_keep(x.C + t[r], keep) << LB) | u32(r * G + lane) : kNoKey;
+    for (int r = 0; r < K; ++r) {
+      const u32 c = t[r] == v ? vfrom : (t[r] != kEmpty ? ld_keep(x.C + t[r], keep) : 0u);
+      key[r] = t[r] != kEmpty ? (c << LB) | u32(r * G + lane) : kNoKey;
+      if (t[r] == v) w[r] = V(0);
+    }
   };
 
   // prologue: vertex i fully loaded, vertex i+1's header
@@ -594,7 +600,7 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
   }
   load_row(u, lo, hi, t, val);
   if (have) sf = x.sigma[from];
-  gather(u, t, key);
+  gather(u, from, t, key, val);
   bool have1 = i0 + stride + gi < count;
   u32 u1 = 0, from1 = kEmpty;
   u64 lo1 = 0, hi1 = 0;
@@ -625,7 +631,16 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
     }
 #pragma unroll
     for (int r = 0; r < K; ++r) tl.rand += key[r] != kNoKey ? 1 : 0;
-    psort<G, K>(key, dirs);
+    // rows whose communities already ascend (every row in the first sweep of
+    // a pass: rows are stored sorted by target and C is the identity) skip
+    // the network
+    {
+      const u32 nxt = __shfl_down_sync(FULL, key[0], 1, G);
+      bool up = lane == G - 1 || key[K - 1] <= nxt;
+#pragma unroll
+      for (int r = 0; r + 1 < K; ++r) up = up && key[r] <= key[r + 1];
+      if (!__all_sync(FULL, up)) psort<G, K>(key, dirs);
+    }
     u32 ck[K];
     V run[K];
 #pragma unroll
@@ -641,7 +656,7 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
     prun_sums<G, K, V>(ck, run, tail, lane, gshift);
 
     // (i+1) communities of its arcs, Sigma of its community
-    gather(u1, t1, key1);
+    gather(u1, from1, t1, key1, val1);
     const double sf1 = have1 ? x.sigma[from1] : 0.0;
 
     // (i) weight to the own community (one run tail in the group holds it),
