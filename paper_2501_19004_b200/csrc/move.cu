@@ -623,23 +623,27 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
     const u32 u2 = have2 ? list[in2] : 0u;
 
     // (i) group the arcs by community, fetch the weights in sorted order
-    if (K > 1) {
-      __syncwarp();
-#pragma unroll
-      for (int r = 0; r < K; ++r) gbuf[r * G + lane] = val[r];
-      __syncwarp();
-    }
 #pragma unroll
     for (int r = 0; r < K; ++r) tl.rand += key[r] != kNoKey ? 1 : 0;
-    // rows whose communities already ascend (every row in the first sweep of
-    // a pass: rows are stored sorted by target and C is the identity) skip
-    // the network
-    {
-      const u32 nxt = __shfl_down_sync(FULL, key[0], 1, G);
-      bool up = lane == G - 1 || key[K - 1] <= nxt;
+    // rows whose communities already ascend in row order (every row in the
+    // first sweep of a pass: rows are stored sorted by target and C is the
+    // identity) skip the network and take the row-order run sums
+    bool rows = true;
 #pragma unroll
-      for (int r = 0; r + 1 < K; ++r) up = up && key[r] <= key[r + 1];
-      if (!__all_sync(FULL, up)) psort<G, K>(key, dirs);
+    for (int r = 0; r < K; ++r) {
+      const u32 nxt = __shfl_down_sync(FULL, key[r], 1, G);
+      const u32 wrap = r + 1 < K ? __shfl_sync(FULL, key[r + 1], 0, G) : kNoKey;
+      rows = rows && key[r] <= (lane + 1 < u32(G) ? nxt : wrap);
+    }
+    rows = __all_sync(FULL, rows);
+    if (!rows) {
+      if (K > 1) {
+        __syncwarp();
+#pragma unroll
+        for (int r = 0; r < K; ++r) gbuf[r * G + lane] = val[r];
+        __syncwarp();
+      }
+      psort<G, K>(key, dirs);
     }
     u32 ck[K];
     V run[K];
@@ -647,13 +651,15 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
     for (int r = 0; r < K; ++r) {
       const u32 pos = key[r] & u32(N - 1);
       V w;
-      if (K == 1) w = __shfl_sync(FULL, val[0], pos, G);
+      if (rows) w = val[r];
+      else if (K == 1) w = __shfl_sync(FULL, val[0], pos, G);
       else w = gbuf[pos];
       ck[r] = key[r] == kNoKey ? kEmpty : key[r] >> LB;
       run[r] = key[r] == kNoKey ? V(0) : w;
     }
     bool tail[K];
-    prun_sums<G, K, V>(ck, run, tail, lane, gshift);
+    if (rows) prun_sums_rows<G, K, V>(ck, run, tail, lane, gshift);
+    else prun_sums<G, K, V>(ck, run, tail, lane, gshift);
 
     // (i+1) communities of its arcs, Sigma of its community
     gather(u1, from1, t1, key1, val1);

@@ -120,6 +120,43 @@ __device__ __forceinline__ void prun_sums(const u32 (&ck)[K], V (&val)[K], bool 
   for (int r = 0; r < K; ++r) tail[r] = r + 1 < K ? head[r + 1] : last_lane_tail;
 }
 
+// The same run sums for elements already ordered in *row* order, element
+// e = r*G + lane (the load layout), so an ascending row needs no network:
+// each register row is scanned across the lanes, and the run open at the end
+// of register r carries into register r+1.
+template <int G, int K, class V>
+__device__ __forceinline__ void prun_sums_rows(const u32 (&ck)[K], V (&val)[K], bool (&tail)[K], u32 lane,
+                                               u32 gshift) {
+  constexpr u32 FULL = 0xffffffffu;
+  constexpr u32 GMASK = G == 32 ? FULL : ((1u << G) - 1u);
+  bool head[K];
+  u32 hb[K];
+  V carry = V(0);  // total of the run open at the end of the previous register
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const u32 up = __shfl_up_sync(FULL, ck[r], 1, G);
+    const u32 prev_last = r > 0 ? __shfl_sync(FULL, ck[r - 1], G - 1, G) : kEmpty;
+    head[r] = lane == 0 ? (r == 0 || ck[r] != prev_last) : ck[r] != up;
+    hb[r] = (__ballot_sync(FULL, head[r]) >> gshift) & GMASK;
+    const u32 below = hb[r] & ((2u << lane) - 1u);  // heads at lanes <= this one
+    const u32 start = below ? 31u - __clz(below) : 0u;
+    V agg = val[r];
+#pragma unroll
+    for (int d = 1; d < G; d <<= 1) {
+      const V p = __shfl_up_sync(FULL, agg, d, G);
+      if (lane >= start + d) agg += p;
+    }
+    if (!below) agg += carry;  // the run entering this register continues here
+    val[r] = agg;
+    carry = __shfl_sync(FULL, agg, G - 1, G);
+  }
+#pragma unroll
+  for (int r = 0; r < K; ++r) {
+    const bool next_head = lane + 1 < u32(G) ? ((hb[r] >> (lane + 1)) & 1u) : (r + 1 < K ? (hb[r + 1] & 1u) : 1u);
+    tail[r] = next_head != 0;
+  }
+}
+
 // order-preserving map of a double to u64 (greater double -> greater key)
 __device__ __forceinline__ ull ordered_bits(double g) {
   const ull b = ull(__double_as_longlong(g + 0.0));  // -0 -> +0
