@@ -67,8 +67,13 @@ void* Pool::raw(size_t bytes) {
 
 constexpr size_t kBigBytes = size_t(64) << 20;
 
+bool pool_nocache() {
+  static const bool v = std::getenv("LVN_POOL_NOCACHE") != nullptr;
+  return v;
+}
+
 void* Pool::get(size_t bytes) {
-  if (bytes >= kBigBytes) {
+  if (bytes >= kBigBytes && !pool_nocache()) {
     const size_t unit = (size_t(1) << (63 - __builtin_clzll(bytes))) / 16;
     const size_t r = (bytes + unit - 1) / unit * unit;
     auto it = big_free_.lower_bound(r);
