@@ -76,12 +76,17 @@ __device__ __forceinline__ bool key_ok(const MoveArgs& x, u32 key) {
   return false;
 }
 
-// Eq. 2 for ranking: exact (reference operation order) or with reciprocals
-template <bool EXACT>
+// Eq. 2 for ranking: exact (reference operation order) or with reciprocals.
+// With 32-bit scan values the reference stores each gain back into its f32
+// table slot before taking the maximum (decide_serial, louvain_compact.cpp:
+// 59-64), so gains that agree to f32 precision tie and the lowest community id
+// wins; the ranking rounds the same way (V = float).
+template <bool EXACT, class V = double>
 __device__ __forceinline__ double score(const MoveArgs& x, double k_to_c, double own, double ku,
                                         double sigma_c, double sigma_d) {
-  if (EXACT) return delta_q(k_to_c, own, ku, sigma_c, sigma_d, x.m);
-  return (k_to_c - own) * x.inv_m - ku * (ku + sigma_c - sigma_d) * x.inv_2m2;
+  const double g = EXACT ? delta_q(k_to_c, own, ku, sigma_c, sigma_d, x.m)
+                         : (k_to_c - own) * x.inv_m - ku * (ku + sigma_c - sigma_d) * x.inv_2m2;
+  return sizeof(V) == 4 ? double(float(g)) : g;
 }
 
 // Sigma-free upper bound of Eq. 2: with Sigma_c >= 0 the gain of c is at most
@@ -203,7 +208,7 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
       for (int j = k; j < kThreadMaxD; ++j)
         if (c[j] == ck) sum += wv[j];
       if (first && (DRY || may_gain(x, double(sum), double(own), ku, sf))) {
-        const double g = score<DRY>(x, double(sum), double(own), ku, x.sigma[ck], sf);
+        const double g = score<DRY, V>(x, double(sum), double(own), ku, x.sigma[ck], sf);
         ++tl.rand;
         if (better(g, ck, bg, bc)) bg = g, bc = ck, bk = double(sum);
       }
@@ -294,7 +299,7 @@ __device__ __forceinline__ void rank_live(const MoveArgs& x, const Tab& tab, con
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       if (key[k] == kEmpty) continue;
-      const double g = score<DRY>(x, val[k], own, ku, sc[k], sf);
+      const double g = score<DRY, typename Tab::V>(x, val[k], own, ku, sc[k], sf);
       if (better(g, key[k], bg, bc)) bg = g, bc = key[k], bk = val[k];
     }
   }
@@ -491,7 +496,7 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
 #pragma unroll
     for (int r = 0; r < K; ++r) {
       if (!cand[r]) continue;
-      const double g = score<DRY>(x, double(run[r]), double(own), ku, sc[r], sf);
+      const double g = score<DRY, V>(x, double(run[r]), double(own), ku, sc[r], sf);
       if (better(g, key[r], bg, bc)) bg = g, bc = key[r], bk = double(run[r]);
     }
 #pragma unroll
@@ -703,7 +708,7 @@ __global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(M
 #pragma unroll
     for (int r = 0; r < K; ++r) {
       if (!cand[r]) continue;
-      const double g = score<DRY>(x, double(run[r]), double(own), ku, sc[r], sf);
+      const double g = score<DRY, V>(x, double(run[r]), double(own), ku, sc[r], sf);
       if (better(g, ck[r], bg, bc)) bg = g, bc = ck[r], bk = double(run[r]);
     }
     const u32 best = group_best<G>(bg, bc);
@@ -848,7 +853,7 @@ __global__ void __launch_bounds__(256) lm_match(MoveArgs x, const u32* __restric
       const bool cand = ckey != kEmpty && key_ok(x, ckey);
       const double sc = cand ? x.sigma[ckey] : 0.0;
       if (cand) {
-        bg = score<DRY>(x, double(cval), double(own), ku, sc, sf);
+        bg = score<DRY, V>(x, double(cval), double(own), ku, sc, sf);
         bc = ckey, bk = double(cval);
       }
     } else {

@@ -234,7 +234,7 @@ def decisions_equal(lvn, port, g, memb, force=-1, value_bits=64):
     opts = lvn.CompactOptions(value_bits=value_bits)
     to, gain = lvn.evaluate_moves(G_(g, lvn), memb, kw, cw, g.total_weight, opts, force)
     for u in range(g.n):
-        want = port.evaluate_move(g, memb, kw, cw, g.total_weight, u, 64)
+        want = port.evaluate_move(g, memb, kw, cw, g.total_weight, u, value_bits)
         assert (int(to[u]), float(gain[u])) == want, (u, g.offsets[u + 1] - g.offsets[u])
 
 
@@ -246,7 +246,8 @@ def test_decisions_golden(lvn, t):
     kw = G.field(p, "vertex_weights")
     cw = np.zeros(g.n)
     np.add.at(cw, memb, kw)
-    to, gain = lvn.evaluate_moves(G_(g, lvn), memb, kw, cw, g.total_weight)
+    # the fixtures are compact_evaluate_move<double> (value_bits 64)
+    to, gain = lvn.evaluate_moves(G_(g, lvn), memb, kw, cw, g.total_weight, lvn.CompactOptions(value_bits=64))
     assert (to == G.field(p, "move_to")).all() and (gain == G.field(p, "move_gain")).all()
 
 
