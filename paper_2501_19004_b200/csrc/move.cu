@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
 // in registers for the neighbour marks. Gathers for i+1 may miss the move of
 // i (asynchrony the validated join tolerates); DRY writes no state.
 template <int G, int K, class V, bool DRY>
-__global__ void __launch_bounds__(256, K <= 2 ? 4 : (K == 4 ? 3 : 2)) lm_psort(MoveArgs x, const u32* __restrict__ list, u64 count) {
+__global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(MoveArgs x, const u32* __restrict__ list, u64 count) {
   constexpr int GPB = 256 / G;
   constexpr int N = G * K;
   constexpr int LB = ilog2<N>();
