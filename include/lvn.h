@@ -118,7 +118,10 @@ typedef struct lvn_params {
    * rounds per iteration, exchanging Sigma / C / marks after each (more
    * rounds: fresher cross-rank state, more collectives); 0 = 2 x ranks */
   int shard_rounds;             /* 0 */
-  int reserved[1];
+  /* 1: keep the dendrogram, one local membership per pass, in lvn_result
+   * (levels[k][v] = community of vertex v of pass k's graph; composing the
+   * levels gives the final partition, lookup_dendrogram of louvain_mc.cpp:145) */
+  int keep_levels;              /* 0 */
 } lvn_params;
 
 /* Per-kernel-family device accounting (CUDA events on the engine stream). */
@@ -158,6 +161,8 @@ typedef struct lvn_result {
   int num_shards;         /* ranks of lvn_louvain_sharded (1 otherwise) */
   int sharded_passes;     /* passes run sharded (the rest ran whole on every rank) */
   double exchange_seconds; /* host time inside the collectives */
+  int num_levels;          /* dendrogram levels kept (lvn_params.keep_levels), else 0 */
+  uint32_t** levels;       /* host arrays, level k has vertices_per_pass[k] entries */
 } lvn_result;
 
 /* ---- lifecycle -------------------------------------------------------- */

@@ -68,7 +68,7 @@ class lvn_params(C.Structure):
         ("singleton_rule", C.c_int),
         ("shard_min_arcs_log2", C.c_int),
         ("shard_rounds", C.c_int),
-        ("reserved", C.c_int * 1),
+        ("keep_levels", C.c_int),
     ]
 
 
@@ -107,6 +107,8 @@ class lvn_result(C.Structure):
         ("num_shards", C.c_int),
         ("sharded_passes", C.c_int),
         ("exchange_seconds", C.c_double),
+        ("num_levels", C.c_int),
+        ("levels", C.POINTER(C.POINTER(C.c_uint32))),
     ]
 
 

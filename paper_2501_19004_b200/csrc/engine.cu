@@ -717,6 +717,19 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   Comm& cm = comm ? *comm : solo;
   Bins own_bins;
   DBuf<u32> mrec, mall, mcount;  // sharded: own move records (u, to), everyone's, per-rank counts
+  struct Levels : std::vector<u32*> {  // dendrogram (p.keep_levels): local membership of every pass
+    ~Levels() {
+      for (u32* q : *this) std::free(q);
+    }
+  } levels;
+  auto keep_level = [&](u32 nv) {
+    if (!p.keep_levels) return;
+    u32* h = static_cast<u32*>(std::malloc(size_t(nv ? nv : 1) * sizeof(u32)));
+    if (!h) fail(kOom, "host allocation failed");
+    if (nv) LVN_CUDA(cudaMemcpyAsync(h, C.p, size_t(nv) * sizeof(u32), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    levels.push_back(h);
+  };
 
   for (int pass = 0; pass < p.max_passes; ++pass) {
     const auto t_pass = Clock::now();
@@ -856,6 +869,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     app.push_back(cur.arcs);
 
     if (iterations <= 1) {  // no effective movement (louvain_compact.cpp:370-374)
+      keep_level(nv);
       sp = tm.begin(LVN_STAT_RENUMBER, s);
       lookup(global.p, N, C.p, nv, err.p, s);
       tm.end(sp, s, 12.0 * N);
@@ -866,6 +880,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     const u32 count = renumber_device(C.p, nv, nv, used, rank, s, false);
     tm.end(sp, s, 12.0 * nv);
     if (double(count) / nv > p.aggregation_tolerance) {  // low shrink (louvain_compact.cpp:375-380)
+      keep_level(nv);
       sp = tm.begin(LVN_STAT_RENUMBER, s);
       lookup(global.p, N, C.p, nv, err.p, s);
       tm.end(sp, s, 12.0 * N);
@@ -874,6 +889,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     }
     sp = tm.begin(LVN_STAT_RENUMBER, s);
     remap(C.p, nv, rank.p, s);                  // renumber_communities (louvain_compact.cpp:382)
+    keep_level(nv);
     lookup(global.p, N, C.p, nv, err.p, s);     // lookup_dendrogram (louvain_compact.cpp:383)
     tm.end(sp, s, 12.0 * nv + 12.0 * N);
     const auto t1 = Clock::now();
@@ -936,6 +952,12 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   tm.collect(r->stats);
   r->wall_seconds = since(t_start);
   if (verbose()) c.pool.report();
+  r->num_levels = int(levels.size());
+  if (!levels.empty()) {
+    r->levels = static_cast<u32**>(std::calloc(levels.size(), sizeof(u32*)));
+    for (size_t i = 0; i < levels.size(); ++i) r->levels[i] = levels[i];
+    levels.clear();
+  }
   r->num_shards = cm.size();
   r->sharded_passes = sharded_passes;
   r->exchange_seconds = cm.seconds;
@@ -1026,6 +1048,7 @@ void lvn_params_default(lvn_params* p) {
   p->singleton_rule = 0;
   p->shard_min_arcs_log2 = 22;
   p->shard_rounds = 0;
+  p->keep_levels = 0;
 }
 
 int lvn_init(int num_gpus, const int* devices) {
@@ -1062,6 +1085,8 @@ void lvn_result_free(lvn_result* r) {
   std::free(r->pass_seconds);
   std::free(r->vertices_per_pass);
   std::free(r->arcs_per_pass);
+  for (int i = 0; i < r->num_levels; ++i) std::free(r->levels[i]);
+  std::free(r->levels);
   delete r;
 }
 

@@ -179,6 +179,7 @@ class LouvainResult:  # louvain.hpp:28-39 (+ device breakdown)
     num_shards: int = 1
     sharded_passes: int = 0
     exchange_seconds: float = 0.0
+    levels: list = field(default_factory=list)  # dendrogram (keep_levels=True)
 
 
 @dataclass
@@ -293,7 +294,8 @@ def generate(kind: str, seed: int = 1, **kw) -> DeviceGraph:
 # --------------------------------------------------------------------------
 
 
-def _params(params: LouvainParams | None, options: CompactOptions | None, on_device=False) -> N.lvn_params:
+def _params(params: LouvainParams | None, options: CompactOptions | None, on_device=False,
+            keep_levels=False) -> N.lvn_params:
     params = params or LouvainParams()
     options = options or CompactOptions()
     p = N.lvn_params()
@@ -322,6 +324,7 @@ def _params(params: LouvainParams | None, options: CompactOptions | None, on_dev
     p.singleton_rule = int(bool(options.singleton_rule))
     p.shard_min_arcs_log2 = options.shard_min_arcs_log2
     p.shard_rounds = options.shard_rounds
+    p.keep_levels = int(bool(keep_levels))
     return p
 
 
@@ -346,9 +349,12 @@ def _graph_out(ptr) -> CsrGraph:
 
 
 def louvain_compact(g, params: LouvainParams | None = None, options: CompactOptions | None = None,
-                    membership_on_device: bool = False) -> LouvainResult:
-    """The ν-Louvain engine on the B200 (louvain_compact.hpp:57-58)."""
-    p = _params(params, options, membership_on_device)
+                    membership_on_device: bool = False, keep_levels: bool = False) -> LouvainResult:
+    """The ν-Louvain engine on the B200 (louvain_compact.hpp:57-58). With
+    keep_levels the result carries the dendrogram: `levels[k]` maps the
+    vertices of pass k's graph to their communities (lookup_dendrogram,
+    louvain_mc.cpp:145-160, composes them into `membership`)."""
+    p = _params(params, options, membership_on_device, keep_levels)
     csr = g._csr()
     out = C.POINTER(N.lvn_result)()
     _check(N.lib().lvn_louvain(C.byref(csr), C.byref(p), C.byref(out)))
@@ -424,6 +430,8 @@ def _result(out) -> LouvainResult:
             sharded_passes=r.sharded_passes,
             exchange_seconds=r.exchange_seconds,
         )
+        res.levels = [np.ctypeslib.as_array(r.levels[i], (max(r.vertices_per_pass[i], 1),))[: r.vertices_per_pass[i]].copy()
+                      for i in range(r.num_levels)]
         res.membership_device_ptr = dev_ptr
         if dev_ptr is not None:  # valid while the result object lives
             res._handle = _ResultHandle(out)

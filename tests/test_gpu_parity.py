@@ -404,3 +404,22 @@ def test_generators_produce_valid_csr(lvn, kind, kw):
     rev = g.targets.astype(np.uint64) << np.uint64(32) | rows.astype(np.uint64)
     assert np.array_equal(np.sort(rev), key), "symmetric"
     assert g.total_weight == g.num_arcs() / 2
+
+
+# ---------------------------------------------------------------- dendrogram
+def test_dendrogram_levels(lvn, port):
+    # keep_levels: one local membership per pass; composing them in order
+    # (lookup_dendrogram, louvain_mc.cpp:145-160) gives the final partition
+    g = planted(20000, 40, 24, 0.2, 12)
+    r = lvn.louvain_compact(G_(g, lvn), keep_levels=True)
+    assert len(r.levels) == r.passes >= 2
+    assert [len(l) for l in r.levels] == r.vertices_per_pass
+    glob = np.arange(g.n)
+    for k, lvl in enumerate(r.levels):
+        glob = lvl[glob]
+        if k + 1 < len(r.levels):  # aggregated levels are renumbered to the next graph
+            assert lvl.max() + 1 == r.vertices_per_pass[k + 1]
+    a, b = glob, r.membership
+    pairs = set(zip(a.tolist(), b.tolist()))
+    assert len(pairs) == len(set(a.tolist())) == len(set(b.tolist())) == r.num_communities
+    assert lvn.louvain_compact(G_(g, lvn)).levels == []
