@@ -42,6 +42,59 @@ __global__ void mod_thread(DGraph g, const u32* __restrict__ list, u64 count,
   if ((threadIdx.x & 31) == 0 && internal != 0.0) atomicAdd(&sums[0], internal);
 }
 
+// Rows of the register-sort bins: a G-lane group per row, K arcs per lane
+// (arc r*G + lane, coalesced), two rows per group in flight so each lane has
+// 2K independent gathers of C[t] outstanding. The thread-per-row kernel above
+// reads 32 different rows per warp load (one L1TEX line per lane per arc).
+template <int G, int K>
+__global__ void __launch_bounds__(256) mod_group(DGraph g, const u32* __restrict__ list, u64 count,
+                                                 const u32* __restrict__ C, double* __restrict__ tot,
+                                                 double* sums) {
+  constexpr int GPB = 256 / G;
+  const u32 lane = threadIdx.x & (G - 1);
+  const u64 gi = (blockIdx.x * u64(blockDim.x) + threadIdx.x) / G;
+  const u64 groups = u64(gridDim.x) * GPB;
+  double internal = 0.0;
+  for (u64 i = gi; i < count; i += 2 * groups) {
+    u32 v[2], c[2], t[2][K];
+    u64 lo[2], hi[2];
+    float w[2][K];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const u64 ij = i + u64(j) * groups;
+      v[j] = ij < count ? list[ij] : 0u;
+      lo[j] = ij < count ? g.off[v[j]] : 0;
+      hi[j] = ij < count ? g.off[v[j] + 1] : 0;
+      c[j] = ij < count ? C[v[j]] : kEmpty;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const u64 a = lo[j] + u64(r) * G + lane;
+        t[j][r] = a < hi[j] ? __ldcs(g.tgt + a) : kEmpty;
+        w[j][r] = a < hi[j] ? __ldcs(g.w + a) : 0.f;
+      }
+    }
+    u32 ct[2][K];
+#pragma unroll
+    for (int j = 0; j < 2; ++j)
+#pragma unroll
+      for (int r = 0; r < K; ++r) ct[j][r] = t[j][r] != kEmpty ? C[t[j][r]] : kEmpty;
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double k = 0.0;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        k += double(w[j][r]);
+        if (ct[j][r] == c[j]) internal += double(w[j][r]);
+      }
+#pragma unroll
+      for (int o = G / 2; o > 0; o >>= 1) k += __shfl_xor_sync(0xffffffffu, k, o, G);
+      if (lane == 0 && c[j] != kEmpty && k != 0.0) atomicAdd(&tot[c[j]], k);
+    }
+  }
+  internal = warp_sum(internal);
+  if ((threadIdx.x & 31) == 0 && internal != 0.0) atomicAdd(&sums[0], internal);
+}
+
 __global__ void mod_warp(DGraph g, const u32* __restrict__ list, u64 count,
                          const u32* __restrict__ C, double* __restrict__ tot, double* sums) {
   const int lane = threadIdx.x & 31;
@@ -110,16 +163,34 @@ void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot,
   LVN_CUDA(cudaMemsetAsync(tot, 0, width * sizeof(double), s));
   LVN_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), s));
   const int sms = sm_count();
-  const u64 small = b.start[kBinSort64] - b.start[kBinIso];  // rows of <= 32 arcs
-  if (small) {
-    const u64 blocks = std::min<u64>((small + 255) / 256, u64(sms) * 8);
-    mod_thread<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinIso), small, C, tot, sums);
+  // rows in the register-sort bins: a lane group per row (the bin fixes the
+  // row length bound); isolated vertices contribute nothing
+  auto grp = [&](int bin, auto kernel, int G) {
+    if (!b.count(bin)) return;
+    const u64 per_block = 256 / G;
+    const u64 blocks = std::min<u64>((b.count(bin) + per_block - 1) / per_block, u64(sms) * 8);
+    kernel<<<unsigned(blocks), 256, 0, s>>>(g, b.of(bin), b.count(bin), C, tot, sums);
     LVN_LAUNCH();
+  };
+  if (b.edges.thread_max <= 8) {
+    grp(kBinThread, mod_group<8, 1>, 8);
+  } else {
+    const u64 blocks = std::min<u64>((b.count(kBinThread) + 255) / 256, u64(sms) * 8);
+    if (b.count(kBinThread)) {
+      mod_thread<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinThread), b.count(kBinThread), C, tot, sums);
+      LVN_LAUNCH();
+    }
   }
-  const u64 mid = b.start[kBinBlock] - b.start[kBinSort64];
+  grp(kBinSort8, mod_group<8, 1>, 8);
+  grp(kBinSort16, mod_group<16, 1>, 16);
+  grp(kBinSort32, mod_group<32, 1>, 32);
+  grp(kBinSort64, mod_group<32, 2>, 32);
+  grp(kBinSort128, mod_group<32, 4>, 32);
+  grp(kBinSort256, mod_group<32, 8>, 32);
+  const u64 mid = b.count(kBinWarp);
   if (mid) {
     const u64 blocks = std::min<u64>((mid + 7) / 8, u64(sms) * 8);
-    mod_warp<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinSort64), mid, C, tot, sums);
+    mod_warp<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinWarp), mid, C, tot, sums);
     LVN_LAUNCH();
   }
   const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
