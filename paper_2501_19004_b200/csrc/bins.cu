@@ -128,6 +128,42 @@ __global__ void reset_thread(DGraph g, u32 short_max, double* __restrict__ K,
   }
 }
 
+// rows of the register-sort bins above 32 arcs: a warp per row, K arcs per
+// lane, two rows in flight per warp
+template <int K>
+__global__ void __launch_bounds__(256) reset_group(DGraph g, const u32* __restrict__ list, u64 count,
+                                                   double* __restrict__ K_out, double* __restrict__ sigma) {
+  const u32 lane = threadIdx.x & 31;
+  const u64 wi = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
+  const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
+  for (u64 i = wi; i < count; i += 2 * warps) {
+    u32 v[2];
+    float w[2][K];
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      const u64 ij = i + u64(j) * warps;
+      v[j] = ij < count ? list[ij] : 0u;
+      const u64 lo = ij < count ? g.off[v[j]] : 0, hi = ij < count ? g.off[v[j] + 1] : 0;
+#pragma unroll
+      for (int r = 0; r < K; ++r) {
+        const u64 a = lo + u64(r) * 32 + lane;
+        w[j][r] = a < hi ? __ldcs(g.w + a) : 0.f;
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < 2; ++j) {
+      double k = 0.0;
+#pragma unroll
+      for (int r = 0; r < K; ++r) k += double(w[j][r]);
+      k = warp_sum(k);
+      if (lane == 0 && i + u64(j) * warps < count) {
+        K_out[v[j]] = k;
+        if (sigma) sigma[v[j]] = k;
+      }
+    }
+  }
+}
+
 __global__ void reset_warp(DGraph g, const u32* __restrict__ list, u64 count,
                            double* __restrict__ K, double* __restrict__ sigma) {
   const int lane = threadIdx.x & 31;
@@ -175,11 +211,21 @@ void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C
   // rows of <= 32 arcs: one thread, sequential sum (the reference's order)
   reset_thread<<<unsigned(tb), 256, 0, s>>>(g, 32u, K, sigma, C, flags);
   LVN_LAUNCH();
-  // 32 < deg <= warp_max (plus any short rows binned there): one warp per row
-  const u64 mid = b.start[kBinBlock] - b.start[kBinSort64];
+  // 32 < deg <= 256 in the register-sort bins: a warp per row, K arcs per lane
+  auto grp = [&](int bin, auto kernel) {
+    if (!b.count(bin)) return;
+    const u64 wb = std::min<u64>((b.count(bin) + 7) / 8, u64(sms) * 8);
+    kernel<<<unsigned(wb), 256, 0, s>>>(g, b.of(bin), b.count(bin), K, sigma);
+    LVN_LAUNCH();
+  };
+  grp(kBinSort64, reset_group<2>);
+  grp(kBinSort128, reset_group<4>);
+  grp(kBinSort256, reset_group<8>);
+  // the warp bin (deg <= warp_max, plus any short rows binned there): one warp per row
+  const u64 mid = b.count(kBinWarp);
   if (mid) {
     const u64 wb = std::min<u64>((mid + 7) / 8, u64(sms) * 16);
-    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinSort64), mid, K, sigma);
+    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinWarp), mid, K, sigma);
     LVN_LAUNCH();
   }
   const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
