@@ -79,7 +79,10 @@ void* Pool::get(size_t bytes) {
     auto it = big_free_.lower_bound(r);
     void* p = nullptr;
     size_t have = r;
-    if (it != big_free_.end() && it->first <= r + r / 4) {
+    // any cached block up to 4x the request is reused: growing the pool maps
+    // new physical memory (hundreds of ms for the multi-GB tables of a skewed
+    // graph), whereas an oversized block only idles memory
+    if (it != big_free_.end() && it->first <= 4 * r) {
       p = it->second, have = it->first;
       big_free_.erase(it);
     } else {

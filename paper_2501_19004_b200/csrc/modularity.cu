@@ -172,17 +172,13 @@ void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot,
     kernel<<<unsigned(blocks), 256, 0, s>>>(g, b.of(bin), b.count(bin), C, tot, sums);
     LVN_LAUNCH();
   };
-  if (b.edges.thread_max <= 8) {
-    grp(kBinThread, mod_group<8, 1>, 8);
-  } else {
-    const u64 blocks = std::min<u64>((b.count(kBinThread) + 255) / 256, u64(sms) * 8);
-    if (b.count(kBinThread)) {
-      mod_thread<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinThread), b.count(kBinThread), C, tot, sums);
-      LVN_LAUNCH();
-    }
+  // rows of <= 16 arcs (thread, sort8 and sort16 bins, adjacent in the list): a thread each
+  const u64 small = b.start[kBinSort32] - b.start[kBinThread];
+  if (small) {
+    const u64 blocks = std::min<u64>((small + 255) / 256, u64(sms) * 8);
+    mod_thread<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinThread), small, C, tot, sums);
+    LVN_LAUNCH();
   }
-  grp(kBinSort8, mod_group<8, 1>, 8);
-  grp(kBinSort16, mod_group<16, 1>, 16);
   grp(kBinSort32, mod_group<32, 1>, 32);
   grp(kBinSort64, mod_group<32, 2>, 32);
   grp(kBinSort128, mod_group<32, 4>, 32);

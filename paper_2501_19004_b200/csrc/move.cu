@@ -917,6 +917,11 @@ template <class Tab>
 constexpr size_t block_smem() {
   return (size_t(1) << kBlockCapLog) * Tab::kSlotBytes + (size_t(1) << (kBlockCapLog - 1)) * 4;
 }
+// lm_block also stages the row: 4096 (community, f32 weight) pairs
+template <class Tab>
+constexpr size_t block_stage_smem() {
+  return block_smem<Tab>() + (size_t(1) << (kBlockCapLog - 1)) * 8;
+}
 
 template <class Tab, bool DRY>
 __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32* __restrict__ list,
@@ -930,6 +935,8 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
   __shared__ u32 bcast, nlive;
   const Tab tab(smem, u64(1) << kBlockCapLog);
   u32* live = reinterpret_cast<u32*>(smem + (size_t(1) << kBlockCapLog) * Tab::kSlotBytes);
+  u32* st_c = live + (size_t(1) << (kBlockCapLog - 1));
+  float* st_w = reinterpret_cast<float*>(st_c + (size_t(1) << (kBlockCapLog - 1)));
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   for (u32 s = threadIdx.x; s < (1u << kBlockCapLog); s += kBlockThreads) tab.clear(s);
   if (threadIdx.x == 0) nlive = 0;
@@ -956,20 +963,93 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
       if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
       continue;
     }
+    // stage the row's (community, weight) pairs in smem (coalesced loads, B
+    // gathers in flight per thread); a self-loop is staged as a zero-weight
+    // entry of u's own community, so rows stored sorted by target under an
+    // ascending C (every row of a pass's first sweep) stay strictly ascending
     V own = V(0);
-    scan_arcs<kBatch, true>(x, tab, lg, u, from, lo, lo + d, threadIdx.x, kBlockThreads, own, live, &nlive);
+    bool up = true;
+    for (u64 b0 = 0; b0 < d; b0 += u64(kBlockThreads) * kBatch) {
+      u32 t[kBatch];
+      float w[kBatch];
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {
+        const u64 e = b0 + threadIdx.x + u64(k) * kBlockThreads;
+        t[k] = e < d ? __ldcs(x.g.tgt + lo + e) : kEmpty;
+        w[k] = e < d ? __ldcs(x.g.w + lo + e) : 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < kBatch; ++k) {
+        const u64 e = b0 + threadIdx.x + u64(k) * kBlockThreads;
+        if (t[k] == kEmpty) continue;
+        const u32 c = t[k] == u ? from : x.C[t[k]];
+        if (t[k] == u) w[k] = 0.f;
+        if (c == from) own += V(w[k]);
+        st_c[e] = c;
+        st_w[e] = w[k];
+      }
+    }
+    __syncthreads();
+    for (u64 e = threadIdx.x; e + 1 < d; e += kBlockThreads) up = up && st_c[e] < st_c[e + 1];
+    const bool rows_sorted = __syncthreads_and(up);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
     if (lane == 0) red_v[wid] = own;
+    if (!rows_sorted) {
+      // merge the staged pairs into the table, combining duplicates per warp round
+      for (u64 e0 = 0; e0 < d; e0 += kBlockThreads) {
+        const u64 e = e0 + threadIdx.x;
+        u32 c = e < d ? st_c[e] : kEmpty;
+        V w = e < d ? V(st_w[e]) : V(0);
+        if (c == from) c = kEmpty;
+        if (!__all_sync(0xffffffffu, __match_any_sync(0xffffffffu, c) == (1u << lane) || c == kEmpty)) {
+          u32 kk[1] = {c};
+          V vv[1] = {w};
+          bitonic_sort<32, 1, V>(kk, vv, lane);
+          bool tl1[1];
+          segmented_runs<32, 1, V>(kk, vv, tl1, lane);
+          c = tl1[0] ? kk[0] : kEmpty, w = vv[0];
+        }
+        if (c != kEmpty) {
+          const int slot = tab.insert(lg, c, w);
+          if (slot >= 0) live[atomicAdd(&nlive, 1u)] = u32(slot);
+        }
+      }
+    }
     __syncthreads();
     V own_all = V(0);
 #pragma unroll
     for (int k = 0; k < W; ++k) own_all += red_v[k];
-    const u32 n = nlive;
+    const u32 n = rows_sorted ? u32(d) : nlive;
     const double ku = x.K[u], sf = x.sigma[from];
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
-    rank_live<kBatch, DRY>(x, tab, live, n, threadIdx.x, kBlockThreads, double(own_all), ku, sf, bg, bc, bk);
+    if (rows_sorted) {
+      // every staged entry is its own community: rank them directly
+      for (u32 j0 = threadIdx.x; j0 < n; j0 += kBlockThreads * kBatch) {
+        u32 key[kBatch];
+        double val[kBatch], sc[kBatch];
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+          const u32 j = j0 + k * kBlockThreads;
+          key[k] = j < n ? st_c[j] : kEmpty;
+          val[k] = j < n ? double(V(st_w[j])) : 0.0;
+          if (key[k] == from || (key[k] != kEmpty && !(key_ok(x, key[k]) &&
+                                                      (DRY || may_gain(x, val[k], double(own_all), ku, sf)))))
+            key[k] = kEmpty;
+        }
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) sc[k] = key[k] != kEmpty ? x.sigma[key[k]] : 0.0;
+#pragma unroll
+        for (int k = 0; k < kBatch; ++k) {
+          if (key[k] == kEmpty) continue;
+          const double g = score<DRY, V>(x, val[k], double(own_all), ku, sc[k], sf);
+          if (better(g, key[k], bg, bc)) bg = g, bc = key[k], bk = val[k];
+        }
+      }
+    } else {
+      rank_live<kBatch, DRY>(x, tab, live, n, threadIdx.x, kBlockThreads, double(own_all), ku, sf, bg, bc, bk);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double og = __shfl_xor_sync(0xffffffffu, bg, o);
@@ -979,7 +1059,8 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
     }
     if (lane == 0) red_g[wid] = bg, red_c[wid] = bc, red_k[wid] = bk;
     __syncthreads();
-    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) tab.clear(live[j]);
+    if (!rows_sorted)
+      for (u32 j = threadIdx.x; j < n; j += kBlockThreads) tab.clear(live[j]);
     if (threadIdx.x == 0) {
       for (int k = 1; k < W; ++k)
         if (better(red_g[k], red_c[k], bg, bc)) bg = red_g[k], bc = red_c[k], bk = red_k[k];
@@ -1266,7 +1347,7 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
       }
       case kBinBlock: {
         auto k = lm_block<Tab, DRY>;
-        constexpr size_t smem = block_smem<Tab>();
+        constexpr size_t smem = block_stage_smem<Tab>();
         static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
         MoveArgs ab = a;
         ab.chunk = std::min(a.chunk, a.hub_chunk);
