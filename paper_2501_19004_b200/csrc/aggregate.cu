@@ -592,12 +592,46 @@ __global__ void __launch_bounds__(256) ag_big_arcs(AggArgs x, const u32* __restr
   }
 }
 
+// present entries of the dense regions, all regions' chunks spread over the
+// whole grid (one block per region left most SMs idle on few giant
+// communities): warp-compacted appends to the region's row (live_n counts)
+constexpr u64 kDenseChunk = 16384;
+__global__ void __launch_bounds__(256) ag_dense_scan(AggArgs x, const u32* __restrict__ big, u64 nbig,
+                                                     const u64* __restrict__ tab_off, const unsigned char* tables,
+                                                     u32* __restrict__ live_n) {
+  const u64 cpc = (u64(x.count) + kDenseChunk - 1) / kDenseChunk;
+  const u32 lane = threadIdx.x & 31;
+  for (u64 q = blockIdx.x; q < nbig * cpc; q += gridDim.x) {
+    const u64 i = q / cpc, j0 = (q % cpc) * kDenseChunk;
+    const u32 c = big[i];
+    const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
+    if (!big_dense(hcap, x.count, x.big_mode)) continue;
+    const ull* d = reinterpret_cast<const ull*>(tables + tab_off[i]);
+    const u64 j1 = min(j0 + kDenseChunk, u64(x.count));
+    for (u64 b = j0; b < j1; b += blockDim.x) {
+      const u64 j = b + threadIdx.x;
+      const ull bits = j < j1 ? d[j] : kDenseEmpty;
+      const bool live = bits != kDenseEmpty;
+      const u32 bal = __ballot_sync(0xffffffffu, live);
+      u32 wbase = 0;
+      if (lane == 0 && bal) wbase = atomicAdd(&live_n[i], __popc(bal));
+      wbase = __shfl_sync(0xffffffffu, wbase, 0);
+      if (live) {
+        const u32 o = wbase + __popc(bal & ((1u << lane) - 1u));
+        if (o < hcap) {
+          x.htgt[hbase + o] = u32(j);
+          x.hw[hbase + o] = float(__longlong_as_double((long long)bits));  // fp64 sum narrowed once
+        }
+      }
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, const u32* __restrict__ big, u64 nbig,
                                                              const u64* __restrict__ tab_off,
                                                              unsigned char* tables, u32* __restrict__ live_n,
                                                              const double* __restrict__ own_sum,
                                                              const u32* __restrict__ own_seen) {
-  __shared__ u32 cursor;
   for (u64 i = blockIdx.x; i < nbig; i += gridDim.x) {
     const u32 c = big[i];
     const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
@@ -605,29 +639,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, const u3
     const u32 self = own_seen[i] ? 1u : 0u;
     u32 n = 0;
     if (big_dense(hcap, x.count, x.big_mode)) {
-      // present entries of the dense array, compacted through a block cursor
-      if (threadIdx.x == 0) cursor = 0;
-      __syncthreads();
-      const ull* d = reinterpret_cast<const ull*>(base);
-      for (u64 j0 = 0; j0 < x.count; j0 += kBlockThreads) {
-        const u64 j = j0 + threadIdx.x;
-        const ull bits = j < x.count ? d[j] : kDenseEmpty;
-        const bool live = bits != kDenseEmpty;
-        const u32 bal = __ballot_sync(0xffffffffu, live);
-        u32 wbase = 0;
-        if ((threadIdx.x & 31) == 0 && bal) wbase = atomicAdd(&cursor, __popc(bal));
-        wbase = __shfl_sync(0xffffffffu, wbase, 0);
-        if (live) {
-          const u32 o = wbase + __popc(bal & ((1u << (threadIdx.x & 31)) - 1u));
-          if (o < hcap) {
-            x.htgt[hbase + o] = u32(j);
-            x.hw[hbase + o] = float(__longlong_as_double((long long)bits));  // fp64 sum narrowed once
-          }
-        }
-      }
-      __syncthreads();
-      n = cursor;
-      __syncthreads();
+      n = live_n[i];  // entries already emitted by ag_dense_scan
     } else {
       const u64 slots = big_slots(hcap);
       const BigSlot* t = reinterpret_cast<const BigSlot*>(base);
@@ -800,6 +812,8 @@ void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
       }
       ag_big_arcs<<<unsigned(u64(sms) * occ), 256, 0, s>>>(a, index.p, tab_off.p, base, live_n.p, own.p,
                                                             own_seen.p, L.p, P.p, kpos.p + M, arc_lo, arc_hi);
+      LVN_LAUNCH();
+      ag_dense_scan<<<unsigned(u64(sms) * 8), 256, 0, s>>>(a, big + b0, nb, tab_off.p + b0, base, live_n.p + b0);
       LVN_LAUNCH();
       ag_big_emit<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), kBlockThreads, 0, s>>>(
           a, big + b0, nb, tab_off.p + b0, base, live_n.p + b0, own.p + b0, own_seen.p + b0);
