@@ -11,6 +11,13 @@ namespace lvn {
 namespace {
 
 constexpr int kT = 256;     // threads per tile
+
+// uniform-weight detection folded into the reset's row reads: any arc weight
+// differing from the first arc's clears *uni (one atomic per warp at most)
+__device__ __forceinline__ void uni_flush(u32* uni, bool differs) {
+  if (uni && __any_sync(__activemask(), differs) && (threadIdx.x & 31) == (__ffs(__activemask()) - 1))
+    atomicAnd(uni, 0u);
+}
 constexpr int kRounds = 8;  // vertices per thread per tile
 constexpr int kTileV = kT * kRounds;
 
@@ -113,7 +120,9 @@ __global__ void gather_starts(const u64* pos, u32 nblocks, const ull* max_deg, u
 // short rows (same summation order as the reference)
 __global__ void reset_thread(DGraph g, u32 short_max, double* __restrict__ K,
                              double* __restrict__ sigma, u32* __restrict__ C,
-                             u8* __restrict__ flags) {
+                             u8* __restrict__ flags, u32* uni) {
+  const float wref = g.arcs ? g.w[0] : 0.f;
+  bool differs = false;
   for (u64 v = blockIdx.x * u64(blockDim.x) + threadIdx.x; v < g.n;
        v += u64(gridDim.x) * blockDim.x) {
     const u64 lo = g.off[v], hi = g.off[v + 1];
@@ -121,18 +130,26 @@ __global__ void reset_thread(DGraph g, u32 short_max, double* __restrict__ K,
     if (flags) flags[v] = hi > lo ? 1 : 0;
     if (hi - lo <= short_max) {
       double s = 0.0;
-      for (u64 a = lo; a < hi; ++a) s += double(g.w[a]);
+      for (u64 a = lo; a < hi; ++a) {
+        const float w = g.w[a];
+        differs = differs || w != wref;
+        s += double(w);
+      }
       K[v] = s;
       if (sigma) sigma[v] = s;
     }
   }
+  uni_flush(uni, differs);
 }
 
 // rows of the register-sort bins above 32 arcs: a warp per row, K arcs per
 // lane, two rows in flight per warp
 template <int K>
 __global__ void __launch_bounds__(256) reset_group(DGraph g, const u32* __restrict__ list, u64 count,
-                                                   double* __restrict__ K_out, double* __restrict__ sigma) {
+                                                   double* __restrict__ K_out, double* __restrict__ sigma,
+                                                   u32* uni) {
+  const float wref = g.arcs ? g.w[0] : 0.f;
+  bool differs = false;
   const u32 lane = threadIdx.x & 31;
   const u64 wi = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5;
   const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
@@ -148,13 +165,16 @@ __global__ void __launch_bounds__(256) reset_group(DGraph g, const u32* __restri
       for (int r = 0; r < K; ++r) {
         const u64 a = lo + u64(r) * 32 + lane;
         w[j][r] = a < hi ? __ldcs(g.w + a) : 0.f;
+        differs = differs || (a < hi && w[j][r] != wref);
       }
     }
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
       double k = 0.0;
 #pragma unroll
-      for (int r = 0; r < K; ++r) k += double(w[j][r]);
+      for (int r = 0; r < K; ++r) {
+        k += double(w[j][r]);
+      }
       k = warp_sum(k);
       if (lane == 0 && i + u64(j) * warps < count) {
         K_out[v[j]] = k;
@@ -162,34 +182,48 @@ __global__ void __launch_bounds__(256) reset_group(DGraph g, const u32* __restri
       }
     }
   }
+  uni_flush(uni, differs);
 }
 
 __global__ void reset_warp(DGraph g, const u32* __restrict__ list, u64 count,
-                           double* __restrict__ K, double* __restrict__ sigma) {
+                           double* __restrict__ K, double* __restrict__ sigma, u32* uni) {
+  const float wref = g.arcs ? g.w[0] : 0.f;
+  bool differs = false;
   const int lane = threadIdx.x & 31;
   const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
   for (u64 i = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; i < count; i += warps) {
     const u32 v = list[i];
     const u64 lo = g.off[v], hi = g.off[v + 1];
     double s = 0.0;
-    for (u64 a = lo + lane; a < hi; a += 32) s += double(g.w[a]);
+    for (u64 a = lo + lane; a < hi; a += 32) {
+      const float w = g.w[a];
+      differs = differs || w != wref;
+      s += double(w);
+    }
     s = warp_sum(s);
     if (lane == 0) {
       K[v] = s;
       if (sigma) sigma[v] = s;
     }
   }
+  uni_flush(uni, differs);
 }
 
 __global__ void __launch_bounds__(512) reset_block(DGraph g, const u32* __restrict__ list,
                                                    u64 count, double* __restrict__ K,
-                                                   double* __restrict__ sigma) {
+                                                   double* __restrict__ sigma, u32* uni) {
   __shared__ double ws[16];
+  const float wref = g.arcs ? g.w[0] : 0.f;
+  bool differs = false;
   for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
     const u32 v = list[i];
     const u64 lo = g.off[v], hi = g.off[v + 1];
     double s = 0.0;
-    for (u64 a = lo + threadIdx.x; a < hi; a += blockDim.x) s += double(g.w[a]);
+    for (u64 a = lo + threadIdx.x; a < hi; a += blockDim.x) {
+      const float w = g.w[a];
+      differs = differs || w != wref;
+      s += double(w);
+    }
     s = warp_sum(s);
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
     __syncthreads();
@@ -201,21 +235,22 @@ __global__ void __launch_bounds__(512) reset_block(DGraph g, const u32* __restri
     }
     __syncthreads();
   }
+  uni_flush(uni, differs);
 }
 
 void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C, u8* flags,
-                cudaStream_t s) {
+                cudaStream_t s, u32* uni = nullptr) {
   if (g.n == 0) return;
   const int sms = sm_count();
   const u64 tb = std::min<u64>((g.n + 255) / 256, u64(sms) * 16);
   // rows of <= 32 arcs: one thread, sequential sum (the reference's order)
-  reset_thread<<<unsigned(tb), 256, 0, s>>>(g, 32u, K, sigma, C, flags);
+  reset_thread<<<unsigned(tb), 256, 0, s>>>(g, 32u, K, sigma, C, flags, uni);
   LVN_LAUNCH();
   // 32 < deg <= 256 in the register-sort bins: a warp per row, K arcs per lane
   auto grp = [&](int bin, auto kernel) {
     if (!b.count(bin)) return;
     const u64 wb = std::min<u64>((b.count(bin) + 7) / 8, u64(sms) * 8);
-    kernel<<<unsigned(wb), 256, 0, s>>>(g, b.of(bin), b.count(bin), K, sigma);
+    kernel<<<unsigned(wb), 256, 0, s>>>(g, b.of(bin), b.count(bin), K, sigma, uni);
     LVN_LAUNCH();
   };
   grp(kBinSort64, reset_group<2>);
@@ -225,13 +260,13 @@ void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C
   const u64 mid = b.count(kBinWarp);
   if (mid) {
     const u64 wb = std::min<u64>((mid + 7) / 8, u64(sms) * 16);
-    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinWarp), mid, K, sigma);
+    reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinWarp), mid, K, sigma, uni);
     LVN_LAUNCH();
   }
   const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
   if (big) {
     const u64 bb = std::min<u64>(big, u64(sms) * 4);
-    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(kBinBlock), big, K, sigma);
+    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(kBinBlock), big, K, sigma, uni);
     LVN_LAUNCH();
   }
 }
@@ -300,8 +335,9 @@ void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStrea
 }
 
 void pass_reset(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C, u8* flags,
-                cudaStream_t s) {
-  reset_impl(g, b, K, sigma, C, flags, s);
+                cudaStream_t s, u32* uniform) {
+  if (uniform) LVN_CUDA(cudaMemsetAsync(uniform, 0xFF, sizeof(u32), s));
+  reset_impl(g, b, K, sigma, C, flags, s, uniform);
 }
 
 void vertex_weights(const DGraph& g, const Bins& b, double* K, cudaStream_t s) {

@@ -682,6 +682,14 @@ void check_err(const u32* err, cudaStream_t s) {
 // sharded by row range across the ranks; every rank keeps the
 // whole current graph, the replicated C / Sigma / flags, and ends with the same
 // result (the passes that run whole run redundantly on every rank).
+bool no_uniform() {
+  static const bool v = [] {
+    const char* e = std::getenv("LVN_UNIFORM");
+    return e && std::string(e) == "0";
+  }();
+  return v;
+}
+
 void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* comm = nullptr) {
   const auto t_start = Clock::now();
   Context& c = ctx();
@@ -701,7 +709,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   HubPlan hubs;
   DBuf<u8> flags(N ? N : 1);
   DBuf<IterRecord> rec(1);
-  DBuf<u32> err(1);
+  DBuf<u32> err(1), uni(1);
   LVN_CUDA(cudaMemsetAsync(err.p, 0, sizeof(u32), s));
   iota_u32(global.p, N, s);
 
@@ -741,8 +749,16 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     compute_bins(cur.off, nv, edges, B, s);
     if (pass == 0) have_in_bins = true;
     size_t sp = tm.begin(LVN_STAT_RESET, s);
-    pass_reset(cur, B, K.p, S.p, C.p, flags.p, s);
+    pass_reset(cur, B, K.p, S.p, C.p, flags.p, s, uni.p);
     tm.end(sp, s, 4.0 * double(cur.arcs) + 29.0 * nv);
+    // uniform arc weights (every unit-weight input's first pass): the sort
+    // bins key on the community alone (LVN_UNIFORM=0 disables)
+    bool uniform = false;
+    float uniform_w = 0.f;
+    if (cur.arcs && !no_uniform()) {
+      uniform = read_scalar(uni.p, s) != 0;
+      if (uniform) uniform_w = read_scalar(cur.w, s);
+    }
 
     // sharded pass: this rank decides the rows [v0, v1)
     const bool shard = cm.on() && cur.arcs >= (u64(1) << p.shard_min_arcs_log2);
@@ -769,6 +785,8 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     a.counters = &rec.p->verts;
     a.err = err.p;
     a.chunk = sweep_chunk(p, nv);
+    a.uniform = uniform;
+    a.uniform_w = uniform_w;
     // LVN_HUB_CHUNK=k: decide the block / hub bins k vertices per launch, so
     // later hubs see earlier hubs' moves (tuning aid; +0.0003 Q on RMAT-24)
     if (const char* e = std::getenv("LVN_HUB_CHUNK")) a.hub_chunk = std::strtoull(e, nullptr, 10);

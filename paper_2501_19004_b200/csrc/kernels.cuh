@@ -68,9 +68,10 @@ void compact_active(const Bins& b, const u8* flags, u32* out_list, ull* counts, 
 // vertex range: off points at the range's first offset).
 void compute_bins(const u64* off, u32 n, const BinEdges& e, Bins& out, cudaStream_t s,
                   u64 cap = ~u64(0), u32 id_base = 0);
-// K_u = row sums (fp64), Sigma = K, C = identity, flags = deg > 0
+// K_u = row sums (fp64), Sigma = K, C = identity, flags = deg > 0; *uniform
+// (when given) ends non-zero iff every arc weight equals the first one
 void pass_reset(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C, u8* flags,
-                cudaStream_t s);
+                cudaStream_t s, u32* uniform = nullptr);
 void vertex_weights(const DGraph& g, const Bins& b, double* K, cudaStream_t s);
 
 // ---- move.cu: local-moving sweep ------------------------------------------
@@ -91,6 +92,8 @@ struct MoveArgs {
   u32* err = nullptr;
   u64 chunk = ~u64(0);         // max vertices of one bin decided per launch
   u64 hub_chunk = ~u64(0);     // max vertices of the block / hub bins decided per launch
+  int uniform = 0;             // every arc weight equals uniform_w: sort bins key on the community alone
+  float uniform_w = 0.f;
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
   int hubs_first = 0;          // bin order of a sweep: highest degree class first
   u32* csize = nullptr;        // community member counts (singleton-pair rule), or null

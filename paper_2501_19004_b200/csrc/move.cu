@@ -550,7 +550,7 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
 // compute step of its own between issue and use. The targets of i and i+1 stay
 // in registers for the neighbour marks. Gathers for i+1 may miss the move of
 // i (asynchrony the validated join tolerates); DRY writes no state.
-template <int G, int K, class V, bool DRY>
+template <int G, int K, class V, bool DRY, bool U>
 __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(MoveArgs x, const u32* __restrict__ list, u64 count) {
   constexpr int GPB = 256 / G;
   constexpr int N = G * K;
@@ -579,12 +579,18 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
   // padding carries no key; a self-loop keeps its place in the row as a
   // zero-weight element of u's own community (K_{u->c} excludes self-loops,
   // louvain_compact.cpp:46), so rows stored sorted by target stay sorted
+  // U (every arc weight equals x.uniform_w): the key is the community alone,
+  // so any n fits, and self-loops are dropped
   auto gather = [&](u32 v, u32 vfrom, const u32 (&t)[K], u32 (&key)[K], V (&w)[K]) {
 #pragma unroll
     for (int r = 0; r < K; ++r) {
-      const u32 c = t[r] == v ? vfrom : (t[r] != kEmpty ? ld_keep(x.C + t[r], keep) : 0u);
-      key[r] = t[r] != kEmpty ? (c << LB) | u32(r * G + lane) : kNoKey;
-      if (t[r] == v) w[r] = V(0);
+      if (U) {
+        key[r] = (t[r] != kEmpty && t[r] != v) ? ld_keep(x.C + t[r], keep) : kNoKey;
+      } else {
+        const u32 c = t[r] == v ? vfrom : (t[r] != kEmpty ? ld_keep(x.C + t[r], keep) : 0u);
+        key[r] = t[r] != kEmpty ? (c << LB) | u32(r * G + lane) : kNoKey;
+        if (t[r] == v) w[r] = V(0);
+      }
     }
   };
 
@@ -642,7 +648,7 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
     }
     rows = __all_sync(FULL, rows);
     if (!rows) {
-      if (K > 1) {
+      if (K > 1 && !U) {
         __syncwarp();
 #pragma unroll
         for (int r = 0; r < K; ++r) gbuf[r * G + lane] = val[r];
@@ -656,10 +662,11 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
     for (int r = 0; r < K; ++r) {
       const u32 pos = key[r] & u32(N - 1);
       V w;
-      if (rows) w = val[r];
+      if (U) w = V(x.uniform_w);
+      else if (rows) w = val[r];
       else if (K == 1) w = __shfl_sync(FULL, val[0], pos, G);
       else w = gbuf[pos];
-      ck[r] = key[r] == kNoKey ? kEmpty : key[r] >> LB;
+      ck[r] = key[r] == kNoKey ? kEmpty : (U ? key[r] : key[r] >> LB);
       run[r] = key[r] == kNoKey ? V(0) : w;
     }
     bool tail[K];
@@ -1288,9 +1295,15 @@ void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
   if (!b.count(bin)) return;
   constexpr int T = 256;
   constexpr int LB = ilog2<G * K>();
-  // packed keys need (n - 1) << LB | (N - 1) < 0xFFFFFFFF
+  // community-only keys for uniform weights; packed keys need (n - 1) << LB | (N - 1) < 0xFFFFFFFF
+  if (move_kernel_choice() == 0 && a.uniform && !DRY) {
+    auto k = lm_psort<G, K, V, DRY, true>;
+    static const int occ = occupancy(k, T, 0);
+    launch_chunks(k, a, b.of(bin), b.count(bin), T, T / G, u64(sm_count()) * occ, 0, s);
+    return;
+  }
   if (move_kernel_choice() == 0 && u64(a.g.n) < (u64(1) << (32 - LB))) {
-    auto k = lm_psort<G, K, V, DRY>;
+    auto k = lm_psort<G, K, V, DRY, false>;
     static const int occ = occupancy(k, T, 0);
     launch_chunks(k, a, b.of(bin), b.count(bin), T, T / G, u64(sm_count()) * occ, 0, s);
     return;
