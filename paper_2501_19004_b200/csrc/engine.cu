@@ -38,6 +38,7 @@ void Pool::bind(int device, cudaStream_t s) {
   size_t free_b = 0, total_b = 0;
   LVN_CUDA(cudaMemGetInfo(&free_b, &total_b));
   cache_budget_ = total_b / 4;
+  if (const char* e = std::getenv("LVN_CACHE_FRAC")) cache_budget_ = size_t(double(total_b) * std::atof(e));
   total_ = total_b;
 }
 
