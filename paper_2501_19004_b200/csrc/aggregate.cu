@@ -124,20 +124,57 @@ __global__ void __launch_bounds__(256) ag_psort(AggArgs x, const u32* __restrict
     u64 mlo = 0, mhi = 0;
     if (have) mlo = x.coff[c], mhi = x.coff[c + 1];
     __syncwarp();
-    u64 base = 0;
-    for (u64 k = mlo; k < mhi; ++k) {
-      const u32 v = x.members[k];
-      const u64 lo = x.g.off[v], d = x.g.off[v + 1] - lo;
+    const u64 nm = mhi - mlo;
+    if (__all_sync(FULL, nm <= u64(G))) {
+      // lane j holds member j's row: an inclusive scan of the row lengths
+      // maps every element to its member (shuffle search), so all K arcs per
+      // lane are loaded at once instead of one member row after another
+      u64 mlo_j = 0, md_j = 0;
+      if (lane < nm) {
+        const u32 v = x.members[mlo + lane];
+        mlo_j = x.g.off[v];
+        md_j = x.g.off[v + 1] - mlo_j;
+      }
+      u64 end_j = md_j;  // inclusive prefix of the row lengths
+#pragma unroll
+      for (int o = 1; o < G; o <<= 1) {
+        const u64 y = __shfl_up_sync(FULL, end_j, o, G);
+        if (lane >= u32(o)) end_j += y;
+      }
+      const u64 total = __shfl_sync(FULL, end_j, G - 1, G);
 #pragma unroll
       for (int r = 0; r < K; ++r) {
         const u64 e = u64(r) * G + lane;
-        if (e >= base && e < base + d) {
-          const u64 a = lo + (e - base);
+        u32 j = 0;  // first member whose inclusive end exceeds e
+#pragma unroll
+        for (u32 step = G / 2; step; step >>= 1) {
+          const u64 en = __shfl_sync(FULL, end_j, j + step - 1, G);
+          if (en <= e) j += step;
+        }
+        const u64 lo_j = __shfl_sync(FULL, mlo_j, j, G);
+        const u64 st_j = __shfl_sync(FULL, end_j - md_j, j, G);
+        if (e < total) {
+          const u64 a = lo_j + (e - st_j);
           key[r] = (x.C[__ldcs(x.g.tgt + a)] << LB) | u32(e);
           gw[e] = __ldcs(x.g.w + a);
         }
       }
-      base += d;
+    } else {
+      u64 base = 0;
+      for (u64 k = mlo; k < mhi; ++k) {
+        const u32 v = x.members[k];
+        const u64 lo = x.g.off[v], d = x.g.off[v + 1] - lo;
+#pragma unroll
+        for (int r = 0; r < K; ++r) {
+          const u64 e = u64(r) * G + lane;
+          if (e >= base && e < base + d) {
+            const u64 a = lo + (e - base);
+            key[r] = (x.C[__ldcs(x.g.tgt + a)] << LB) | u32(e);
+            gw[e] = __ldcs(x.g.w + a);
+          }
+        }
+        base += d;
+      }
     }
     __syncwarp();
     psort<G, K>(key, dirs);
