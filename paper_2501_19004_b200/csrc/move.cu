@@ -634,8 +634,6 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
     const u32 u2 = have2 ? list[in2] : 0u;
 
     // (i) group the arcs by community, fetch the weights in sorted order
-#pragma unroll
-    for (int r = 0; r < K; ++r) tl.rand += key[r] != kNoKey ? 1 : 0;
     // rows whose communities already ascend in row order (every row in the
     // first sweep of a pass: rows are stored sorted by target and C is the
     // identity) skip the network and take the row-order run sums
@@ -725,6 +723,7 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
       if (!DRY) x.flags[u] = 0;
       ++tl.verts;
       tl.arcs += hi - lo;
+      tl.rand += hi - lo;  // C[t] gathers (one per arc)
       moved = decide<DRY>(x, u, from, ku, best, best == kEmpty ? -INFINITY : bg, bk, double(own), tl);
     }
     if (!DRY && x.prune && ((__ballot_sync(FULL, moved) >> gshift) & GMASK)) {
