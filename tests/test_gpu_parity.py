@@ -423,3 +423,27 @@ def test_dendrogram_levels(lvn, port):
     pairs = set(zip(a.tolist(), b.tolist()))
     assert len(pairs) == len(set(a.tolist())) == len(set(b.tolist())) == r.num_communities
     assert lvn.louvain_compact(G_(g, lvn)).levels == []
+
+
+def test_uniform_weight_passes(lvn, port):
+    # equal arc weights (any value) take community-only sort keys in the first
+    # pass; modularity is scale-free, so scaled weights must land where unit
+    # weights do, and a single odd weight takes the packed-key path
+    g = planted(30000, 60, 24, 0.15, 21)
+    r1 = lvn.louvain_compact(G_(g, lvn))
+    src, dst = edge_arrays(g)
+    g25 = port.build_csr(g.n, src, dst, np.full(len(src), 2.5))
+    r25 = lvn.louvain_compact(G_(g25, lvn))
+    assert abs(r25.modularity - r1.modularity) < 0.01
+    assert_q(r25.modularity, port.modularity(g25, r25.membership))
+    w = g.weights.copy()
+    w[7] = 3.0
+    gx = lvn.CsrGraph(g.offsets, g.targets, w, float(w.astype(np.float64).sum()) / 2)
+    rx = lvn.louvain_compact(gx)
+    assert rx.modularity > r1.modularity - 0.01
+
+
+def edge_arrays(g):
+    src = np.repeat(np.arange(g.n, dtype=np.uint32), np.diff(g.offsets).astype(np.int64))
+    keep = src < g.targets
+    return src[keep], g.targets[keep]
