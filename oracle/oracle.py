@@ -329,6 +329,8 @@ class _Ref:
             L.ref_graph_total_weight.argtypes = [vp]
             L.ref_graph_total_weight.restype = C.c_double
             L.ref_graph_export.argtypes = [vp, u64p, u32p, f32p]
+            L.ref_generate.argtypes = [C.c_int, C.c_uint64, C.c_uint64, C.c_uint32, C.c_uint32] + [C.c_double] * 6 + \
+                [C.c_uint64, C.POINTER(vp)]
             L.ref_build_csr.argtypes = [C.c_uint32, C.c_uint64, u32p, u32p, f64p, C.c_int, C.POINTER(vp)]
             L.ref_random_edges.argtypes = [C.c_uint32, C.c_uint64, C.c_double, C.c_double, C.c_uint64, C.c_int,
                                            C.c_int]
@@ -397,6 +399,46 @@ class _Ref:
         off, tgt, w = _g(g)
         h = self.lib.ref_graph_from_arrays(len(off) - 1, off, tgt, w, float(g.total_weight))
         return _Ref._Handle(self.lib, h)
+
+    def generate(self, kind: str, seed: int = 1, **kw) -> "_Ref._Handle":
+        """The GPU engine's synthetic inputs built on the host (gen_host.cpp),
+        same parameters as paper_2501_19004_b200.generate; returns a graph
+        handle (use n/arcs/export on it)."""
+        a, b, c, mu, p, deg = 0.57, 0.19, 0.19, 0.1, 0.6, 16.0
+        n = edges = scale = blocks = 0
+        if kind == "rmat":
+            k, scale = 0, kw["scale"]
+            edges = (1 << scale) * kw.get("edgefactor", 16)
+            a, b, c = kw.get("a", a), kw.get("b", b), kw.get("c", c)
+        elif kind == "sbm":
+            k, n, blocks = 1, kw["n"], kw["blocks"]
+            edges = int(kw["n"] * kw.get("avg_degree", 32) / 2)
+            mu = kw.get("mu", mu)
+        elif kind == "grid":
+            k, n, p = 2, kw["side"], kw.get("p", p)
+        elif kind == "web":
+            k, n, deg = 3, kw["n"], kw.get("avg_degree", 75.0)
+        elif kind == "uniform":
+            k, n, edges = 4, kw["n"], kw["edges"]
+        else:
+            raise ValueError(f"unknown generator {kind}")
+        h = C.c_void_p()
+        self._rc(self.lib.ref_generate(k, n, edges, scale, blocks, a, b, c, mu, p, deg, seed, C.byref(h)))
+        return _Ref._Handle(self.lib, h.value)
+
+    def graph_size(self, g) -> tuple[int, int]:
+        """(vertices, arcs) of a graph handle"""
+        return int(self.lib.ref_graph_n(g.h)), int(self.lib.ref_graph_arcs(g.h))
+
+    def export(self, g) -> Csr:
+        """copy a graph handle's CSR out (the handle stays valid)"""
+        L = self.lib
+        n, a = self.graph_size(g)
+        off = np.empty(n + 1, np.uint64)
+        tgt = np.empty(max(a, 1), np.uint32)
+        w = np.empty(max(a, 1), np.float32)
+        L.ref_graph_export(g.h, off, tgt, w)
+        return Csr(off, tgt[:a], w[:a], L.ref_graph_total_weight(g.h))
 
     def _export(self, h) -> Csr:
         L = self.lib

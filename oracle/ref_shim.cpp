@@ -36,6 +36,8 @@
 #include "louvain/quality.hpp"
 #include "louvain/synthetic.hpp"
 
+#include "gen_host.hpp"
+
 using namespace louvain;
 
 namespace {
@@ -138,6 +140,27 @@ int ref_build_csr(std::uint32_t n, std::uint64_t ntriples, const std::uint32_t* 
     el.triples.resize(ntriples);
     for (std::uint64_t i = 0; i < ntriples; ++i) el.triples[i] = {src[i], dst[i], w[i]};
     *out = new CsrGraph(build_csr(el, symmetrize != 0));
+  });
+}
+
+// ---- the GPU engine's synthetic inputs, built on the host (gen_host.cpp) ----
+// kind: 0 rmat(scale, edges), 1 sbm(n, blocks, edges, mu), 2 grid(side n, p),
+// 3 web(n, avg_degree), 4 uniform(n, edges). Returns a CsrGraph handle.
+int ref_generate(int kind, std::uint64_t n, std::uint64_t edges, std::uint32_t scale,
+                 std::uint32_t blocks, double a, double b, double c, double mu, double p,
+                 double avg_degree, std::uint64_t seed, void** out) {
+  return guard([&] {
+    genhost::Spec s;
+    s.kind = kind, s.n = n, s.edges = edges, s.scale = scale, s.blocks = blocks;
+    s.a = a, s.b = b, s.c = c, s.mu = mu, s.p = p, s.avg_degree = avg_degree, s.seed = seed;
+    auto* g = new CsrGraph;
+    try {
+      genhost::generate(s, *g);
+    } catch (...) {
+      delete g;
+      throw;
+    }
+    *out = g;
   });
 }
 

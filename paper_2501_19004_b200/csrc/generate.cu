@@ -121,7 +121,9 @@ __global__ void gen_uniform(ull* keys, u64 edges, u64 n, u64 seed) {
 // (truncated power law) edges, most inside its host within a locality window
 // of +-2 deg(u) ids (clipped to the host, so small hosts saturate towards
 // cliques, as navigation-linked web hosts do), the rest to global
-// preferential-attachment targets (low ids).
+// preferential-attachment targets (low ids). Only exact IEEE operations feed
+// the integer decisions (no pow/exp: the host restatement in
+// oracle/gen_host.cpp reproduces every sample bit for bit).
 __global__ void gen_web(ull* keys, const u64* __restrict__ eoff, u64 n, const u32* __restrict__ host_lo,
                         const u32* __restrict__ host_hi, double p_local, u64 window, u64 seed) {
   for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n;
@@ -139,9 +141,11 @@ __global__ void gen_web(ull* keys, const u64* __restrict__ eoff, u64 n, const u3
         const u64 b = u + w + 1 < hi ? u + w + 1 : hi;
         v = a + below(r1, b - a);
       } else {
-        // preferential attachment: P(v) ~ v^(-0.8) over the id space
+        // preferential attachment: v = n x^5, P(v) ~ v^(-0.8) over the id space
         const double x = unit(r1);
-        v = u64(double(n) * pow(x, 5.0));
+        const double x2 = __dmul_rn(x, x);
+        const double x5 = __dmul_rn(__dmul_rn(x2, x2), x);
+        v = u64(__dmul_rn(double(n), x5));
         if (v >= n) v = n - 1;
       }
       emit(keys, e, u32(u), u32(v));
@@ -149,16 +153,20 @@ __global__ void gen_web(ull* keys, const u64* __restrict__ eoff, u64 n, const u3
   }
 }
 
-__global__ void web_degrees(u64* __restrict__ deg, u64 n, double alpha, double dmin, double dmax,
+// out-degree: inverse CDF of a discrete power law over k = 1..K by binary
+// search on 53-bit integer thresholds, scaled to the requested mean
+__global__ void web_degrees(u64* __restrict__ deg, u64 n, const u64* __restrict__ thr, u32 kmax,
                             double scale, u64 seed) {
   for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n;
        u += u64(gridDim.x) * blockDim.x) {
-    // inverse-CDF sample of a power law truncated to [dmin, dmax]
-    const double x = unit(mix64(seed ^ mix64(u)));
-    const double a1 = 1.0 - alpha;
-    const double lo = pow(dmin, a1), hi = pow(dmax, a1);
-    const double d = pow(lo + x * (hi - lo), 1.0 / a1) * scale;
-    deg[u] = u64(d < 1.0 ? 1.0 : d);
+    const u64 x = mix64(seed ^ mix64(u)) >> 11;
+    u32 lo = 0, hi = kmax - 1;  // smallest k with x < thr[k]
+    while (lo < hi) {
+      const u32 mid = (lo + hi) >> 1;
+      if (x < thr[mid]) hi = mid; else lo = mid + 1;
+    }
+    const double dd = __dmul_rn(double(lo + 1), scale);
+    deg[u] = u64(dd < 1.0 ? 1.0 : dd);
   }
 }
 
@@ -212,6 +220,53 @@ __global__ void __launch_bounds__(kTileT) tile_place(const ull* __restrict__ key
 __global__ void fill_ones(float* w, u64 n) {
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
     w[i] = 1.0f;
+}
+
+constexpr double kWebLocal = 0.92;  // fraction of in-host (windowed) endpoints
+constexpr u64 kWebWindow = 64;       // minimum half-width of the locality window
+constexpr double kWebAlpha = 2.1;    // out-degree power-law exponent
+constexpr u32 kWebKmax = 100000;     // largest raw out-degree
+// undirected samples per vertex for a requested mean arc degree (absorbs the
+// loss to self-loops and duplicates; C5: 50.6 M vertices -> 3.80 G arcs)
+constexpr double kWebSamplesPerArc = 0.8615;
+
+struct WebShape {
+  std::vector<u32> host_lo, host_hi;
+  std::vector<u64> thresholds;  // thresholds[k-1] = floor(2^53 P(deg <= k))
+  double scale = 1.0;
+};
+
+// Host-side shape of the web graph, shared by every sample: Zipf host sizes in
+// [10, 1e6] (P(size >= x) ~ 1/x) from a seeded xorshift, the discrete
+// power-law CDF of the raw out-degree and its scale to the requested mean.
+void web_shape(u64 n, double avg_degree, u64 seed, WebShape& ws) {
+  ws.host_lo.resize(n);
+  ws.host_hi.resize(n);
+  u64 state = seed * 0x2545F4914F6CDD1Dull + 1;
+  auto rnd = [&]() {
+    state ^= state >> 12, state ^= state << 25, state ^= state >> 27;
+    return double((state * 0x2545F4914F6CDD1Dull) >> 11) * (1.0 / 9007199254740992.0);
+  };
+  for (u64 v = 0; v < n;) {
+    const double x = rnd();
+    u64 size = u64(10.0 / (1.0 - x * (1.0 - 10.0 / 1e6)));
+    if (size > n - v) size = n - v;
+    for (u64 k = v; k < v + size; ++k) ws.host_lo[k] = u32(v), ws.host_hi[k] = u32(v + size);
+    v += size;
+  }
+  std::vector<double> cdf(kWebKmax);
+  double total = 0.0, mean = 0.0;
+  for (u32 k = 1; k <= kWebKmax; ++k) {
+    const double pk = std::pow(double(k), -kWebAlpha);
+    total += pk;
+    cdf[k - 1] = total;
+    mean += double(k) * pk;
+  }
+  mean /= total;
+  ws.thresholds.resize(kWebKmax);
+  for (u32 k = 0; k < kWebKmax; ++k) ws.thresholds[k] = u64(cdf[k] / total * 9007199254740992.0);
+  ws.thresholds[kWebKmax - 1] = u64(1) << 53;
+  ws.scale = avg_degree * kWebSamplesPerArc / mean;
 }
 
 unsigned grid(u64 n) {
@@ -292,39 +347,21 @@ void generate(const GenSpec& g, OwnedCsr& out, cudaStream_t s) {
     }
     case 3: {  // web
       if (n < 16) fail(kInvalid, "web graph needs n >= 16");
-      // host side: Zipf host sizes in [10, 1e6]
-      std::vector<u32> hlo(n), hhi(n);
-      u64 state = g.seed * 0x2545F4914F6CDD1Dull + 1;
-      auto rnd = [&]() {
-        state ^= state >> 12, state ^= state << 25, state ^= state >> 27;
-        return double((state * 0x2545F4914F6CDD1Dull) >> 11) * (1.0 / 9007199254740992.0);
-      };
-      for (u64 v = 0; v < n;) {
-        // P(size >= x) ~ x^-1 truncated to [10, 1e6]
-        const double x = rnd();
-        u64 size = u64(10.0 / (1.0 - x * (1.0 - 10.0 / 1e6)));
-        if (size > n - v) size = n - v;
-        for (u64 k = v; k < v + size; ++k) hlo[k] = u32(v), hhi[k] = u32(v + size);
-        v += size;
-      }
+      WebShape ws;
+      web_shape(n, g.avg_degree, g.seed, ws);
       DBuf<u32> dlo(n), dhi(n);
-      LVN_CUDA(cudaMemcpyAsync(dlo.p, hlo.data(), n * 4, cudaMemcpyHostToDevice, s));
-      LVN_CUDA(cudaMemcpyAsync(dhi.p, hhi.data(), n * 4, cudaMemcpyHostToDevice, s));
+      DBuf<u64> thr(ws.thresholds.size());
+      LVN_CUDA(cudaMemcpyAsync(dlo.p, ws.host_lo.data(), n * 4, cudaMemcpyHostToDevice, s));
+      LVN_CUDA(cudaMemcpyAsync(dhi.p, ws.host_hi.data(), n * 4, cudaMemcpyHostToDevice, s));
+      LVN_CUDA(cudaMemcpyAsync(thr.p, ws.thresholds.data(), ws.thresholds.size() * 8, cudaMemcpyHostToDevice, s));
       DBuf<u64> deg(n), eoff(n + 1);
-      // out-degree power law (exponent 2.1) scaled to the requested mean
-      const double alpha = 2.1, dmin = 1.0, dmax = 1e5;
-      const double a1 = 1.0 - alpha, a2 = 2.0 - alpha;
-      const double mean_raw = (a1 / a2) * (std::pow(dmax, a2) - std::pow(dmin, a2)) /
-                              (std::pow(dmax, a1) - std::pow(dmin, a1));
-      const double target = g.avg_degree / 2.0 * 1.63;  // undirected samples per vertex (dedupe loss)
-      web_degrees<<<grid(n), 256, 0, s>>>(deg.p, n, alpha, dmin, dmax, target / mean_raw,
-                                          g.seed + 7);
+      web_degrees<<<grid(n), 256, 0, s>>>(deg.p, n, thr.p, u32(ws.thresholds.size()), ws.scale, g.seed + 7);
       LVN_LAUNCH();
       exclusive_scan_u64(deg.p, eoff.p, n, s);
       LVN_CUDA(cudaMemcpyAsync(&edges, eoff.p + n, sizeof(u64), cudaMemcpyDeviceToHost, s));
       LVN_CUDA(cudaStreamSynchronize(s));
       keys.alloc(2 * edges);
-      gen_web<<<grid(n), 256, 0, s>>>(keys.p, eoff.p, n, dlo.p, dhi.p, 0.92, 64, g.seed);
+      gen_web<<<grid(n), 256, 0, s>>>(keys.p, eoff.p, n, dlo.p, dhi.p, kWebLocal, kWebWindow, g.seed);
       LVN_LAUNCH();
       LVN_CUDA(cudaStreamSynchronize(s));
       break;

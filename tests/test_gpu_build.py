@@ -77,3 +77,24 @@ def test_build_rejects_bad_input(lvn):
         lvn.build_csr(3, [0], [1], [float("nan")])
     with pytest.raises(ValueError):
         lvn.build_csr(3, [0], [1], [float("inf")])
+
+
+# the GPU generators (generate.cu) against their host restatement
+# (oracle/gen_host.cpp, what bench.py's reference arm runs on): bit-identical CSRs
+GEN_CASES = [
+    ("rmat", dict(scale=12, edgefactor=16, seed=1)),
+    ("sbm", dict(n=50_000, blocks=50, avg_degree=32, mu=0.1, seed=2)),
+    ("grid", dict(side=300, p=0.6, seed=4)),
+    ("web", dict(n=200_000, avg_degree=75.0, seed=5)),
+    ("uniform", dict(n=20_000, edges=100_000, seed=9)),
+]
+
+
+@pytest.mark.parametrize("kind,kw", GEN_CASES, ids=[c[0] for c in GEN_CASES])
+def test_generate_matches_host_restatement(lvn, ref, kind, kw):
+    dg = lvn.generate(kind, **kw)
+    g = dg.download()
+    dg.close()
+    h = ref.export(ref.generate(kind, **kw))
+    same(g, h)
+    assert g.num_arcs() > 0
