@@ -216,6 +216,15 @@ int lvn_aggregate(const lvn_csr* g, const uint32_t* membership, int membership_l
 int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
                        const double* community_w, double m, const lvn_params* p,
                        int force_kernel, uint32_t* to, double* gain);
+/* The same batched decision through the engine's LIVE ranking path (the
+ * kernels lvn_louvain runs: reciprocal Eq. 2 ranking, Sigma-free may_gain
+ * pruning, community-only sort keys when every arc weight is equal), with the
+ * choice written out instead of applied; gain[u] is the exact Eq. 2 value of
+ * the chosen community (compact_evaluate_move, louvain_compact.cpp:413-445),
+ * rounded to f32 for value_bits 32. Same arguments as lvn_evaluate_moves. */
+int lvn_probe_moves(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
+                    const double* community_w, double m, const lvn_params* p,
+                    int force_kernel, uint32_t* to, double* gain);
 
 /* ---- sharded multi-GPU run -------------------------------
  * One process per GPU, each calling lvn_louvain_sharded on the same graph (its

@@ -150,7 +150,7 @@ EXPORTS = (
     "lvn_init", "lvn_finalize", "lvn_last_error", "lvn_version", "lvn_params_default",
     "lvn_result_free", "lvn_graph_free", "lvn_louvain", "lvn_modularity", "lvn_vertex_weights",
     "lvn_count_communities", "lvn_renumber", "lvn_lookup_dendrogram", "lvn_community_csr",
-    "lvn_aggregate", "lvn_evaluate_moves", "lvn_generate", "lvn_dgraph_upload", "lvn_dgraph_view",
+    "lvn_aggregate", "lvn_evaluate_moves", "lvn_probe_moves", "lvn_generate", "lvn_dgraph_upload", "lvn_dgraph_view",
     "lvn_dgraph_download", "lvn_dgraph_free", "lvn_device_alloc", "lvn_device_free", "lvn_memcpy",
     "lvn_louvain_sharded", "lvn_partition_rows", "lvn_build_csr",
 )
@@ -201,6 +201,8 @@ def lib() -> C.CDLL:
                                 C.POINTER(C.POINTER(lvn_graph_out))]
     L.lvn_build_csr.argtypes = [C.c_uint32, C.c_uint64, vp, vp, vp, i, C.POINTER(C.POINTER(lvn_graph_out))]
     L.lvn_evaluate_moves.argtypes = [C.POINTER(lvn_csr), vp, vp, vp, C.c_double, C.POINTER(lvn_params), i,
+                                     vp, vp]
+    L.lvn_probe_moves.argtypes = [C.POINTER(lvn_csr), vp, vp, vp, C.c_double, C.POINTER(lvn_params), i,
                                      vp, vp]
     L.lvn_generate.argtypes = [C.POINTER(lvn_gen_params), C.POINTER(vp)]
     L.lvn_dgraph_upload.argtypes = [C.POINTER(lvn_csr), C.POINTER(vp)]

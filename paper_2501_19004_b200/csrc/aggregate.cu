@@ -458,7 +458,6 @@ __global__ void __launch_bounds__(kBlockThreads) ag_block(AggArgs x, const u32* 
 //           `count` target communities, the array itself (no keys, no probing:
 //           one reduction per arc; present entries are the ones no longer -0.0).
 // Then one block per community emits the row.
-constexpr u64 kBigChunk = 1024;
 constexpr ull kDenseEmpty = 0x8000000000000000ull;  // -0.0: never produced by adding a weight
 
 struct BigSlot {
@@ -555,78 +554,178 @@ __global__ void ag_big_list(const DGraph g, const u32* __restrict__ vert, const 
   }
 }
 
-// P: exclusive scan of the arc counts of L (nL + 1 entries, P[nL] = all arcs)
-__global__ void __launch_bounds__(256) ag_big_arcs(AggArgs x, const u32* __restrict__ index,
-                                                   const u64* __restrict__ tab_off, unsigned char* tables,
-                                                   u32* __restrict__ live_n, double* __restrict__ own_sum,
-                                                   u32* __restrict__ own_seen, const u32* __restrict__ L,
-                                                   const u64* __restrict__ P, const u32* __restrict__ nL_p,
-                                                   u64 a_lo, u64 a_hi) {
-  const u32 lane = threadIdx.x & 31;
+// P: exclusive scan of the arc counts of L (nL + 1 entries, P[nL] = all arcs).
+//
+// The flat arc space [0, P[nL]) is cut into tiles of kBigTile arcs; tile t's
+// first owner (last i with P[i] <= t kBigTile) comes from big_tile_owner. A
+// block takes one tile at a time:
+//   1. owner metadata of the tile (<= kBigTile members: vertex, community,
+//      region, row base) into smem, one thread per owner, all loads in flight;
+//   2. owner of every arc: head marks + block max-scan over the tile;
+//   3. the tile's targets and weights staged into smem with cp.async
+//      (LDGSTS, 4 B per arc, every copy of the tile in flight before one wait):
+//      the neighbour lists of the members are contiguous CSR segments;
+//   4. C[t] gathers for all staged targets (8 per thread in flight), then per
+//      warp batch of 32 consecutive arcs: own-community weight summed per
+//      lane, the rest pre-combined across the warp and merged into the
+//      community's region (dense fp64 reductions or the 16-byte-slot table).
+// The dependent chain owner -> vertex -> row -> target -> community is paid
+// once per tile instead of once per 32 arcs.
+constexpr u32 kBigTile = 2048;
+constexpr u32 kBigThreads = 256;
+constexpr u32 kBigPer = kBigTile / kBigThreads;
+constexpr size_t kBigSmem = size_t(kBigTile) * (8 + 4 + 4 + 4 + 4 + 2);
+
+__global__ void big_tile_owner(const u64* __restrict__ P, const u32* __restrict__ nL_p, u32* __restrict__ first) {
+  const u64 nL = *nL_p;
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < nL; i += u64(gridDim.x) * blockDim.x) {
+    const u64 p0 = P[i], p1 = P[i + 1];
+    // tiles whose start t * kBigTile falls in [p0, p1): owner i
+    for (u64 t = (p0 + kBigTile - 1) / kBigTile; t * kBigTile < p1; ++t) first[t] = u32(i);
+  }
+}
+
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gmem_src) {
+  const unsigned d = static_cast<unsigned>(__cvta_generic_to_shared(smem_dst));
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(d), "l"(gmem_src) : "memory");
+}
+__device__ __forceinline__ void cp_async_wait_all() {
+  asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
+}
+
+__global__ void __launch_bounds__(kBigThreads) ag_big_arcs(AggArgs x, const u32* __restrict__ index,
+                                                           const u64* __restrict__ tab_off, unsigned char* tables,
+                                                           u32* __restrict__ live_n, double* __restrict__ own_sum,
+                                                           u32* __restrict__ own_seen, const u32* __restrict__ L,
+                                                           const u64* __restrict__ P, const u32* __restrict__ nL_p,
+                                                           const u32* __restrict__ tile_first, u64 a_lo, u64 a_hi) {
+  extern __shared__ __align__(16) unsigned char big_smem[];
+  u64* s_base = reinterpret_cast<u64*>(big_smem);        // owner -> row start - P[i]
+  u32* s_tgt = reinterpret_cast<u32*>(s_base + kBigTile);  // staged targets
+  float* s_w = reinterpret_cast<float*>(s_tgt + kBigTile); // staged weights
+  u32* s_c = reinterpret_cast<u32*>(s_w + kBigTile);       // owner -> community
+  u32* s_pi = s_c + kBigTile;                              // owner -> region index
+  u16* s_own = reinterpret_cast<u16*>(s_pi + kBigTile);    // tile-local owner of each arc
+  __shared__ u32 s_scan[kBigThreads];
+  const u32 tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const u64 nL = *nL_p;
   if (!nL) return;
   const u64 E = min(P[nL], a_hi);
-  const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
-  for (u64 w = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; a_lo + w * kBigChunk < E; w += warps) {
-    const u64 lo = a_lo + w * kBigChunk, hi = min(E, lo + kBigChunk);
-    u64 i0 = last_le(P, nL, lo);  // owner of the chunk's first arc (every vertex of L has arcs)
-    u32 own_pi = ~0u, seen = 0;
-    double own = 0.0;
-    for (u64 b = lo; b < hi; b += 32) {
-      // the batch's <= 32 arcs span <= 32 consecutive L entries from i0:
-      // a 5-step shuffle search over their ends finds each lane's owner
-      const u64 wend = (i0 + lane + 1 <= nL) ? P[i0 + lane + 1] : ~u64(0);
-      const u64 a = b + lane;
-      u32 k = 0;
+  if (a_lo >= E) return;
+  const u64 t_lo = a_lo / kBigTile, t_hi = (E + kBigTile - 1) / kBigTile;
+  u32 own_pi = ~0u, seen = 0;  // per-lane run of the own-community weight
+  double own = 0.0;
+  for (u64 t = t_lo + blockIdx.x; t < t_hi; t += gridDim.x) {
+    const u64 lo = max(t * kBigTile, a_lo), hi = min((t + 1) * kBigTile, E);
+    const u32 nA = u32(hi - lo);
+    // owner of lo: the tile's first owner, or (first tile of a batch) within
+    // the next kBigTile owners (every owner has at least one arc)
+    u64 i0 = tile_first[t];
+    if (lo != t * kBigTile) i0 += last_le(P + i0, min(nL - i0, u64(kBigTile) + 1), lo);
+    // 1. owners: i0 + j while P[i0 + j] < hi
+    for (u32 j = tid; j < kBigTile; j += kBigThreads) s_own[j] = 0;
+    __syncthreads();
+    for (u32 j = tid; j < nA; j += kBigThreads) {
+      const u64 i = i0 + j;
+      if (i >= nL) break;
+      const u64 p = P[i];
+      if (p >= hi) break;
+      const u32 v = L[i];
+      const u32 c = x.C[v];
+      s_c[j] = c;
+      s_pi[j] = index[c];
+      s_base[j] = x.g.off[v] - p;
+      s_own[p > lo ? u32(p - lo) : 0u] = u16(j);
+    }
+    __syncthreads();
+    // 2. owner of each arc: inclusive max-scan of the head marks
+    {
+      u32 run = 0;
+      u16 loc[kBigPer];
 #pragma unroll
-      for (u32 step = 16; step; step >>= 1) {
-        const u64 e = __shfl_sync(0xffffffffu, wend, k + step - 1);
-        if (e <= a) k += step;
+      for (u32 k = 0; k < kBigPer; ++k) {
+        run = max(run, u32(s_own[tid * kBigPer + k]));
+        loc[k] = u16(run);
       }
-      const u64 owner = i0 + k;
-      i0 += __shfl_sync(0xffffffffu, k, 31);
-      u32 key = kEmpty, c = 0, pi = 0;
+      u32 incl = run;
+#pragma unroll
+      for (u32 d = 1; d < 32; d <<= 1) {
+        const u32 o = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl = max(incl, o);
+      }
+      if (lane == 31) s_scan[wid] = incl;
+      __syncthreads();
+      u32 carry = 0;
+      for (u32 w = 0; w < wid; ++w) carry = max(carry, s_scan[w]);
+      const u32 prev = __shfl_up_sync(0xffffffffu, incl, 1);
+      carry = max(carry, lane ? prev : 0u);
+#pragma unroll
+      for (u32 k = 0; k < kBigPer; ++k) s_own[tid * kBigPer + k] = u16(max(carry, u32(loc[k])));
+    }
+    __syncthreads();
+    // 3. stage targets and weights (cp.async, every copy in flight)
+#pragma unroll
+    for (u32 k = 0; k < kBigPer; ++k) {
+      const u32 e = k * kBigThreads + tid;
+      if (e < nA) {
+        const u64 ga = s_base[s_own[e]] + lo + e;
+        cp_async4(&s_tgt[e], x.g.tgt + ga);
+        cp_async4(&s_w[e], x.g.w + ga);
+      }
+    }
+    cp_async_wait_all();
+    __syncthreads();
+    // 4. communities of the targets, then merge per warp batch
+    u32 key[kBigPer];
+#pragma unroll
+    for (u32 k = 0; k < kBigPer; ++k) {
+      const u32 e = k * kBigThreads + wid * 32 + lane;
+      key[k] = e < nA ? x.C[s_tgt[e]] : kEmpty;
+    }
+#pragma unroll
+    for (u32 k = 0; k < kBigPer; ++k) {
+      const u32 e = k * kBigThreads + wid * 32 + lane;
+      u32 kk = key[k], c = 0, pi = 0;
       double wt = 0.0;
-      if (a < hi) {
-        const u32 v = L[owner];
-        c = x.C[v];
-        pi = index[c];
-        const u64 ga = x.g.off[v] + (a - P[owner]);
-        key = x.C[__ldcs(x.g.tgt + ga)];
-        wt = double(__ldcs(x.g.w + ga));
-        if (key == c) {
+      if (e < nA) {
+        const u32 o = s_own[e];
+        c = s_c[o];
+        pi = s_pi[o];
+        wt = double(s_w[e]);
+        if (kk == c) {
           if (pi != own_pi) {
             if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
             own_pi = pi, own = 0.0;
           }
           own += wt;
           seen = 1;
-          key = kEmpty;
+          kk = kEmpty;
         }
       }
       // a batch inside one community (the usual case): one merge per distinct key
-      const u32 phi = __reduce_max_sync(0xffffffffu, key != kEmpty ? pi : 0u);
-      const u32 plo = __reduce_min_sync(0xffffffffu, key != kEmpty ? pi : ~0u);
+      const u32 phi = __reduce_max_sync(0xffffffffu, kk != kEmpty ? pi : 0u);
+      const u32 plo = __reduce_min_sync(0xffffffffu, kk != kEmpty ? pi : ~0u);
       if (phi == plo) {
-        const u32 cc = __reduce_max_sync(0xffffffffu, key != kEmpty ? c : 0u);
-        if (!warp_combine(key, wt, lane)) continue;
+        const u32 cc = __reduce_max_sync(0xffffffffu, kk != kEmpty ? c : 0u);
+        if (!warp_combine(kk, wt, lane)) continue;
         c = cc, pi = phi;
-      } else if (key == kEmpty) {
+      } else if (kk == kEmpty) {
         continue;
       }
       const u64 hcap = x.hoff[c + 1] - x.hoff[c];
       unsigned char* base = tables + tab_off[pi];
       if (big_dense(hcap, x.count, x.big_mode)) {
-        atomicAdd(reinterpret_cast<double*>(base) + key, wt);
+        atomicAdd(reinterpret_cast<double*>(base) + kk, wt);
       } else {
         const u64 slots = big_slots(hcap);
         bool fresh;
-        const u32 sl = big_insert(reinterpret_cast<BigSlot*>(base), slots, key, wt, fresh);
+        const u32 sl = big_insert(reinterpret_cast<BigSlot*>(base), slots, kk, wt, fresh);
         if (fresh) reinterpret_cast<u32*>(base + slots * sizeof(BigSlot))[atomicAdd(&live_n[pi], 1u)] = sl;
       }
     }
-    if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
+    __syncthreads();  // the stage is rewritten by the next tile
   }
+  if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
 }
 
 // present entries of the dense regions, all regions' chunks spread over the
@@ -827,7 +926,22 @@ void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
     ag_big_list<<<mg, 256, 0, s>>>(a.g, vert.p, keep.p, kpos.p, M, L.p, D.p);
     LVN_LAUNCH();
     exclusive_scan_u32_to_u64(D.p, P.p, M, s);
-    static const int occ = occupancy(ag_big_arcs, 256, 0);
+    // first owner of every kBigTile-arc tile of the flat arc space; the arc
+    // total P[nL] is read back once (the batches below need it anyway)
+    u32 nL32 = 0;
+    LVN_CUDA(cudaMemcpyAsync(&nL32, kpos.p + M, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    u64 total_arcs = 0;
+    LVN_CUDA(cudaMemcpyAsync(&total_arcs, P.p + nL32, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    const u64 nL = nL32;
+    const u64 ntiles = total_arcs / kBigTile + 1;
+    DBuf<u32> tile_first(ntiles);
+    LVN_CUDA(cudaMemsetAsync(tile_first.p, 0, ntiles * sizeof(u32), s));
+    big_tile_owner<<<unsigned(std::min<u64>((nL + 255) / 256 + 1, u64(sms) * 8)), 256, 0, s>>>(P.p, kpos.p + M,
+                                                                                               tile_first.p);
+    LVN_LAUNCH();
+    static const int occ = occupancy(ag_big_arcs, kBigThreads, kBigSmem);
     for (size_t bi = 0; bi + 1 < cuts.size(); ++bi) {
       const u64 b0 = cuts[bi], b1 = cuts[bi + 1], nb = b1 - b0;
       if (!nb) continue;
@@ -847,8 +961,9 @@ void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
         LVN_CUDA(cudaMemcpyAsync(&arc_hi, P.p + k[1], sizeof(u64), cudaMemcpyDeviceToHost, s));
         LVN_CUDA(cudaStreamSynchronize(s));
       }
-      ag_big_arcs<<<unsigned(u64(sms) * occ), 256, 0, s>>>(a, index.p, tab_off.p, base, live_n.p, own.p,
-                                                            own_seen.p, L.p, P.p, kpos.p + M, arc_lo, arc_hi);
+      ag_big_arcs<<<unsigned(u64(sms) * occ), kBigThreads, kBigSmem, s>>>(a, index.p, tab_off.p, base, live_n.p, own.p,
+                                                                    own_seen.p, L.p, P.p, kpos.p + M, tile_first.p,
+                                                                    arc_lo, arc_hi);
       LVN_LAUNCH();
       ag_dense_scan<<<unsigned(u64(sms) * 8), 256, 0, s>>>(a, big + b0, nb, tab_off.p + b0, base, live_n.p + b0);
       LVN_LAUNCH();

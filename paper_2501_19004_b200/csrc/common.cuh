@@ -17,6 +17,7 @@
 namespace lvn {
 
 using u8 = std::uint8_t;
+using u16 = std::uint16_t;
 using u32 = std::uint32_t;
 using u64 = std::uint64_t;
 using ull = unsigned long long;

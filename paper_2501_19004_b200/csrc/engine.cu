@@ -42,12 +42,26 @@ void Pool::bind(int device, cudaStream_t s) {
   total_ = total_b;
 }
 
+// Device memory this pool can still hand out: the driver's free memory (which
+// sees the CUDA context, borrowed caller buffers and other processes sharing
+// the GPU) plus the blocks cached here, minus a 1 GB margin, capped by the
+// pool's own accounting. Callers query it right after a stream
+// synchronisation (cudaMemGetInfo stalls while kernels are in flight).
 size_t Pool::available() {
   std::uint64_t used = 0;
   (void)cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemCurrent, &used);
   size_t cached = 0;
   for (auto& kv : big_free_) cached += kv.first;
-  return used + (size_t(1) << 30) < total_ + cached ? total_ + cached - used - (size_t(1) << 30) : 0;
+  const size_t margin = size_t(1) << 30;
+  size_t est = used + margin < total_ + cached ? total_ + cached - used - margin : 0;
+  size_t free_b = 0, total_b = 0;
+  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
+    const size_t drv = free_b + cached > margin ? free_b + cached - margin : 0;
+    est = std::min(est, drv);
+  } else {
+    (void)cudaGetLastError();
+  }
+  return est;
 }
 
 void* Pool::raw(size_t bytes) {
@@ -425,19 +439,19 @@ __host__ __device__ inline u64 split_target(u64 A, int parts, int k) {
   return A / u64(parts) * u64(k) + (A % u64(parts)) * u64(k) / u64(parts);
 }
 __global__ void split_rows_k(const u64* __restrict__ off, u32 n, int parts, u32* __restrict__ bounds) {
-  const int k = threadIdx.x;
-  if (k > parts) return;
-  if (k == parts) {
-    bounds[k] = n;
-    return;
+  for (int k = threadIdx.x; k <= parts; k += blockDim.x) {
+    if (k == parts) {
+      bounds[k] = n;
+      continue;
+    }
+    const u64 target = split_target(off[n], parts, k);
+    u32 lo = 0, hi = n;
+    while (lo < hi) {
+      const u32 mid = lo + (hi - lo) / 2;
+      if (off[mid] >= target) hi = mid; else lo = mid + 1;
+    }
+    bounds[k] = lo;
   }
-  const u64 target = split_target(off[n], parts, k);
-  u32 lo = 0, hi = n;
-  while (lo < hi) {
-    const u32 mid = lo + (hi - lo) / 2;
-    if (off[mid] >= target) hi = mid; else lo = mid + 1;
-  }
-  bounds[k] = lo;
 }
 std::vector<u32> split_rows(const u64* off, u32 n, int parts, cudaStream_t s) {
   DBuf<u32> b(parts + 1);
@@ -1094,10 +1108,9 @@ void lvn_result_free(lvn_result* r) {
   if (!r) return;
   if (r->membership) {
     if (r->membership_on_device) {
-      try {
-        ctx().pool.put(r->membership);
-      } catch (...) {
-      }
+      // through guard(): the context mutex serialises the pool against calls
+      // running on other threads (ctypes releases the GIL), on the right device
+      (void)guard([&](Context& c) { c.pool.put(r->membership); });
     } else if (!(lvn::g_ctx && lvn::g_ctx->host.put(r->membership))) {
       (void)cudaFreeHost(r->membership);  // pinned block that outlived its context
     }
@@ -1405,9 +1418,12 @@ int lvn_aggregate(const lvn_csr* g, const uint32_t* membership, int membership_l
   return kOk;
 }
 
-int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
-                       const double* community_w, double m, const lvn_params* p, int force_kernel,
-                       uint32_t* to, double* gain) {
+namespace lvn {
+namespace {
+// lvn_evaluate_moves (probe = false) and lvn_probe_moves (probe = true)
+int evaluate_moves_impl(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
+                        const double* community_w, double m, const lvn_params* p, int force_kernel,
+                        uint32_t* to, double* gain, bool probe) {
   return guard([&](Context& c) {
     lvn_params def;
     lvn_params_default(&def);
@@ -1449,7 +1465,23 @@ int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const doubl
     a.K = K.p;
     a.sigma = S.p;
     a.m = m;
-    a.dry = 1;
+    a.dry = probe ? 0 : 1;
+    a.probe = probe ? 1 : 0;
+    a.value_f32 = pp.value_bits == 32 ? 1 : 0;
+    a.prune = 0;
+    DBuf<u8> flags(n ? n : 1);
+    a.flags = flags.p;
+    if (probe && n) {
+      // uniform-weight detection exactly as the pass reset does it (scratch K,
+      // Sigma, C; only the flag is kept)
+      DBuf<double> k2(n), s2(n);
+      DBuf<u32> c2(n), uni(1);
+      pass_reset(ig.g, b, k2.p, s2.p, c2.p, flags.p, s, uni.p);
+      if (ig.g.arcs && !no_uniform() && read_scalar(uni.p, s) != 0) {
+        a.uniform = 1;
+        a.uniform_w = read_scalar(ig.g.w, s);
+      }
+    }
     a.out_to = ot.p;
     a.out_gain = og.p;
     a.gain_acc = &rec.p->gain;
@@ -1467,6 +1499,20 @@ int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const doubl
     }
     LVN_CUDA(cudaStreamSynchronize(s));
   });
+}
+}  // namespace
+}  // namespace lvn
+
+int lvn_evaluate_moves(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
+                       const double* community_w, double m, const lvn_params* p, int force_kernel,
+                       uint32_t* to, double* gain) {
+  return lvn::evaluate_moves_impl(g, membership, vertex_w, community_w, m, p, force_kernel, to, gain, false);
+}
+
+int lvn_probe_moves(const lvn_csr* g, const uint32_t* membership, const double* vertex_w,
+                    const double* community_w, double m, const lvn_params* p, int force_kernel,
+                    uint32_t* to, double* gain) {
+  return lvn::evaluate_moves_impl(g, membership, vertex_w, community_w, m, p, force_kernel, to, gain, true);
 }
 
 // ---- device-resident graphs ----------------------------------------------------

@@ -85,6 +85,11 @@ struct MoveArgs {
   int pickless = 0;
   int prune = 1;
   int dry = 0;              // evaluate only: write out_to / out_gain, apply nothing
+  // probe (lvn_probe_moves): the live kernels (the engine's ranking: reciprocal
+  // Eq. 2, may_gain pruning, community-only keys on uniform weights) with the
+  // decision written to out_to / out_gain instead of applied
+  int probe = 0;
+  int value_f32 = 1;        // probe: round the reported gain to f32 like the V = float table
   u32* out_to = nullptr;
   double* out_gain = nullptr;
   double* gain_acc = nullptr;  // summed gain of applied moves

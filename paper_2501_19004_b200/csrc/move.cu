@@ -125,6 +125,14 @@ __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, doubl
     x.out_gain[u] = mv ? bg : 0.0;
     return false;
   }
+  if (x.probe) {  // report the live ranking's choice with the reference's exact gain
+    const double ge = mv ? delta_q(bk, own, ku, x.sigma[bc], x.sigma[from], x.m) : 0.0;
+    const double gr = x.value_f32 ? double(float(ge)) : ge;
+    mv = mv && gr > 0.0;
+    x.out_to[u] = mv ? bc : from;
+    x.out_gain[u] = mv ? gr : 0.0;
+    return false;
+  }
   if (mv && x.pickless && bc > from) mv = false;
   // singleton pairs: two singletons that pick each other would swap labels
   // instead of merging when they decide concurrently; only the move toward

@@ -531,9 +531,11 @@ def build_csr(num_vertices: int, sources, targets, weights=None, symmetrize: boo
 
 
 def evaluate_moves(g, membership, vertex_w, community_w, m: float, options: CompactOptions | None = None,
-                   force_kernel: int = -1):
+                   force_kernel: int = -1, live: bool = False):
     """Decision of every vertex on one fixed snapshot, nothing applied
-    (compact_evaluate_move, louvain_compact.hpp:65-72, batched)."""
+    (compact_evaluate_move, louvain_compact.hpp:65-72, batched). live=True runs
+    the engine's own ranking kernels (lvn_probe_moves) instead of the
+    reference-order evaluation."""
     memb = _u32(membership)
     kw = np.ascontiguousarray(vertex_w, dtype=np.float64)
     cw = np.ascontiguousarray(community_w, dtype=np.float64)
@@ -542,8 +544,9 @@ def evaluate_moves(g, membership, vertex_w, community_w, m: float, options: Comp
     gain = np.empty(max(n, 1), np.float64)
     p = _params(None, options)
     csr = g._csr()
-    _check(N.lib().lvn_evaluate_moves(C.byref(csr), memb.ctypes.data, kw.ctypes.data, cw.ctypes.data, float(m),
-                                      C.byref(p), int(force_kernel), to.ctypes.data, gain.ctypes.data))
+    fn = N.lib().lvn_probe_moves if live else N.lib().lvn_evaluate_moves
+    _check(fn(C.byref(csr), memb.ctypes.data, kw.ctypes.data, cw.ctypes.data, float(m),
+              C.byref(p), int(force_kernel), to.ctypes.data, gain.ctypes.data))
     return to[:n], gain[:n]
 
 

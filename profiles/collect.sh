@@ -16,8 +16,8 @@ timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv \
 # 3. dram traffic of every local-moving launch of one Louvain run
 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum \
   --clock-control none -k regex:'^lm_' --csv --log-file gpurun_out/move_traffic_$cfg.csv \
-  python tests/_prof.py "$cfg" 1 > gpurun_out/move_traffic_$cfg.log 2>&1
+  python profiles/prof_run.py "$cfg" 1 > gpurun_out/move_traffic_$cfg.log 2>&1
 # 4. full capture of the dominant local-moving kernels (first iteration of pass 0)
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:'^lm_p?sort' -c 6 \
-  -o gpurun_out/prof_lm_sort_$cfg -f python tests/_prof.py "$cfg" 1 > gpurun_out/prof_lm_sort_$cfg.log 2>&1
+  -o gpurun_out/prof_lm_sort_$cfg -f python profiles/prof_run.py "$cfg" 1 > gpurun_out/prof_lm_sort_$cfg.log 2>&1
 echo done

@@ -19,4 +19,4 @@ M=$M,smsp__average_warps_issue_stalled_drain_per_issue_active.ratio
 M=$M,smsp__average_warps_issue_stalled_branch_resolving_per_issue_active.ratio
 M=$M,smsp__thread_inst_executed_per_inst_executed.ratio
 timeout 900 ncu --metrics $M --clock-control none -k regex:"$rx" --csv --log-file "$out" \
-  python tests/_prof.py "$cfg" 1 > "${out%.csv}.log" 2>&1
+  python profiles/prof_run.py "$cfg" 1 > "${out%.csv}.log" 2>&1

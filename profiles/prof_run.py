@@ -1,6 +1,7 @@
 """Profiling driver (run under ncu on the GPU box): one warm-up and N runs of a config."""
 import sys
-sys.path.insert(0, '.')
+import os
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2501_19004_b200 as lvn
 from bench import CONFIGS
 cfg = sys.argv[1] if len(sys.argv) > 1 else "c2"

@@ -21,7 +21,7 @@ def declared_symbols():
 
 def test_header_declares_the_boundary():
     syms = declared_symbols()
-    for s in ("lvn_louvain", "lvn_modularity", "lvn_aggregate", "lvn_evaluate_moves", "lvn_renumber",
+    for s in ("lvn_louvain", "lvn_modularity", "lvn_aggregate", "lvn_evaluate_moves", "lvn_probe_moves", "lvn_renumber",
               "lvn_lookup_dendrogram", "lvn_community_csr", "lvn_count_communities", "lvn_init",
               "lvn_finalize", "lvn_last_error", "lvn_result_free"):
         assert s in syms

@@ -227,12 +227,12 @@ def test_aggregate_planted(lvn, port):
 
 
 # ------------------------------------------------------------ move decisions
-def decisions_equal(lvn, port, g, memb, force=-1, value_bits=64):
+def decisions_equal(lvn, port, g, memb, force=-1, value_bits=64, live=False):
     kw = port.vertex_weights(g)
     cw = np.zeros(g.n)
     np.add.at(cw, memb, kw)
     opts = lvn.CompactOptions(value_bits=value_bits)
-    to, gain = lvn.evaluate_moves(G_(g, lvn), memb, kw, cw, g.total_weight, opts, force)
+    to, gain = lvn.evaluate_moves(G_(g, lvn), memb, kw, cw, g.total_weight, opts, force, live)
     for u in range(g.n):
         want = port.evaluate_move(g, memb, kw, cw, g.total_weight, u, value_bits)
         assert (int(to[u]), float(gain[u])) == want, (u, g.offsets[u + 1] - g.offsets[u])
@@ -259,6 +259,28 @@ def test_decisions_every_kernel_class(lvn, port, force, value_bits):
     g = random_graph(600, 6000, 11 + force, 1.0, 6.0, True, True)
     memb = random_membership(g.n, 40, 3)
     decisions_equal(lvn, port, g, memb, force, value_bits)
+
+
+@pytest.mark.parametrize("force", [-1, 1, 2, 3, 4])
+@pytest.mark.parametrize("value_bits", [32, 64])
+@pytest.mark.parametrize("unit", [True, False])
+def test_live_decisions_every_kernel_class(lvn, port, force, value_bits, unit):
+    # the engine's own ranking path (lvn_probe_moves: reciprocal Eq. 2,
+    # may_gain pruning, community-only keys on unit weights) must pick what
+    # compact_evaluate_move picks, with the reference's exact gain
+    g = random_graph(600, 6000, 31 + force, 1.0, 1.0 if unit else 6.0, True, True)
+    for k in (40, 300):
+        memb = random_membership(g.n, k, 5 + k)
+        decisions_equal(lvn, port, g, memb, force, value_bits, live=True)
+
+
+@pytest.mark.parametrize("value_bits", [32, 64])
+def test_live_decisions_hubs_and_planted(lvn, port, value_bits):
+    g = hubs_graph(25000, 5, 20000, 60000, 3)
+    decisions_equal(lvn, port, g, random_membership(g.n, 300, 9), -1, value_bits, live=True)
+    g = planted(20000, 50, 24, 0.1, 4)  # unit weights: community-only keys
+    decisions_equal(lvn, port, g, (np.arange(g.n) // 400).astype(np.uint32), -1, value_bits, live=True)
+    decisions_equal(lvn, port, g, np.arange(g.n, dtype=np.uint32), -1, value_bits, live=True)
 
 
 def test_decisions_hub(lvn, port):
