@@ -445,19 +445,26 @@ __global__ void __launch_bounds__(kBlockThreads) ag_block(AggArgs x, const u32* 
 
 // ---- communities with budget > block_max: arc-parallel ---------------------------
 // The members of the big communities (grouped by community, vertices without
-// arcs dropped) form a list L whose arcs are cut into fixed chunks of kBigChunk
-// arcs, one chunk per warp task: a hub row is split across many warps and the
-// warps of one community run together, so its HBM region stays hot in L2. The
-// weight to the community itself (the super-vertex self-loop, usually the
-// dominant key) is summed per lane while the lane stays in one community and
-// added once per run; the other arcs are pre-combined across the warp and
-// merged into the community's region:
+// arcs dropped) form a list L whose arcs are cut into tiles (ag_big_arcs): a
+// hub row is split across many blocks and the blocks of one community run
+// together, so its HBM region stays hot in L2. The weight to the community
+// itself (the super-vertex self-loop, usually the dominant key) is summed per
+// lane while the lane stays in one community and added once per run; the
+// other arcs are pre-combined across the warp and merged into the
+// community's region:
 //   hash  : 16-byte slots {key, fp64 value} (one sector per probe), claimed by
 //           CAS (one L2 round trip per probe), fp64 L2 reductions, a live list;
 //   dense : when the hash table would outgrow a dense fp64 array over all
 //           `count` target communities, the array itself (no keys, no probing:
 //           one reduction per arc; present entries are the ones no longer -0.0).
 // Then one block per community emits the row.
+//
+// Region sizes: a region holds the community's holey capacity min(ext + 1,
+// count) keys (ext: its arcs to other communities, counted by external_arcs),
+// which bounds its distinct targets, at load <= 1/2. Inserts still check for
+// a full region (live list full, or a probe sequence wrapping): a flagged
+// community stops inserting and is redone in a second round sized by the arcs
+// it counted there (a guard: with exact capacities it does not trigger).
 constexpr ull kDenseEmpty = 0x8000000000000000ull;  // -0.0: never produced by adding a weight
 
 struct BigSlot {
@@ -466,26 +473,24 @@ struct BigSlot {
   double val;
 };
 
-__device__ __forceinline__ u64 big_slots(u64 hcap) {
-  const u32 l = ceil_log2_u64(2 * (hcap ? hcap : 1));
-  return u64(1) << (l > 5 ? l : 5);
+// slots of a hash region for `keys` expected keys (load <= 1/2), or 0 for dense
+__device__ __forceinline__ u64 big_region_slots(u64 keys, u32 count, int mode) {
+  const u32 l = ceil_log2_u64(2 * (keys ? keys : 1));
+  const u64 slots = u64(1) << (l > 5 ? l : 5);
+  const bool dense = mode ? mode == 2 : slots * sizeof(BigSlot) >= u64(count) * sizeof(double);
+  return dense ? 0 : slots;
 }
-__device__ __forceinline__ bool big_dense(u64 hcap, u32 count, int mode) {
-  if (mode) return mode == 2;
-  return big_slots(hcap) * sizeof(BigSlot) >= u64(count) * sizeof(double);
-}
-__device__ __forceinline__ u64 big_region_bytes(u64 hcap, u32 count, int mode) {
-  if (big_dense(hcap, count, mode)) return (u64(count) * sizeof(double) + 15) & ~u64(15);
-  const u64 slots = big_slots(hcap);
+__device__ __forceinline__ u64 big_region_bytes(u64 slots, u32 count) {
+  if (!slots) return (u64(count) * sizeof(double) + 15) & ~u64(15);
   return (slots * sizeof(BigSlot) + slots / 2 * 4 + 15) & ~u64(15);
 }
-// claim-or-find by CAS (one round trip per probe); returns the slot, and
-// whether this call claimed it
+// claim-or-find by CAS (one round trip per probe); returns the slot and
+// whether this call claimed it, or ~0u when the probe sequence wraps (full)
 __device__ __forceinline__ u32 big_insert(BigSlot* t, u64 slots, u32 key, double w, bool& fresh) {
   const u32 lg = ceil_log2_u64(slots);
   const u32 mask = u32(slots - 1);
   u32 h = slot_hash(key, lg);
-  while (true) {
+  for (u64 probe = 0; probe < slots; ++probe) {
     const u32 cur = atomicCAS(&t[h].key, kEmpty, key);
     if (cur == kEmpty || cur == key) {
       atomicAdd(&t[h].val, w);
@@ -494,6 +499,8 @@ __device__ __forceinline__ u32 big_insert(BigSlot* t, u64 slots, u32 key, double
     }
     h = (h + 1) & mask;
   }
+  fresh = false;
+  return ~0u;
 }
 // largest i in [0, n) with p[i] <= x (p ascending, p[0] <= x)
 __device__ __forceinline__ u64 last_le(const u64* __restrict__ p, u64 n, u64 x) {
@@ -505,29 +512,33 @@ __device__ __forceinline__ u64 last_le(const u64* __restrict__ p, u64 n, u64 x) 
   return lo;
 }
 
-__global__ void ag_big_plan(const u32* __restrict__ big, u64 nbig, u32 count, int mode, const u64* __restrict__ hoff,
-                            const u64* __restrict__ coff, u32* __restrict__ index, u64* __restrict__ bytes,
-                            u32* __restrict__ mcount) {
+// round 1 (ext_c == nullptr): estimated region sizes; round 2: sized by the
+// community's arcs to other communities counted in round 1 (>= its keys)
+__global__ void ag_big_plan(const u32* __restrict__ big, u64 nbig, u32 count, int mode,
+                            const u64* __restrict__ ext_c, const u64* __restrict__ hoff,
+                            const u64* __restrict__ boff, const u64* __restrict__ coff, u32* __restrict__ index,
+                            u64* __restrict__ rslots, u64* __restrict__ bytes, u32* __restrict__ mcount) {
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < nbig; i += u64(gridDim.x) * blockDim.x) {
     const u32 c = big[i];
     index[c] = u32(i);
-    bytes[i] = big_region_bytes(hoff[c + 1] - hoff[c], count, mode);
+    const u64 hcap = hoff[c + 1] - hoff[c];
+    const u64 sl = big_region_slots(ext_c ? min(hcap, ext_c[c] + 1) : hcap, count, mode);
+    rslots[i] = sl;
+    bytes[i] = big_region_bytes(sl, count);
     mcount[i] = u32(coff[c + 1] - coff[c]);
   }
 }
 
-__global__ void ag_big_clear(const u32* __restrict__ big, u64 nbig, u32 count, int mode, const u64* __restrict__ hoff,
+__global__ void ag_big_clear(u64 nbig, u32 count, const u64* __restrict__ rslots,
                              const u64* __restrict__ tab_off, unsigned char* tables) {
   for (u64 i = blockIdx.x; i < nbig; i += gridDim.x) {
-    const u32 c = big[i];
-    const u64 hcap = hoff[c + 1] - hoff[c];
     unsigned char* base = tables + tab_off[i];
-    if (big_dense(hcap, count, mode)) {
+    const u64 slots = rslots[i];
+    if (!slots) {
       ull* d = reinterpret_cast<ull*>(base);
       for (u64 j = threadIdx.x; j < count; j += blockDim.x) d[j] = kDenseEmpty;
     } else {
       BigSlot* t = reinterpret_cast<BigSlot*>(base);
-      const u64 slots = big_slots(hcap);
       for (u64 j = threadIdx.x; j < slots; j += blockDim.x) t[j] = BigSlot{kEmpty, 0u, 0.0};
     }
   }
@@ -553,6 +564,20 @@ __global__ void ag_big_list(const DGraph g, const u32* __restrict__ vert, const 
     D[kpos[j]] = u32(g.off[v + 1] - g.off[v]);
   }
 }
+
+// Per-round state of the big path, indexed by the position of a community in
+// the round's list.
+struct BigState {
+  const u32* index;     // community -> position
+  const u64* rslots;    // position -> hash slots (0: dense region)
+  const u64* tab_off;   // position -> byte offset of its region
+  unsigned char* tables;
+  u32* live_n;          // live entries (hash) / emitted entries (dense)
+  double* own_sum;      // weight to the community itself
+  u32* own_seen;
+  u32* ovf;             // region overflowed: redone in round 2
+  u64* ext;             // arcs to other communities (round 2 sizes regions by it)
+};
 
 // P: exclusive scan of the arc counts of L (nL + 1 entries, P[nL] = all arcs).
 //
@@ -593,10 +618,7 @@ __device__ __forceinline__ void cp_async_wait_all() {
   asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;\n" ::: "memory");
 }
 
-__global__ void __launch_bounds__(kBigThreads) ag_big_arcs(AggArgs x, const u32* __restrict__ index,
-                                                           const u64* __restrict__ tab_off, unsigned char* tables,
-                                                           u32* __restrict__ live_n, double* __restrict__ own_sum,
-                                                           u32* __restrict__ own_seen, const u32* __restrict__ L,
+__global__ void __launch_bounds__(kBigThreads) ag_big_arcs(AggArgs x, BigState st, const u32* __restrict__ L,
                                                            const u64* __restrict__ P, const u32* __restrict__ nL_p,
                                                            const u32* __restrict__ tile_first, u64 a_lo, u64 a_hi) {
   extern __shared__ __align__(16) unsigned char big_smem[];
@@ -633,7 +655,7 @@ __global__ void __launch_bounds__(kBigThreads) ag_big_arcs(AggArgs x, const u32*
       const u32 v = L[i];
       const u32 c = x.C[v];
       s_c[j] = c;
-      s_pi[j] = index[c];
+      s_pi[j] = st.index[c];
       s_base[j] = x.g.off[v] - p;
       s_own[p > lo ? u32(p - lo) : 0u] = u16(j);
     }
@@ -694,7 +716,7 @@ __global__ void __launch_bounds__(kBigThreads) ag_big_arcs(AggArgs x, const u32*
         wt = double(s_w[e]);
         if (kk == c) {
           if (pi != own_pi) {
-            if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
+            if (seen) atomicAdd(&st.own_sum[own_pi], own), st.own_seen[own_pi] = 1;
             own_pi = pi, own = 0.0;
           }
           own += wt;
@@ -706,43 +728,50 @@ __global__ void __launch_bounds__(kBigThreads) ag_big_arcs(AggArgs x, const u32*
       const u32 phi = __reduce_max_sync(0xffffffffu, kk != kEmpty ? pi : 0u);
       const u32 plo = __reduce_min_sync(0xffffffffu, kk != kEmpty ? pi : ~0u);
       if (phi == plo) {
-        const u32 cc = __reduce_max_sync(0xffffffffu, kk != kEmpty ? c : 0u);
+        const u32 next = __popc(__ballot_sync(0xffffffffu, kk != kEmpty));
+        if (lane == 0 && next) atomicAdd(reinterpret_cast<ull*>(&st.ext[phi]), ull(next));
         if (!warp_combine(kk, wt, lane)) continue;
-        c = cc, pi = phi;
+        pi = phi;
       } else if (kk == kEmpty) {
         continue;
-      }
-      const u64 hcap = x.hoff[c + 1] - x.hoff[c];
-      unsigned char* base = tables + tab_off[pi];
-      if (big_dense(hcap, x.count, x.big_mode)) {
-        atomicAdd(reinterpret_cast<double*>(base) + kk, wt);
       } else {
-        const u64 slots = big_slots(hcap);
+        atomicAdd(reinterpret_cast<ull*>(&st.ext[pi]), 1ull);
+      }
+      unsigned char* base = st.tables + st.tab_off[pi];
+      const u64 slots = st.rslots[pi];
+      if (!slots) {
+        atomicAdd(reinterpret_cast<double*>(base) + kk, wt);
+      } else if (!*reinterpret_cast<volatile u32*>(&st.ovf[pi])) {
         bool fresh;
         const u32 sl = big_insert(reinterpret_cast<BigSlot*>(base), slots, kk, wt, fresh);
-        if (fresh) reinterpret_cast<u32*>(base + slots * sizeof(BigSlot))[atomicAdd(&live_n[pi], 1u)] = sl;
+        if (sl == ~0u) {
+          st.ovf[pi] = 1;
+        } else if (fresh) {
+          const u32 at = atomicAdd(&st.live_n[pi], 1u);
+          if (at < slots / 2) reinterpret_cast<u32*>(base + slots * sizeof(BigSlot))[at] = sl;
+          else st.ovf[pi] = 1;
+        }
       }
     }
     __syncthreads();  // the stage is rewritten by the next tile
   }
-  if (seen) atomicAdd(&own_sum[own_pi], own), own_seen[own_pi] = 1;
+  if (seen) atomicAdd(&st.own_sum[own_pi], own), st.own_seen[own_pi] = 1;
 }
 
 // present entries of the dense regions, all regions' chunks spread over the
 // whole grid (one block per region left most SMs idle on few giant
 // communities): warp-compacted appends to the region's row (live_n counts)
 constexpr u64 kDenseChunk = 16384;
-__global__ void __launch_bounds__(256) ag_dense_scan(AggArgs x, const u32* __restrict__ big, u64 nbig,
-                                                     const u64* __restrict__ tab_off, const unsigned char* tables,
-                                                     u32* __restrict__ live_n) {
+__global__ void __launch_bounds__(256) ag_dense_scan(AggArgs x, BigState st, const u32* __restrict__ big,
+                                                     u64 nbig) {
   const u64 cpc = (u64(x.count) + kDenseChunk - 1) / kDenseChunk;
   const u32 lane = threadIdx.x & 31;
   for (u64 q = blockIdx.x; q < nbig * cpc; q += gridDim.x) {
     const u64 i = q / cpc, j0 = (q % cpc) * kDenseChunk;
+    if (st.rslots[i]) continue;
     const u32 c = big[i];
     const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
-    if (!big_dense(hcap, x.count, x.big_mode)) continue;
-    const ull* d = reinterpret_cast<const ull*>(tables + tab_off[i]);
+    const ull* d = reinterpret_cast<const ull*>(st.tables + st.tab_off[i]);
     const u64 j1 = min(j0 + kDenseChunk, u64(x.count));
     for (u64 b = j0; b < j1; b += blockDim.x) {
       const u64 j = b + threadIdx.x;
@@ -750,7 +779,7 @@ __global__ void __launch_bounds__(256) ag_dense_scan(AggArgs x, const u32* __res
       const bool live = bits != kDenseEmpty;
       const u32 bal = __ballot_sync(0xffffffffu, live);
       u32 wbase = 0;
-      if (lane == 0 && bal) wbase = atomicAdd(&live_n[i], __popc(bal));
+      if (lane == 0 && bal) wbase = atomicAdd(&st.live_n[i], __popc(bal));
       wbase = __shfl_sync(0xffffffffu, wbase, 0);
       if (live) {
         const u32 o = wbase + __popc(bal & ((1u << lane) - 1u));
@@ -763,24 +792,20 @@ __global__ void __launch_bounds__(256) ag_dense_scan(AggArgs x, const u32* __res
   }
 }
 
-__global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, const u32* __restrict__ big, u64 nbig,
-                                                             const u64* __restrict__ tab_off,
-                                                             unsigned char* tables, u32* __restrict__ live_n,
-                                                             const double* __restrict__ own_sum,
-                                                             const u32* __restrict__ own_seen) {
+// rows of the regions that did not overflow (the others are redone in round 2)
+__global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, BigState st, const u32* __restrict__ big,
+                                                             u64 nbig) {
   for (u64 i = blockIdx.x; i < nbig; i += gridDim.x) {
+    if (st.ovf[i]) continue;
     const u32 c = big[i];
     const u64 hbase = x.hoff[c], hcap = x.hoff[c + 1] - hbase;
-    unsigned char* base = tables + tab_off[i];
-    const u32 self = own_seen[i] ? 1u : 0u;
-    u32 n = 0;
-    if (big_dense(hcap, x.count, x.big_mode)) {
-      n = live_n[i];  // entries already emitted by ag_dense_scan
-    } else {
-      const u64 slots = big_slots(hcap);
+    unsigned char* base = st.tables + st.tab_off[i];
+    const u32 self = st.own_seen[i] ? 1u : 0u;
+    const u64 slots = st.rslots[i];
+    const u32 n = st.live_n[i];  // dense: entries already emitted by ag_dense_scan
+    if (slots) {
       const BigSlot* t = reinterpret_cast<const BigSlot*>(base);
       const u32* live = reinterpret_cast<const u32*>(base + slots * sizeof(BigSlot));
-      n = live_n[i];
       for (u32 j = threadIdx.x; j < n && j < hcap; j += kBlockThreads) {
         const BigSlot e = t[live[j]];
         x.htgt[hbase + j] = e.key;
@@ -793,12 +818,23 @@ __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, const u3
       } else {
         if (self) {
           x.htgt[hbase + n] = c;
-          x.hw[hbase + n] = float(own_sum[i]);
+          x.hw[hbase + n] = float(st.own_sum[i]);
         }
         x.fill[c] = n + self;
       }
     }
   }
+}
+
+// communities of the list whose region overflowed, compacted (round 2 input)
+__global__ void ag_big_redo(const u32* __restrict__ big, u64 nbig, const u32* __restrict__ ovf,
+                            const u64* __restrict__ ext, u32* __restrict__ out, u32* __restrict__ nout,
+                            u64* __restrict__ ext_c) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < nbig; i += u64(gridDim.x) * blockDim.x)
+    if (ovf[i]) {
+      out[atomicAdd(nout, 1u)] = big[i];
+      ext_c[big[i]] = ext[i];
+    }
 }
 
 __global__ void compact_k(const u64* __restrict__ hoff, const u32* __restrict__ htgt,
@@ -833,6 +869,116 @@ int occupancy(K kernel, int threads, size_t smem) {
 
 }  // namespace
 
+
+// One round of the big path over `big` (nbig communities): region plan,
+// batches sized to the free memory, member arc list, tiles, merge, emit.
+// Round 1 (ext_c == nullptr) uses estimated region sizes and appends the
+// communities whose regions overflowed to redo[*nredo], with their counted
+// arcs to other communities in ext_out[c]; round 2 sizes regions by those.
+void big_round(const AggArgs& a, const u32* big, u64 nbig, const u64* ext_c, u32* redo, u32* nredo, u64* ext_out,
+               cudaStream_t s) {
+  const bool exact = ext_c != nullptr;
+  const int sms = sm_count();
+  DBuf<u32> index(a.count), live_n(nbig), own_seen(nbig), mcount(nbig), ovf(nbig);
+  DBuf<u64> bytes(nbig), rslots(nbig), tab_off(nbig + 1), moff(nbig + 1), ext(nbig);
+  DBuf<double> own(nbig);
+  LVN_CUDA(cudaMemsetAsync(ext.p, 0, nbig * sizeof(u64), s));
+  LVN_CUDA(cudaMemsetAsync(live_n.p, 0, nbig * sizeof(u32), s));
+  LVN_CUDA(cudaMemsetAsync(own_seen.p, 0, nbig * sizeof(u32), s));
+  LVN_CUDA(cudaMemsetAsync(ovf.p, 0, nbig * sizeof(u32), s));
+  LVN_CUDA(cudaMemsetAsync(own.p, 0, nbig * sizeof(double), s));
+  const unsigned pg = unsigned(std::min<u64>((nbig + 255) / 256, u64(sms) * 4));
+  ag_big_plan<<<pg, 256, 0, s>>>(big, nbig, a.count, a.big_mode, ext_c, a.hoff, a.boff, a.coff, index.p,
+                                 rslots.p, bytes.p, mcount.p);
+  LVN_LAUNCH();
+  exclusive_scan_u64(bytes.p, tab_off.p, nbig, s);
+  exclusive_scan_u32_to_u64(mcount.p, moff.p, nbig, s);
+  // host copies of the region offsets and member offsets (batch planning)
+  std::vector<u64> h_tab(nbig + 1), h_moff(nbig + 1);
+  LVN_CUDA(cudaMemcpyAsync(h_tab.data(), tab_off.p, (nbig + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaMemcpyAsync(h_moff.data(), moff.p, (nbig + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  const u64 M = h_moff[nbig];
+  // The regions can exceed device memory; communities are processed in
+  // batches whose regions fit a budget of a quarter of the free memory (at
+  // least the largest single region).
+  const size_t free_b = ctx().pool.available();
+  u64 largest = 0;
+  for (u64 i = 0; i < nbig; ++i) largest = std::max(largest, h_tab[i + 1] - h_tab[i]);
+  u64 budget = std::min<u64>(h_tab[nbig], u64(free_b / 4));
+  if (const char* e = std::getenv("LVN_BIG_TABLE_BUDGET")) budget = std::strtoull(e, nullptr, 10);  // tests
+  budget = std::max<u64>(budget, largest);
+  std::vector<u64> cuts{0};
+  for (u64 i = 0; i < nbig; ++i)
+    if (h_tab[i + 1] - h_tab[cuts.back()] > budget) cuts.push_back(i);
+  cuts.push_back(nbig);
+  if (const char* e = std::getenv("LVN_VERBOSE"); e && *e && *e != '0')
+    std::fprintf(stderr, "[lvn] aggregate round %d: %llu giant communities, %llu members, regions %.2f GB in %zu "
+                 "batches (budget %.2f GB, free %.2f GB)\n", exact ? 2 : 1, (unsigned long long)nbig,
+                 (unsigned long long)M, h_tab[nbig] / 1e9, cuts.size() - 1, budget / 1e9, free_b / 1e9);
+  DBuf<unsigned char> tables(budget ? budget : 16);
+  // L = members of the big communities with arcs, P = scan of their degrees
+  DBuf<u32> vert(M ? M : 1), keep(M + 1), kpos(M + 1), L(M ? M : 1), D(M ? M : 1);
+  DBuf<u64> P(M + 1);
+  const unsigned mg = unsigned(std::min<u64>((M + 255) / 256 + 1, u64(sms) * 8));
+  ag_big_keep<<<mg, 256, 0, s>>>(a, big, nbig, moff.p, M, vert.p, keep.p);
+  LVN_LAUNCH();
+  exclusive_scan_u32(keep.p, kpos.p, M, s);
+  // D past nL = kpos[M] stays 0, so P[nL..M] all hold the arc total
+  LVN_CUDA(cudaMemsetAsync(D.p, 0, (M ? M : 1) * sizeof(u32), s));
+  ag_big_list<<<mg, 256, 0, s>>>(a.g, vert.p, keep.p, kpos.p, M, L.p, D.p);
+  LVN_LAUNCH();
+  exclusive_scan_u32_to_u64(D.p, P.p, M, s);
+  // first owner of every kBigTile-arc tile of the flat arc space
+  u32 nL32 = 0;
+  LVN_CUDA(cudaMemcpyAsync(&nL32, kpos.p + M, sizeof(u32), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  u64 total_arcs = 0;
+  LVN_CUDA(cudaMemcpyAsync(&total_arcs, P.p + nL32, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  const u64 nL = nL32;
+  const u64 ntiles = total_arcs / kBigTile + 1;
+  DBuf<u32> tile_first(ntiles);
+  LVN_CUDA(cudaMemsetAsync(tile_first.p, 0, ntiles * sizeof(u32), s));
+  big_tile_owner<<<unsigned(std::min<u64>((nL + 255) / 256 + 1, u64(sms) * 8)), 256, 0, s>>>(P.p, kpos.p + M,
+                                                                                             tile_first.p);
+  LVN_LAUNCH();
+  static const int occ = occupancy(ag_big_arcs, kBigThreads, kBigSmem);
+  for (size_t bi = 0; bi + 1 < cuts.size(); ++bi) {
+    const u64 b0 = cuts[bi], b1 = cuts[bi + 1], nb = b1 - b0;
+    if (!nb) continue;
+    // regions of this batch start at the buffer's base
+    BigState st{index.p, rslots.p, tab_off.p, tables.p - h_tab[b0], live_n.p, own.p, own_seen.p, ovf.p, ext.p};
+    ag_big_clear<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), 256, 0, s>>>(nb, a.count, rslots.p + b0,
+                                                                            tab_off.p + b0, st.tables);
+    LVN_LAUNCH();
+    // arc range of the batch: members [moff[b0], moff[b1]) -> kept L entries -> P
+    u64 arc_lo = 0, arc_hi = ~u64(0);
+    if (cuts.size() > 2) {
+      u32 k[2] = {0, 0};
+      LVN_CUDA(cudaMemcpyAsync(&k[0], kpos.p + h_moff[b0], sizeof(u32), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaMemcpyAsync(&k[1], kpos.p + h_moff[b1], sizeof(u32), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaStreamSynchronize(s));
+      LVN_CUDA(cudaMemcpyAsync(&arc_lo, P.p + k[0], sizeof(u64), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaMemcpyAsync(&arc_hi, P.p + k[1], sizeof(u64), cudaMemcpyDeviceToHost, s));
+      LVN_CUDA(cudaStreamSynchronize(s));
+    }
+    ag_big_arcs<<<unsigned(u64(sms) * occ), kBigThreads, kBigSmem, s>>>(a, st, L.p, P.p, kpos.p + M, tile_first.p,
+                                                                       arc_lo, arc_hi);
+    LVN_LAUNCH();
+    BigState sb = st;  // views starting at the batch's first community
+    sb.rslots += b0, sb.tab_off += b0, sb.live_n += b0, sb.own_sum += b0, sb.own_seen += b0, sb.ovf += b0;
+    sb.ext += b0;
+    ag_dense_scan<<<unsigned(u64(sms) * 8), 256, 0, s>>>(a, sb, big + b0, nb);
+    LVN_LAUNCH();
+    ag_big_emit<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), kBlockThreads, 0, s>>>(a, sb, big + b0, nb);
+    LVN_LAUNCH();
+  }
+  if (redo) {
+    ag_big_redo<<<pg, 256, 0, s>>>(big, nbig, ovf.p, ext.p, redo, nredo, ext_out);
+    LVN_LAUNCH();
+  }
+}
 
 void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
   const int sms = sm_count();
@@ -877,100 +1023,17 @@ void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
   }
   const u64 nbig = b.count(kBinGlobal);
   if (nbig) {
-    const u32* big = b.of(kBinGlobal);
-    DBuf<u32> index(a.count), live_n(nbig), own_seen(nbig), mcount(nbig);
-    DBuf<u64> bytes(nbig), tab_off(nbig + 1), moff(nbig + 1);
-    DBuf<double> own(nbig);
-    LVN_CUDA(cudaMemsetAsync(live_n.p, 0, nbig * sizeof(u32), s));
-    LVN_CUDA(cudaMemsetAsync(own_seen.p, 0, nbig * sizeof(u32), s));
-    LVN_CUDA(cudaMemsetAsync(own.p, 0, nbig * sizeof(double), s));
-    const unsigned pg = unsigned(std::min<u64>((nbig + 255) / 256, u64(sms) * 4));
-    ag_big_plan<<<pg, 256, 0, s>>>(big, nbig, a.count, a.big_mode, a.hoff, a.coff, index.p, bytes.p, mcount.p);
-    LVN_LAUNCH();
-    exclusive_scan_u64(bytes.p, tab_off.p, nbig, s);
-    exclusive_scan_u32_to_u64(mcount.p, moff.p, nbig, s);
-    // host copies of the region offsets and member offsets (batch planning)
-    std::vector<u64> h_tab(nbig + 1), h_moff(nbig + 1);
-    LVN_CUDA(cudaMemcpyAsync(h_tab.data(), tab_off.p, (nbig + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
-    LVN_CUDA(cudaMemcpyAsync(h_moff.data(), moff.p, (nbig + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    DBuf<u32> redo(nbig), nredo(1);
+    DBuf<u64> ext_c(a.count);
+    LVN_CUDA(cudaMemsetAsync(nredo.p, 0, sizeof(u32), s));
+    big_round(a, b.of(kBinGlobal), nbig, nullptr, redo.p, nredo.p, ext_c.p, s);
+    u32 n2 = 0;
+    LVN_CUDA(cudaMemcpyAsync(&n2, nredo.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
     LVN_CUDA(cudaStreamSynchronize(s));
-    const u64 M = h_moff[nbig];
-    // The tables of all big communities can exceed device memory (their sum
-    // approaches 28 B per arc); communities are processed in batches whose
-    // regions fit a budget of a quarter of the free memory (at least the
-    // largest single region).
-    const size_t free_b = ctx().pool.available();
-    u64 largest = 0;
-    for (u64 i = 0; i < nbig; ++i) largest = std::max(largest, h_tab[i + 1] - h_tab[i]);
-    u64 budget = std::min<u64>(h_tab[nbig], u64(free_b / 4));
-    if (const char* e = std::getenv("LVN_BIG_TABLE_BUDGET")) budget = std::strtoull(e, nullptr, 10);  // tests
-    budget = std::max<u64>(budget, largest);
-    std::vector<u64> cuts{0};
-    for (u64 i = 0; i < nbig; ++i)
-      if (h_tab[i + 1] - h_tab[cuts.back()] > budget) cuts.push_back(i);
-    cuts.push_back(nbig);
     if (const char* e = std::getenv("LVN_VERBOSE"); e && *e && *e != '0')
-      std::fprintf(stderr, "[lvn] aggregate: %llu giant communities, %llu members, tables %.2f GB in %zu batches "
-                   "(budget %.2f GB, free %.2f GB)\n", (unsigned long long)nbig, (unsigned long long)M,
-                   h_tab[nbig] / 1e9, cuts.size() - 1, budget / 1e9, free_b / 1e9);
-    DBuf<unsigned char> tables(budget ? budget : 16);
-    // L = members of the big communities with arcs, P = scan of their degrees
-    DBuf<u32> vert(M ? M : 1), keep(M + 1), kpos(M + 1), L(M ? M : 1), D(M ? M : 1);
-    DBuf<u64> P(M + 1);
-    const unsigned mg = unsigned(std::min<u64>((M + 255) / 256 + 1, u64(sms) * 8));
-    ag_big_keep<<<mg, 256, 0, s>>>(a, big, nbig, moff.p, M, vert.p, keep.p);
-    LVN_LAUNCH();
-    exclusive_scan_u32(keep.p, kpos.p, M, s);
-    // D past nL = kpos[M] stays 0, so P[nL..M] all hold the arc total
-    LVN_CUDA(cudaMemsetAsync(D.p, 0, (M ? M : 1) * sizeof(u32), s));
-    ag_big_list<<<mg, 256, 0, s>>>(a.g, vert.p, keep.p, kpos.p, M, L.p, D.p);
-    LVN_LAUNCH();
-    exclusive_scan_u32_to_u64(D.p, P.p, M, s);
-    // first owner of every kBigTile-arc tile of the flat arc space; the arc
-    // total P[nL] is read back once (the batches below need it anyway)
-    u32 nL32 = 0;
-    LVN_CUDA(cudaMemcpyAsync(&nL32, kpos.p + M, sizeof(u32), cudaMemcpyDeviceToHost, s));
-    LVN_CUDA(cudaStreamSynchronize(s));
-    u64 total_arcs = 0;
-    LVN_CUDA(cudaMemcpyAsync(&total_arcs, P.p + nL32, sizeof(u64), cudaMemcpyDeviceToHost, s));
-    LVN_CUDA(cudaStreamSynchronize(s));
-    const u64 nL = nL32;
-    const u64 ntiles = total_arcs / kBigTile + 1;
-    DBuf<u32> tile_first(ntiles);
-    LVN_CUDA(cudaMemsetAsync(tile_first.p, 0, ntiles * sizeof(u32), s));
-    big_tile_owner<<<unsigned(std::min<u64>((nL + 255) / 256 + 1, u64(sms) * 8)), 256, 0, s>>>(P.p, kpos.p + M,
-                                                                                               tile_first.p);
-    LVN_LAUNCH();
-    static const int occ = occupancy(ag_big_arcs, kBigThreads, kBigSmem);
-    for (size_t bi = 0; bi + 1 < cuts.size(); ++bi) {
-      const u64 b0 = cuts[bi], b1 = cuts[bi + 1], nb = b1 - b0;
-      if (!nb) continue;
-      // regions of this batch start at the buffer's base
-      unsigned char* base = tables.p - h_tab[b0];
-      ag_big_clear<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), 256, 0, s>>>(big + b0, nb, a.count, a.big_mode, a.hoff,
-                                                                              tab_off.p + b0, base);
-      LVN_LAUNCH();
-      // arc range of the batch: members [moff[b0], moff[b1]) -> kept L entries -> P
-      u64 arc_lo = 0, arc_hi = ~u64(0);
-      if (cuts.size() > 2) {
-        u32 k[2] = {0, 0};
-        LVN_CUDA(cudaMemcpyAsync(&k[0], kpos.p + h_moff[b0], sizeof(u32), cudaMemcpyDeviceToHost, s));
-        LVN_CUDA(cudaMemcpyAsync(&k[1], kpos.p + h_moff[b1], sizeof(u32), cudaMemcpyDeviceToHost, s));
-        LVN_CUDA(cudaStreamSynchronize(s));
-        LVN_CUDA(cudaMemcpyAsync(&arc_lo, P.p + k[0], sizeof(u64), cudaMemcpyDeviceToHost, s));
-        LVN_CUDA(cudaMemcpyAsync(&arc_hi, P.p + k[1], sizeof(u64), cudaMemcpyDeviceToHost, s));
-        LVN_CUDA(cudaStreamSynchronize(s));
-      }
-      ag_big_arcs<<<unsigned(u64(sms) * occ), kBigThreads, kBigSmem, s>>>(a, index.p, tab_off.p, base, live_n.p, own.p,
-                                                                    own_seen.p, L.p, P.p, kpos.p + M, tile_first.p,
-                                                                    arc_lo, arc_hi);
-      LVN_LAUNCH();
-      ag_dense_scan<<<unsigned(u64(sms) * 8), 256, 0, s>>>(a, big + b0, nb, tab_off.p + b0, base, live_n.p + b0);
-      LVN_LAUNCH();
-      ag_big_emit<<<unsigned(std::min<u64>(nb, u64(sms) * 4)), kBlockThreads, 0, s>>>(
-          a, big + b0, nb, tab_off.p + b0, base, live_n.p + b0, own.p + b0, own_seen.p + b0);
-      LVN_LAUNCH();
-    }
+      std::fprintf(stderr, "[lvn] aggregate: %u of %llu giant communities outgrew their estimated regions\n", n2,
+                   (unsigned long long)nbig);
+    if (n2) big_round(a, redo.p, n2, ext_c.p, nullptr, nullptr, nullptr, s);
   }
 }
 

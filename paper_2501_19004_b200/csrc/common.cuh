@@ -80,10 +80,15 @@ class Pool {
   void trim();         // return cached memory to the driver
   void release_all();  // free every outstanding allocation (context teardown)
   void report();       // pool occupancy on stderr (LVN_VERBOSE)
-  // device memory this pool can still hand out: device total minus the pool's
-  // live allocations, plus its cached big blocks (no cudaMemGetInfo, which can
-  // stall the host for tens of ms while kernels are in flight)
+  // device memory this pool can still hand out: device total minus the
+  // memory held outside the pool (as of the last refresh) minus the pool's
+  // live allocations, plus its cached big blocks, minus a 1 GB margin
   size_t available();
+  // re-measure the memory held outside the pool (CUDA context, caller
+  // buffers such as a borrowed device CSR, other processes on the GPU) with
+  // cudaMemGetInfo; called at the entry of a run while the stream is idle
+  // (mid-run, cudaMemGetInfo stalls the host for tens of ms)
+  void refresh_external();
 
  private:
   void* raw(size_t bytes);
@@ -94,6 +99,7 @@ class Pool {
   std::multimap<size_t, void*> big_free_;
   size_t cache_budget_ = size_t(16) << 30;  // bytes of free big blocks kept across a miss
   size_t total_ = 0;                        // device memory (at bind)
+  size_t external_ = 0;                     // held outside the pool (refresh_external)
 };
 
 // Pinned host blocks for results handed to the caller (membership): device

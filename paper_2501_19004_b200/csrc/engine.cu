@@ -42,26 +42,26 @@ void Pool::bind(int device, cudaStream_t s) {
   total_ = total_b;
 }
 
-// Device memory this pool can still hand out: the driver's free memory (which
-// sees the CUDA context, borrowed caller buffers and other processes sharing
-// the GPU) plus the blocks cached here, minus a 1 GB margin, capped by the
-// pool's own accounting. Callers query it right after a stream
-// synchronisation (cudaMemGetInfo stalls while kernels are in flight).
 size_t Pool::available() {
   std::uint64_t used = 0;
   (void)cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrUsedMemCurrent, &used);
   size_t cached = 0;
   for (auto& kv : big_free_) cached += kv.first;
   const size_t margin = size_t(1) << 30;
-  size_t est = used + margin < total_ + cached ? total_ + cached - used - margin : 0;
+  const size_t held = used + external_ + margin;
+  return held < total_ + cached ? total_ + cached - held : 0;
+}
+
+void Pool::refresh_external() {
+  std::uint64_t reserved = 0;
+  (void)cudaMemPoolGetAttribute(pool_, cudaMemPoolAttrReservedMemCurrent, &reserved);
   size_t free_b = 0, total_b = 0;
-  if (cudaMemGetInfo(&free_b, &total_b) == cudaSuccess) {
-    const size_t drv = free_b + cached > margin ? free_b + cached - margin : 0;
-    est = std::min(est, drv);
-  } else {
+  if (cudaMemGetInfo(&free_b, &total_b) != cudaSuccess) {
     (void)cudaGetLastError();
+    return;
   }
-  return est;
+  const size_t inside = size_t(reserved) + free_b;
+  external_ = total_b > inside ? total_b - inside : 0;
 }
 
 void* Pool::raw(size_t bytes) {
@@ -512,15 +512,28 @@ bool verbose() {
 // [cb[r], cb[r+1]) (split by member-degree budget) and the ranks allgather the
 // row lengths and then the rows, so every rank ends with the whole super-graph.
 void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
-                      u32* err, cudaStream_t s, bool canonical, Comm* comm = nullptr) {
+                      u32* err, cudaStream_t s, bool canonical, Comm* comm = nullptr,
+                      const Bins* gbins = nullptr) {
   const bool sh = comm && comm->on();
   DBuf<u32> msize(count ? count : 1);
-  DBuf<u64> budget(count + 1), coff(count + 1), boff(count + 1), hoff(count + 1), capped(count + 1);
+  DBuf<u64> budget(count + 1), coff(count + 1), boff(count + 1), hoff(count + 1), capped(count + 1),
+      ext(count + 1);
   community_counts(g, C, count, msize.p, budget.p, s);
   exclusive_scan_u32_to_u64(msize.p, coff.p, count, s);
   exclusive_scan_u64(budget.p, boff.p, count, s);
-  // holey row capacity min(budget, count): distinct targets never exceed either
-  cap_budgets(budget.p, capped.p, count, s);
+  // holey row capacity min(ext + 1, count): a super-row's distinct targets are
+  // at most its arcs to other communities plus the self-loop, and at most
+  // count (ext: one row pass over the graph, binned like the modularity pass)
+  {
+    Bins local;
+    const Bins* gb = gbins;
+    if (!gb) {
+      compute_bins(g.off, g.n, e, local, s);
+      gb = &local;
+    }
+    external_arcs(g, *gb, C, ext.p, count, s);
+  }
+  cap_budgets(ext.p, capped.p, count, s);
   exclusive_scan_u64(capped.p, hoff.p, count, s);
   DBuf<u32> members(g.n ? g.n : 1), cursor(count ? count : 1);
   community_scatter(C, g.n, coff.p, count, cursor.p, members.p, s);
@@ -931,7 +944,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     const auto t1 = Clock::now();
     OwnedCsr& next = owned[pass & 1];
     sp = tm.begin(LVN_STAT_AGGREGATE, s);
-    aggregate_device(cur, C.p, count, edges, next, err.p, s, false, shard ? &cm : nullptr);
+    aggregate_device(cur, C.p, count, edges, next, err.p, s, false, shard ? &cm : nullptr, &B);
     tm.end(sp, s, 12.0 * double(cur.arcs) + 16.0 * nv + 8.0 * double(next.arcs) + 8.0 * (count + 1.0),
            nv, cur.arcs);
     t_aggregate += since(t1);
@@ -1010,6 +1023,7 @@ int guard(F&& f) {
     Context& c = ctx();
     std::lock_guard<std::mutex> lk(c.mu);
     LVN_CUDA(cudaSetDevice(c.device));
+    c.pool.refresh_external();  // the stream is idle between calls
     f(c);
     return kOk;
   } catch (const Error& e) {
@@ -1033,15 +1047,16 @@ struct DGraphHandle {
 
 // holey-row capacity kernel (used by aggregate_device)
 namespace lvn {
-__global__ void cap_budgets_k(const u64* __restrict__ budget, u64* __restrict__ capped, u32 count) {
+// capped[c] = min(ext[c] + 1, count): holey row capacity
+__global__ void cap_budgets_k(const u64* __restrict__ ext, u64* __restrict__ capped, u32 count) {
   for (u64 c = blockIdx.x * u64(blockDim.x) + threadIdx.x; c < count;
        c += u64(gridDim.x) * blockDim.x)
-    capped[c] = budget[c] < count ? budget[c] : u64(count);
+    capped[c] = ext[c] + 1 < count ? ext[c] + 1 : u64(count);
 }
-void cap_budgets(const u64* budget, u64* capped, u32 count, cudaStream_t s) {
+void cap_budgets(const u64* ext, u64* capped, u32 count, cudaStream_t s) {
   if (!count) return;
   const u64 blocks = std::min<u64>((u64(count) + 255) / 256, u64(sm_count()) * 8);
-  cap_budgets_k<<<unsigned(blocks), 256, 0, s>>>(budget, capped, count);
+  cap_budgets_k<<<unsigned(blocks), 256, 0, s>>>(ext, capped, count);
   LVN_LAUNCH();
 }
 }  // namespace lvn

@@ -174,8 +174,8 @@ struct AggArgs {
 };
 // Synchronises once when the kBinGlobal bin is non-empty (sizes its HBM tables).
 void aggregate_rows(const AggArgs& a, const Bins& bins, cudaStream_t s);
-// capped[c] = min(budget[c], count): holey row capacity
-void cap_budgets(const u64* budget, u64* capped, u32 count, cudaStream_t s);
+// capped[c] = min(ext[c] + 1, count): holey row capacity (ext: external_arcs)
+void cap_budgets(const u64* ext, u64* capped, u32 count, cudaStream_t s);
 // out rows = holey rows compacted (noff = scan of fill), total weight (fp64) into *tw
 void compact_rows(const u64* hoff, const u32* htgt, const float* hw, const u32* fill,
                   const u64* noff, u32 count, u32* otgt, float* ow, double* tw,
@@ -185,6 +185,9 @@ void compact_rows(const u64* hoff, const u32* htgt, const float* hw, const u32* 
 // sums: [0] internal arc weight, [1] sum_c Sigma_c^2 ; tot (width entries) zeroed here
 void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width,
                       double* sums, cudaStream_t s, double two_m);
+// ext[c] = arcs from members of c to other communities (width entries, zeroed
+// here): bounds the distinct targets of super-row c (aggregation capacities)
+void external_arcs(const DGraph& g, const Bins& b, const u32* C, u64* ext, u64 width, cudaStream_t s);
 
 // ---- generate.cu: device-built synthetic inputs --------------------------------
 struct OwnedCsr {

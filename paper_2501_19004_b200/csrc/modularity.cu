@@ -22,22 +22,46 @@ __device__ __forceinline__ void add_tot(double* tot, u32 c, double k) {
   if (lane == leader) atomicAdd(&tot[c], s);
 }
 
+// one count per vertex into ext[c] (arcs to other communities), warp-aggregated
+__device__ __forceinline__ void add_ext(ull* ext, u32 c, ull n) {
+  const u32 act = __activemask();
+  const u32 peers = __match_any_sync(act, c);
+  const int lane = threadIdx.x & 31;
+  const int leader = __ffs(peers) - 1;
+  ull s = 0;
+  for (u32 rest = peers; rest; rest &= rest - 1) s += __shfl_sync(peers, n, __ffs(rest) - 1);
+  if (lane == leader && s) atomicAdd(&ext[c], s);
+}
+
+// X (ext-only): count each row's arcs to other communities into ext[C[u]]
+// instead of the modularity terms (aggregation capacities, aggregate.cu)
+template <bool X>
 __global__ void mod_thread(DGraph g, const u32* __restrict__ list, u64 count,
-                           const u32* __restrict__ C, double* __restrict__ tot, double* sums) {
+                           const u32* __restrict__ C, double* __restrict__ tot, double* sums, ull* ext) {
   double internal = 0.0;
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < count;
        i += u64(gridDim.x) * blockDim.x) {
     const u32 v = list[i];
     const u32 c = C[v];
     double k = 0.0, in = 0.0;
+    ull out = 0;
     for (u64 a = g.off[v]; a < g.off[v + 1]; ++a) {
+      if (X) {
+        out += C[g.tgt[a]] != c;
+        continue;
+      }
       const double w = double(g.w[a]);
       k += w;
       if (C[g.tgt[a]] == c) in += w;
     }
-    internal += in;
-    add_tot(tot, c, k);
+    if (X) {
+      add_ext(ext, c, out);
+    } else {
+      internal += in;
+      add_tot(tot, c, k);
+    }
   }
+  if (X) return;
   internal = warp_sum(internal);
   if ((threadIdx.x & 31) == 0 && internal != 0.0) atomicAdd(&sums[0], internal);
 }
@@ -46,10 +70,10 @@ __global__ void mod_thread(DGraph g, const u32* __restrict__ list, u64 count,
 // (arc r*G + lane, coalesced), two rows per group in flight so each lane has
 // 2K independent gathers of C[t] outstanding. The thread-per-row kernel above
 // reads 32 different rows per warp load (one L1TEX line per lane per arc).
-template <int G, int K>
+template <int G, int K, bool X>
 __global__ void __launch_bounds__(256) mod_group(DGraph g, const u32* __restrict__ list, u64 count,
                                                  const u32* __restrict__ C, double* __restrict__ tot,
-                                                 double* sums) {
+                                                 double* sums, ull* ext) {
   constexpr int GPB = 256 / G;
   const u32 lane = threadIdx.x & (G - 1);
   const u64 gi = (blockIdx.x * u64(blockDim.x) + threadIdx.x) / G;
@@ -70,7 +94,7 @@ __global__ void __launch_bounds__(256) mod_group(DGraph g, const u32* __restrict
       for (int r = 0; r < K; ++r) {
         const u64 a = lo[j] + u64(r) * G + lane;
         t[j][r] = a < hi[j] ? __ldcs(g.tgt + a) : kEmpty;
-        w[j][r] = a < hi[j] ? __ldcs(g.w + a) : 0.f;
+        w[j][r] = X ? 0.f : a < hi[j] ? __ldcs(g.w + a) : 0.f;
       }
     }
     u32 ct[2][K];
@@ -80,6 +104,15 @@ __global__ void __launch_bounds__(256) mod_group(DGraph g, const u32* __restrict
       for (int r = 0; r < K; ++r) ct[j][r] = t[j][r] != kEmpty ? C[t[j][r]] : kEmpty;
 #pragma unroll
     for (int j = 0; j < 2; ++j) {
+      if (X) {
+        u32 out = 0;
+#pragma unroll
+        for (int r = 0; r < K; ++r) out += ct[j][r] != kEmpty && ct[j][r] != c[j];
+#pragma unroll
+        for (int o = G / 2; o > 0; o >>= 1) out += __shfl_xor_sync(0xffffffffu, out, o, G);
+        if (lane == 0 && c[j] != kEmpty && out) atomicAdd(&ext[c[j]], ull(out));
+        continue;
+      }
       double k = 0.0;
 #pragma unroll
       for (int r = 0; r < K; ++r) {
@@ -91,12 +124,14 @@ __global__ void __launch_bounds__(256) mod_group(DGraph g, const u32* __restrict
       if (lane == 0 && c[j] != kEmpty && k != 0.0) atomicAdd(&tot[c[j]], k);
     }
   }
+  if (X) return;
   internal = warp_sum(internal);
   if ((threadIdx.x & 31) == 0 && internal != 0.0) atomicAdd(&sums[0], internal);
 }
 
+template <bool X>
 __global__ void mod_warp(DGraph g, const u32* __restrict__ list, u64 count,
-                         const u32* __restrict__ C, double* __restrict__ tot, double* sums) {
+                         const u32* __restrict__ C, double* __restrict__ tot, double* sums, ull* ext) {
   const int lane = threadIdx.x & 31;
   const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
   double internal = 0.0;
@@ -104,27 +139,46 @@ __global__ void mod_warp(DGraph g, const u32* __restrict__ list, u64 count,
     const u32 v = list[i];
     const u32 c = C[v];
     double k = 0.0, in = 0.0;
-    for (u64 a = g.off[v] + lane; a < g.off[v + 1]; a += 32) {
-      const double w = double(g.w[a]);
-      k += w;
-      if (C[g.tgt[a]] == c) in += w;
+    if (X) {
+      u32 out = 0;
+      for (u64 a = g.off[v] + lane; a < g.off[v + 1]; a += 32) out += C[g.tgt[a]] != c;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) out += __shfl_xor_sync(0xffffffffu, out, o);
+      if (lane == 0 && out) atomicAdd(&ext[c], ull(out));
+    } else {
+      for (u64 a = g.off[v] + lane; a < g.off[v + 1]; a += 32) {
+        const double w = double(g.w[a]);
+        k += w;
+        if (C[g.tgt[a]] == c) in += w;
+      }
     }
+    if (X) continue;
     k = warp_sum(k);
     internal += in;
     if (lane == 0) atomicAdd(&tot[c], k);
   }
+  if (X) return;
   internal = warp_sum(internal);
   if (lane == 0 && internal != 0.0) atomicAdd(&sums[0], internal);
 }
 
+template <bool X>
 __global__ void __launch_bounds__(512) mod_block(DGraph g, const u32* __restrict__ list, u64 count,
                                                  const u32* __restrict__ C,
-                                                 double* __restrict__ tot, double* sums) {
+                                                 double* __restrict__ tot, double* sums, ull* ext) {
   __shared__ double ws[16];
   double internal = 0.0;
   for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
     const u32 v = list[i];
     const u32 c = C[v];
+    if (X) {
+      u32 out = 0;
+      for (u64 a = g.off[v] + threadIdx.x; a < g.off[v + 1]; a += blockDim.x) out += C[__ldcs(g.tgt + a)] != c;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) out += __shfl_xor_sync(0xffffffffu, out, o);
+      if ((threadIdx.x & 31) == 0 && out) atomicAdd(&ext[c], ull(out));
+      continue;
+    }
     double k = 0.0;
     for (u64 a = g.off[v] + threadIdx.x; a < g.off[v + 1]; a += blockDim.x) {
       const double w = double(g.w[a]);
@@ -141,6 +195,7 @@ __global__ void __launch_bounds__(512) mod_block(DGraph g, const u32* __restrict
     }
     __syncthreads();
   }
+  if (X) return;
   internal = warp_sum(internal);
   if ((threadIdx.x & 31) == 0 && internal != 0.0) atomicAdd(&sums[0], internal);
 }
@@ -156,12 +211,9 @@ __global__ void sum_squares(const double* __restrict__ tot, u64 width, double tw
   if ((threadIdx.x & 31) == 0 && acc != 0.0) atomicAdd(&sums[1], acc);
 }
 
-}  // namespace
 
-void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width,
-                      double* sums, cudaStream_t s, double two_m) {
-  LVN_CUDA(cudaMemsetAsync(tot, 0, width * sizeof(double), s));
-  LVN_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), s));
+template <bool X>
+void row_pass(const DGraph& g, const Bins& b, const u32* C, double* tot, double* sums, ull* ext, cudaStream_t s) {
   const int sms = sm_count();
   // rows in the register-sort bins: a lane group per row (the bin fixes the
   // row length bound); isolated vertices contribute nothing
@@ -169,37 +221,52 @@ void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot,
     if (!b.count(bin)) return;
     const u64 per_block = 256 / G;
     const u64 blocks = std::min<u64>((b.count(bin) + per_block - 1) / per_block, u64(sms) * 8);
-    kernel<<<unsigned(blocks), 256, 0, s>>>(g, b.of(bin), b.count(bin), C, tot, sums);
+    kernel<<<unsigned(blocks), 256, 0, s>>>(g, b.of(bin), b.count(bin), C, tot, sums, ext);
     LVN_LAUNCH();
   };
   // rows of <= 16 arcs (thread, sort8 and sort16 bins, adjacent in the list): a thread each
   const u64 small = b.start[kBinSort32] - b.start[kBinThread];
   if (small) {
     const u64 blocks = std::min<u64>((small + 255) / 256, u64(sms) * 8);
-    mod_thread<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinThread), small, C, tot, sums);
+    mod_thread<X><<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinThread), small, C, tot, sums, ext);
     LVN_LAUNCH();
   }
-  grp(kBinSort32, mod_group<32, 1>, 32);
-  grp(kBinSort64, mod_group<32, 2>, 32);
-  grp(kBinSort128, mod_group<32, 4>, 32);
-  grp(kBinSort256, mod_group<32, 8>, 32);
+  grp(kBinSort32, mod_group<32, 1, X>, 32);
+  grp(kBinSort64, mod_group<32, 2, X>, 32);
+  grp(kBinSort128, mod_group<32, 4, X>, 32);
+  grp(kBinSort256, mod_group<32, 8, X>, 32);
   const u64 mid = b.count(kBinWarp);
   if (mid) {
     const u64 blocks = std::min<u64>((mid + 7) / 8, u64(sms) * 8);
-    mod_warp<<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinWarp), mid, C, tot, sums);
+    mod_warp<X><<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinWarp), mid, C, tot, sums, ext);
     LVN_LAUNCH();
   }
   const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
   if (big) {
     const u64 blocks = std::min<u64>(big, u64(sms) * 4);
-    mod_block<<<unsigned(blocks), 512, 0, s>>>(g, b.of(kBinBlock), big, C, tot, sums);
+    mod_block<X><<<unsigned(blocks), 512, 0, s>>>(g, b.of(kBinBlock), big, C, tot, sums, ext);
     LVN_LAUNCH();
   }
+}
+
+}  // namespace
+
+void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width,
+                      double* sums, cudaStream_t s, double two_m) {
+  LVN_CUDA(cudaMemsetAsync(tot, 0, width * sizeof(double), s));
+  LVN_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), s));
+  row_pass<false>(g, b, C, tot, sums, nullptr, s);
   if (width) {
+    const int sms = sm_count();
     const u64 blocks = std::min<u64>((width + 255) / 256, u64(sms) * 8);
     sum_squares<<<unsigned(blocks), 256, 0, s>>>(tot, width, two_m, sums);
     LVN_LAUNCH();
   }
+}
+
+void external_arcs(const DGraph& g, const Bins& b, const u32* C, u64* ext, u64 width, cudaStream_t s) {
+  LVN_CUDA(cudaMemsetAsync(ext, 0, width * sizeof(u64), s));
+  row_pass<true>(g, b, C, nullptr, nullptr, reinterpret_cast<ull*>(ext), s);
 }
 
 }  // namespace lvn

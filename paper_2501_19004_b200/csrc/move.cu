@@ -51,6 +51,7 @@ constexpr int kWarpCapLog = 9;     // 512 slots (warp_max <= 256)
 constexpr int kBlockCapLog = 13;   // 8192 slots (block_max <= 4096)
 constexpr int kBlockThreads = 512;
 constexpr int kBatch = 4;          // arcs (and ranked entries) in flight per lane
+constexpr u64 kBlockSplit = 1024;  // block bin: rows up to this many arcs use 4 sub-groups per block
 
 // ---- per-thread accounting, flushed once per thread at kernel exit ----------
 struct Tally {
@@ -241,11 +242,11 @@ __global__ void __launch_bounds__(256) lm_thread(MoveArgs x, const u32* __restri
 // memory requests in flight (the sweep is latency-bound otherwise).
 //
 // COMBINE (stride a multiple of 32, consecutive lanes on consecutive arcs):
-// the 32 (community, weight) pairs a warp holds are first sorted across the
-// warp and summed per run, so each distinct community of the batch is merged
-// into the table once. Late passes have few distinct neighbour communities
-// per row; without this, all lanes of a block hammer the same few slots with
-// CAS retries.
+// runs of equal adjacent communities among the 32 (community, weight) pairs a
+// warp holds are summed first (warp_combine), so a run is merged into the
+// table once. Late passes have few distinct neighbour communities per row;
+// without this, all lanes of a block hammer the same few slots with CAS
+// retries.
 template <int B, bool COMBINE, class Tab, class V>
 __device__ __forceinline__ void scan_arcs(const MoveArgs& x, const Tab& tab, u32 lg, u32 u, u32 from,
                                           u64 lo, u64 hi, u32 lane, u32 stride, V& own, u32* live,
@@ -265,15 +266,8 @@ __device__ __forceinline__ void scan_arcs(const MoveArgs& x, const Tab& tab, u32
 #pragma unroll
     for (int k = 0; k < B; ++k) {
       bool tail = true;
-      // combine only when the batch repeats a community (one match.any tells)
-      if (COMBINE && !__all_sync(0xffffffffu, __match_any_sync(0xffffffffu, c[k]) == (1u << (lane & 31)))) {
-        u32 kk[1] = {c[k]};
-        V vv[1] = {w[k]};
-        bitonic_sort<32, 1, V>(kk, vv, lane & 31);
-        bool tl[1];
-        segmented_runs<32, 1, V>(kk, vv, tl, lane & 31);
-        c[k] = kk[0], w[k] = vv[0], tail = tl[0];
-      }
+      // sum runs of equal adjacent communities across the warp first
+      if (COMBINE) tail = warp_combine(c[k], w[k], lane & 31);
       if (!tail || c[k] == kEmpty) continue;
       if (c[k] == from) {
         own += w[k];
@@ -937,44 +931,70 @@ constexpr size_t block_stage_smem() {
   return block_smem<Tab>() + (size_t(1) << (kBlockCapLog - 1)) * 8;
 }
 
-template <class Tab, bool DRY>
+// Sub-groups: the block runs SUB independent groups of kBlockThreads / SUB
+// threads, each deciding its own vertex with its own slice of the smem table
+// (8192 / SUB slots, rows up to 4096 / SUB arcs) and synchronising on its own
+// named barrier, so a group never waits for another group's vertex. SUB = 4
+// takes rows of 257..1024 arcs (four vertices in flight per block instead of
+// one: per vertex the block is latency-bound on its dependent chain
+// list -> row -> communities -> table -> Sigma -> join, and barrier-bound when
+// a long row's 512 threads wait on a short one); SUB = 1 takes 1025..4096.
+template <int SUB>
+__device__ __forceinline__ void sub_sync(u32 g) {
+  if (SUB == 1) {
+    __syncthreads();
+  } else {
+    asm volatile("bar.sync %0, %1;" ::"r"(g + 1), "r"(kBlockThreads / SUB) : "memory");
+  }
+}
+
+template <class Tab, bool DRY, int SUB>
 __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32* __restrict__ list,
-                                                          u64 count) {
+                                                          u64 count, u64 dmin, u64 dmax) {
   using V = typename Tab::V;
-  constexpr int W = kBlockThreads / 32;
+  constexpr int ST = kBlockThreads / SUB;  // threads of a sub-group
+  constexpr int W = ST / 32;               // warps of a sub-group
+  constexpr int CAPLOG = kBlockCapLog - (SUB == 1 ? 0 : SUB == 2 ? 1 : SUB == 4 ? 2 : 3);
+  constexpr u32 CAP = 1u << CAPLOG;
   extern __shared__ __align__(16) unsigned char smem[];
-  __shared__ V red_v[W];
-  __shared__ double red_g[W], red_k[W];
-  __shared__ u32 red_c[W];
-  __shared__ u32 bcast, nlive;
-  const Tab tab(smem, u64(1) << kBlockCapLog);
-  u32* live = reinterpret_cast<u32*>(smem + (size_t(1) << kBlockCapLog) * Tab::kSlotBytes);
-  u32* st_c = live + (size_t(1) << (kBlockCapLog - 1));
-  float* st_w = reinterpret_cast<float*>(st_c + (size_t(1) << (kBlockCapLog - 1)));
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  for (u32 s = threadIdx.x; s < (1u << kBlockCapLog); s += kBlockThreads) tab.clear(s);
-  if (threadIdx.x == 0) nlive = 0;
-  __syncthreads();
+  __shared__ V red_v[SUB][W];
+  __shared__ double red_g[SUB][W], red_k[SUB][W];
+  __shared__ u32 red_c[SUB][W];
+  __shared__ u32 bcast[SUB], nlive[SUB], sorted_flag[SUB];
+  const u32 g = threadIdx.x / ST, lt = threadIdx.x % ST;
+  // sub-group slices: table, live list, stage (communities, weights)
+  unsigned char* tbase = smem + size_t(g) * CAP * Tab::kSlotBytes;
+  const Tab tab(tbase, CAP);
+  u32* live = reinterpret_cast<u32*>(smem + size_t(SUB) * CAP * Tab::kSlotBytes) + size_t(g) * (CAP / 2);
+  u32* st_c = reinterpret_cast<u32*>(smem + size_t(SUB) * CAP * Tab::kSlotBytes) + size_t(SUB) * (CAP / 2) +
+              size_t(g) * (CAP / 2);
+  float* st_w = reinterpret_cast<float*>(reinterpret_cast<u32*>(smem + size_t(SUB) * CAP * Tab::kSlotBytes) +
+                                         size_t(2 * SUB) * (CAP / 2)) + size_t(g) * (CAP / 2);
+  const int lane = threadIdx.x & 31, wid = lt >> 5;
+  for (u32 sl = lt; sl < CAP; sl += ST) tab.clear(sl);
+  if (lt == 0) nlive[g] = 0;
+  sub_sync<SUB>(g);
   Tally tl;
-  for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
+  for (u64 i = u64(blockIdx.x) * SUB + g; i < count; i += u64(gridDim.x) * SUB) {
     const u32 u = list[i];
-    if (!DRY) {
-      if (threadIdx.x == 0) {
-        const u32 act = !x.prune || x.flags[u];
-        if (act) x.flags[u] = 0;
-        bcast = act;
-      }
-      __syncthreads();
-      const u32 act = bcast;
-      __syncthreads();
-      if (!act) continue;
-    }
     const u64 lo = x.g.off[u];
     const u64 d = x.g.off[u + 1] - lo;
+    if (d <= dmin || d > dmax) continue;  // the other sub-group width takes it
+    if (!DRY) {
+      if (lt == 0) {
+        const u32 act = !x.prune || x.flags[u];
+        if (act) x.flags[u] = 0;
+        bcast[g] = act;
+      }
+      sub_sync<SUB>(g);
+      const u32 act = bcast[g];
+      sub_sync<SUB>(g);
+      if (!act) continue;
+    }
     const u32 from = x.C[u];
     const u32 lg = table_log(d, 5);
-    if (lg > u32(kBlockCapLog)) {  // capacity invariant
-      if (threadIdx.x == 0) atomicOr(x.err, u32(kErrTable));
+    if (lg > u32(CAPLOG)) {  // capacity invariant
+      if (lt == 0) atomicOr(x.err, u32(kErrTable));
       continue;
     }
     // stage the row's (community, weight) pairs in smem (coalesced loads, B
@@ -983,18 +1003,18 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
     // ascending C (every row of a pass's first sweep) stay strictly ascending
     V own = V(0);
     bool up = true;
-    for (u64 b0 = 0; b0 < d; b0 += u64(kBlockThreads) * kBatch) {
+    for (u64 b0 = 0; b0 < d; b0 += u64(ST) * kBatch) {
       u32 t[kBatch];
       float w[kBatch];
 #pragma unroll
       for (int k = 0; k < kBatch; ++k) {
-        const u64 e = b0 + threadIdx.x + u64(k) * kBlockThreads;
+        const u64 e = b0 + lt + u64(k) * ST;
         t[k] = e < d ? __ldcs(x.g.tgt + lo + e) : kEmpty;
         w[k] = e < d ? __ldcs(x.g.w + lo + e) : 0.f;
       }
 #pragma unroll
       for (int k = 0; k < kBatch; ++k) {
-        const u64 e = b0 + threadIdx.x + u64(k) * kBlockThreads;
+        const u64 e = b0 + lt + u64(k) * ST;
         if (t[k] == kEmpty) continue;
         const u32 c = t[k] == u ? from : x.C[t[k]];
         if (t[k] == u) w[k] = 0.f;
@@ -1003,49 +1023,45 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
         st_w[e] = w[k];
       }
     }
-    __syncthreads();
-    for (u64 e = threadIdx.x; e + 1 < d; e += kBlockThreads) up = up && st_c[e] < st_c[e + 1];
-    const bool rows_sorted = __syncthreads_and(up);
+    if (lt == 0) sorted_flag[g] = 1;
+    sub_sync<SUB>(g);
+    for (u64 e = lt; e + 1 < d; e += ST) up = up && st_c[e] < st_c[e + 1];
+    if (!up) sorted_flag[g] = 0;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
-    if (lane == 0) red_v[wid] = own;
+    if (lane == 0) red_v[g][wid] = own;
+    sub_sync<SUB>(g);
+    const bool rows_sorted = sorted_flag[g] != 0;
     if (!rows_sorted) {
       // merge the staged pairs into the table, combining duplicates per warp round
-      for (u64 e0 = 0; e0 < d; e0 += kBlockThreads) {
-        const u64 e = e0 + threadIdx.x;
+      for (u64 e0 = 0; e0 < d; e0 += ST) {
+        const u64 e = e0 + lt;
         u32 c = e < d ? st_c[e] : kEmpty;
         V w = e < d ? V(st_w[e]) : V(0);
         if (c == from) c = kEmpty;
-        if (!__all_sync(0xffffffffu, __match_any_sync(0xffffffffu, c) == (1u << lane) || c == kEmpty)) {
-          u32 kk[1] = {c};
-          V vv[1] = {w};
-          bitonic_sort<32, 1, V>(kk, vv, lane);
-          bool tl1[1];
-          segmented_runs<32, 1, V>(kk, vv, tl1, lane);
-          c = tl1[0] ? kk[0] : kEmpty, w = vv[0];
-        }
+        if (!warp_combine(c, w, u32(lane))) c = kEmpty;
         if (c != kEmpty) {
           const int slot = tab.insert(lg, c, w);
-          if (slot >= 0) live[atomicAdd(&nlive, 1u)] = u32(slot);
+          if (slot >= 0) live[atomicAdd(&nlive[g], 1u)] = u32(slot);
         }
       }
     }
-    __syncthreads();
+    sub_sync<SUB>(g);
     V own_all = V(0);
 #pragma unroll
-    for (int k = 0; k < W; ++k) own_all += red_v[k];
-    const u32 n = rows_sorted ? u32(d) : nlive;
+    for (int k = 0; k < W; ++k) own_all += red_v[g][k];
+    const u32 n = rows_sorted ? u32(d) : nlive[g];
     const double ku = x.K[u], sf = x.sigma[from];
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty;
     if (rows_sorted) {
       // every staged entry is its own community: rank them directly
-      for (u32 j0 = threadIdx.x; j0 < n; j0 += kBlockThreads * kBatch) {
+      for (u32 j0 = lt; j0 < n; j0 += ST * kBatch) {
         u32 key[kBatch];
         double val[kBatch], sc[kBatch];
 #pragma unroll
         for (int k = 0; k < kBatch; ++k) {
-          const u32 j = j0 + k * kBlockThreads;
+          const u32 j = j0 + k * ST;
           key[k] = j < n ? st_c[j] : kEmpty;
           val[k] = j < n ? double(V(st_w[j])) : 0.0;
           if (key[k] == from || (key[k] != kEmpty && !(key_ok(x, key[k]) &&
@@ -1057,12 +1073,12 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
 #pragma unroll
         for (int k = 0; k < kBatch; ++k) {
           if (key[k] == kEmpty) continue;
-          const double g = score<DRY, V>(x, val[k], double(own_all), ku, sc[k], sf);
-          if (better(g, key[k], bg, bc)) bg = g, bc = key[k], bk = val[k];
+          const double gk = score<DRY, V>(x, val[k], double(own_all), ku, sc[k], sf);
+          if (better(gk, key[k], bg, bc)) bg = gk, bc = key[k], bk = val[k];
         }
       }
     } else {
-      rank_live<kBatch, DRY>(x, tab, live, n, threadIdx.x, kBlockThreads, double(own_all), ku, sf, bg, bc, bk);
+      rank_live<kBatch, DRY>(x, tab, live, n, lt, ST, double(own_all), ku, sf, bg, bc, bk);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -1071,23 +1087,23 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
       const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
       if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
     }
-    if (lane == 0) red_g[wid] = bg, red_c[wid] = bc, red_k[wid] = bk;
-    __syncthreads();
+    if (lane == 0) red_g[g][wid] = bg, red_c[g][wid] = bc, red_k[g][wid] = bk;
+    sub_sync<SUB>(g);
     if (!rows_sorted)
-      for (u32 j = threadIdx.x; j < n; j += kBlockThreads) tab.clear(live[j]);
-    if (threadIdx.x == 0) {
+      for (u32 j = lt; j < n; j += ST) tab.clear(live[j]);
+    if (lt == 0) {
       for (int k = 1; k < W; ++k)
-        if (better(red_g[k], red_c[k], bg, bc)) bg = red_g[k], bc = red_c[k], bk = red_k[k];
-      nlive = 0;
+        if (better(red_g[g][k], red_c[g][k], bg, bc)) bg = red_g[g][k], bc = red_c[g][k], bk = red_k[g][k];
+      nlive[g] = 0;
       ++tl.verts;
       tl.arcs += d;
       tl.rand += d + n;
-      bcast = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own_all), tl);
+      bcast[g] = decide<DRY>(x, u, from, ku, bc, bg, bk, double(own_all), tl);
     }
-    __syncthreads();
-    if (!DRY && bcast && x.prune)
-      for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) x.flags[x.g.tgt[a]] = 1, ++tl.rand;
-    __syncthreads();
+    sub_sync<SUB>(g);
+    if (!DRY && bcast[g] && x.prune)
+      for (u64 a = lo + lt; a < lo + d; a += ST) x.flags[x.g.tgt[a]] = 1, ++tl.rand;
+    sub_sync<SUB>(g);
   }
   tl.flush(x);
 }
@@ -1366,12 +1382,25 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         break;
       }
       case kBinBlock: {
-        auto k = lm_block<Tab, DRY>;
+        // rows of <= kBlockSplit arcs: four sub-groups per block; longer rows:
+        // the whole block (both kernels walk the bin's list, each takes its rows)
         constexpr size_t smem = block_stage_smem<Tab>();
-        static const int occ = (set_smem(k, smem), occupancy(k, kBlockThreads, smem));
-        MoveArgs ab = a;
-        ab.chunk = std::min(a.chunk, a.hub_chunk);
-        launch_chunks(k, ab, b.of(bin), b.count(bin), kBlockThreads, 1, u64(sms) * occ, smem, s);
+        auto k4 = lm_block<Tab, DRY, 4>;
+        auto k1 = lm_block<Tab, DRY, 1>;
+        static const int occ4 = (set_smem(k4, smem), occupancy(k4, kBlockThreads, smem));
+        static const int occ1 = (set_smem(k1, smem), occupancy(k1, kBlockThreads, smem));
+        const u64 chunk = std::min(a.chunk, a.hub_chunk);
+        const u32* list = b.of(bin);
+        const u64 cnt = b.count(bin);
+        for (u64 off = 0; off < cnt; off += chunk) {
+          const u64 c = std::min<u64>(chunk, cnt - off);
+          const u64 b4 = std::max<u64>(1, std::min<u64>((c + 3) / 4, u64(sms) * occ4));
+          k4<<<unsigned(b4), kBlockThreads, smem, s>>>(a, list + off, c, 0, kBlockSplit);
+          LVN_LAUNCH();
+          const u64 b1 = std::max<u64>(1, std::min<u64>(c, u64(sms) * occ1));
+          k1<<<unsigned(b1), kBlockThreads, smem, s>>>(a, list + off, c, kBlockSplit, ~u64(0));
+          LVN_LAUNCH();
+        }
         break;
       }
       case kBinGlobal: {

@@ -90,15 +90,35 @@ __device__ __forceinline__ void segmented_runs(const u32 (&key)[K], V (&val)[K],
   for (int r = 0; r < K; ++r) tail[r] = r + 1 < K ? head[r + 1] : (lane == G - 1 || next_head);
 }
 
-// Warp-level pre-combine of one (key, value) per lane before a table insert:
-// when a key other than kEmpty repeats across the warp, the 32 pairs are
-// sorted by key and each run summed. Returns true on the lanes that hold a
-// distinct key's total (never for kEmpty), so each key is inserted once per
-// round instead of once per arc (shared-memory atomics serialise per lane,
-// and same-key CAS loops serialise per address).
+// Warp-level pre-combine of one (key, value) per lane before a table insert,
+// for lanes holding consecutive elements of a row. First, runs of equal
+// adjacent keys are summed (segmented Hillis-Steele scan over the run heads;
+// about 20 instructions): a row stored sorted by target whose neighbours share
+// communities (hosts, blocks) keeps one value per run. If a key still repeats
+// across the remaining run totals (more than 8 of them: unordered rows; one
+// match.any tells; few hot communities), the 32 pairs are sorted by key and
+// summed per run, so
+// each distinct key is inserted once: same-key inserts serialise per lane in
+// shared memory and per address in L2. Returns true on the lanes that hold a
+// distinct key's total (never for kEmpty).
 template <class V>
 __device__ __forceinline__ bool warp_combine(u32& key, V& val, u32 lane) {
   constexpr u32 FULL = 0xffffffffu;
+  const u32 up = __shfl_up_sync(FULL, key, 1);
+  const u32 dn = __shfl_down_sync(FULL, key, 1);
+  const u32 heads = __ballot_sync(FULL, lane == 0 || up != key);
+  const u32 start = 31u - __clz(heads & (FULL >> (31u - lane)));  // this lane's run head
+  V x = val;
+#pragma unroll
+  for (u32 d = 1; d < 32; d <<= 1) {
+    const V y = __shfl_up_sync(FULL, x, d);
+    if (lane >= start + d) x += y;
+  }
+  const bool tail = (lane == 31 || dn != key) && key != kEmpty;
+  key = tail ? key : kEmpty;
+  val = tail ? x : V(0);
+  // few run totals left: inserting them directly beats the repeat check
+  if (__popc(__ballot_sync(FULL, tail)) <= 8) return tail;
   const u32 peers = __match_any_sync(FULL, key);
   if (__any_sync(FULL, key != kEmpty && peers != (1u << lane))) {
     u32 kk[1] = {key};
