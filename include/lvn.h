@@ -111,8 +111,9 @@ typedef struct lvn_params {
    * lower (concurrent symmetric pairs merge instead of swapping labels) */
   int singleton_rule;
   /* lvn_louvain_sharded: a pass is sharded across the ranks while its graph
-   * has at least 2^shard_min_arcs_log2 arcs; smaller graphs run whole on
-   * every rank (the collapse of SURVEY.md 8(e)) */
+   * has at least 2^shard_min_arcs_log2 arcs; a smaller graph is gathered
+   * onto rank 0, which runs the remaining passes alone (the collapse of
+   * SURVEY.md 8(e)) */
   int shard_min_arcs_log2;      /* 22 */
   /* lvn_louvain_sharded: each rank sweeps its rows in this many consecutive
    * rounds per iteration, exchanging Sigma / C / marks after each (more
@@ -159,8 +160,9 @@ typedef struct lvn_result {
   lvn_phase_stats stats[LVN_STAT_COUNT];
   int membership_on_device;
   int num_shards;         /* ranks of lvn_louvain_sharded (1 otherwise) */
-  int sharded_passes;     /* passes run sharded (the rest ran whole on every rank) */
-  double exchange_seconds; /* host time inside the collectives */
+  int sharded_passes;     /* passes run sharded (the rest ran on rank 0 after the collapse) */
+  double exchange_seconds; /* time inside the collectives (host time of caller callbacks,
+                             device time of the library's NCCL collectives) */
   int num_levels;          /* dendrogram levels kept (lvn_params.keep_levels), else 0 */
   uint32_t** levels;       /* host arrays, level k has vertices_per_pass[k] entries */
 } lvn_result;
@@ -227,19 +229,28 @@ int lvn_probe_moves(const lvn_csr* g, const uint32_t* membership, const double* 
                     int force_kernel, uint32_t* to, double* gain);
 
 /* ---- sharded multi-GPU run -------------------------------
- * One process per GPU, each calling lvn_louvain_sharded on the same graph (its
- * own device copy, or host input it uploads). A sharded pass gives rank r the
- * rows [bounds[r], bounds[r+1]) of lvn_partition_rows: it decides the moves of
- * those vertices against replicated membership C and community weights Sigma
- * in shard_rounds consecutive rounds per iteration; after each round the ranks
- * allgather their move records (u, to) and every rank applies the others'
- * (C, Sigma, neighbour marks); gain and counters are allreduced once per
- * iteration. Aggregation emits the super-rows of a community range per rank
- * and allgathers them. Passes whose graph has fewer than 2^shard_min_arcs_log2
- * arcs run whole on every rank. The collectives are supplied by the caller
- * (paper_2501_19004_b200.distributed wraps torch.distributed / NCCL): buffers
- * are device pointers on this process's GPU, the library's stream is idle
- * when a callback runs, and a callback returns 0 once its result is in place. */
+ * One process per GPU, each calling lvn_louvain_sharded with the same graph
+ * view (host or device arrays; rank r reads only its own slice of them).
+ * Storage is sharded: a pass gives rank r the rows [b_r, b_{r+1}) of
+ * lvn_partition_rows (pass 0) or of its community range (later passes), and
+ * the rank holds only those rows' targets and weights, plus replicated
+ * per-vertex state (membership C, K, Sigma, pruning marks; 21 B / vertex).
+ * Per local-moving iteration it sweeps its rows in shard_rounds consecutive
+ * rounds; after each round the ranks allgather their move records (u, to)
+ * and apply the others' (C, Sigma); gain / counters are allreduced and the
+ * pruning marks OR-reduced once per iteration. Aggregation is by own rows:
+ * each rank sums its arcs into partial super-edges (fp64), routes them to the
+ * owner of their super-row (all-to-all) and the owner merges them into its
+ * rows of the next graph. Once a pass's graph has fewer than
+ * 2^shard_min_arcs_log2 arcs it is gathered onto rank 0, which runs the
+ * remaining passes alone (the collapse); the final membership and modularity
+ * reach every rank, so all ranks return the same result.
+ * Collectives come from lvn_comm: the library's own NCCL communicator
+ * (lvn_comm_nccl_create: stream-ordered, no host synchronisation) or caller
+ * callbacks (paper_2501_19004_b200.distributed wraps torch.distributed for
+ * the gloo tests): buffers are device pointers on this process's GPU, the
+ * library's stream is idle when a callback runs, and a callback returns 0
+ * once its result is in place. */
 enum lvn_dtype { LVN_U8 = 0, LVN_U32 = 1, LVN_U64 = 2, LVN_F64 = 3 };
 enum lvn_redop { LVN_SUM = 0, LVN_MAX = 1 };
 typedef struct lvn_comm {
@@ -252,8 +263,26 @@ typedef struct lvn_comm {
    * receives the contributions concatenated in rank order; send may lie
    * inside recv at its own rank's position */
   int (*allgatherv)(void* user, const void* send, void* recv, const uint64_t* counts);
+  /* all-to-all of bytes: send holds the blocks for ranks 0..size-1 back to
+   * back (send_counts[k] bytes for rank k), recv receives the blocks from
+   * ranks 0..size-1 back to back (recv_counts[k] bytes from rank k) */
+  int (*alltoallv)(void* user, const void* send, const uint64_t* send_counts, void* recv,
+                   const uint64_t* recv_counts);
 } lvn_comm;
 int lvn_louvain_sharded(const lvn_csr* g, const lvn_params* p, const lvn_comm* comm, lvn_result** out);
+
+/* Library-owned NCCL communicator (one process per GPU, NVLink / NVSwitch).
+ * Rank 0 calls lvn_nccl_unique_id and ships the bytes to the other ranks by
+ * any side channel (torchrun store, MPI, a file); every rank then calls
+ * lvn_comm_nccl_create on its own device (lvn_init first). Passed to
+ * lvn_louvain_sharded, its collectives are enqueued on the engine stream with
+ * no host synchronisation; its public callbacks also work standalone
+ * (synchronous). NCCL is loaded at run time (libnccl.so.2). */
+#define LVN_NCCL_ID_BYTES 128
+int lvn_nccl_version(int* version);
+int lvn_nccl_unique_id(unsigned char id[LVN_NCCL_ID_BYTES]);
+int lvn_comm_nccl_create(int rank, int size, const unsigned char id[LVN_NCCL_ID_BYTES], lvn_comm** out);
+int lvn_comm_destroy(lvn_comm* comm);
 /* rows [0, n) cut into `parts` contiguous ranges of about A/parts arcs each:
  * bounds[k] = the first row whose offset reaches floor(k A / parts), bounds[parts] = n
  * (host offsets; the engine applies the same rule on the device) */

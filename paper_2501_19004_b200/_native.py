@@ -116,6 +116,8 @@ LVN_U8, LVN_U32, LVN_U64, LVN_F64 = 0, 1, 2, 3
 LVN_SUM, LVN_MAX = 0, 1
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_uint64, C.c_int, C.c_int)
 ALLGATHERV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64))
+ALLTOALLV_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.POINTER(C.c_uint64), C.c_void_p,
+                           C.POINTER(C.c_uint64))
 
 
 class lvn_comm(C.Structure):
@@ -125,6 +127,7 @@ class lvn_comm(C.Structure):
         ("user", C.c_void_p),
         ("allreduce", ALLREDUCE_FN),
         ("allgatherv", ALLGATHERV_FN),
+        ("alltoallv", ALLTOALLV_FN),
     ]
 
 
@@ -153,6 +156,7 @@ EXPORTS = (
     "lvn_aggregate", "lvn_evaluate_moves", "lvn_probe_moves", "lvn_generate", "lvn_dgraph_upload", "lvn_dgraph_view",
     "lvn_dgraph_download", "lvn_dgraph_free", "lvn_device_alloc", "lvn_device_free", "lvn_memcpy",
     "lvn_louvain_sharded", "lvn_partition_rows", "lvn_build_csr",
+    "lvn_nccl_version", "lvn_nccl_unique_id", "lvn_comm_nccl_create", "lvn_comm_destroy",
 )
 
 _lib = None
@@ -191,6 +195,10 @@ def lib() -> C.CDLL:
         L.lvn_louvain_sharded.argtypes = [C.POINTER(lvn_csr), C.POINTER(lvn_params), C.POINTER(lvn_comm),
                                           C.POINTER(C.POINTER(lvn_result))]
         L.lvn_partition_rows.argtypes = [vp, C.c_uint32, i, vp]
+        L.lvn_nccl_version.argtypes = [C.POINTER(i)]
+        L.lvn_nccl_unique_id.argtypes = [vp]
+        L.lvn_comm_nccl_create.argtypes = [i, i, vp, C.POINTER(C.POINTER(lvn_comm))]
+        L.lvn_comm_destroy.argtypes = [C.POINTER(lvn_comm)]
     L.lvn_modularity.argtypes = [C.POINTER(lvn_csr), vp, i, C.POINTER(C.c_double)]
     L.lvn_vertex_weights.argtypes = [C.POINTER(lvn_csr), vp]
     L.lvn_count_communities.argtypes = [vp, C.c_uint64, i, C.POINTER(C.c_uint32)]

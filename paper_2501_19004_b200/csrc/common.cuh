@@ -33,6 +33,9 @@ struct Error {
   std::string what;
 };
 
+// lvn_last_error() text of this thread (engine.cu)
+void set_error(const std::string& what);
+
 [[noreturn]] inline void fail(int code, const std::string& what) { throw Error{code, what}; }
 
 inline void cuda_check(cudaError_t e, const char* expr, const char* file, int line) {

@@ -10,8 +10,10 @@
 #include <string>
 #include <vector>
 
+#include "comm.hpp"
 #include "kernels.cuh"
 #include "lvn.h"
+#include "shard.hpp"
 
 namespace lvn {
 
@@ -466,21 +468,67 @@ std::vector<u32> split_rows(const u64* off, u32 n, int parts, cudaStream_t s) {
 
 struct Comm {
   const lvn_comm* c = nullptr;
-  double seconds = 0.0;
+  NcclComm* nc = nullptr;  // library-owned NCCL communicator: stream-ordered, no host sync
+  double seconds = 0.0;    // host time inside caller collectives / device time of NCCL ones
+  std::vector<cudaEvent_t> ev;  // NCCL: (begin, end) event pairs, summed at the end of the run
   bool on() const { return c && c->size > 1; }
   int rank() const { return c ? c->rank : 0; }
   int size() const { return c ? c->size : 1; }
+  void mark(cudaStream_t s) {
+    cudaEvent_t e;
+    LVN_CUDA(cudaEventCreate(&e));
+    LVN_CUDA(cudaEventRecord(e, s));
+    ev.push_back(e);
+  }
   void allreduce(void* buf, u64 count, int dtype, int op, cudaStream_t s) {
+    if (nc) {
+      mark(s);
+      nccl_allreduce(nc, buf, count, dtype, op, s);
+      mark(s);
+      return;
+    }
     LVN_CUDA(cudaStreamSynchronize(s));
     const auto t0 = Clock::now();
     if (c->allreduce(c->user, buf, count, dtype, op) != 0) fail(kCuda, "allreduce collective failed");
     seconds += since(t0);
   }
   void allgatherv(const void* send, void* recv, const std::vector<u64>& counts, cudaStream_t s) {
+    if (nc) {
+      mark(s);
+      nccl_allgatherv(nc, send, recv, counts.data(), s);
+      mark(s);
+      return;
+    }
     LVN_CUDA(cudaStreamSynchronize(s));
     const auto t0 = Clock::now();
     if (c->allgatherv(c->user, send, recv, counts.data()) != 0) fail(kCuda, "allgatherv collective failed");
     seconds += since(t0);
+  }
+  void alltoallv(const void* send, const std::vector<u64>& scnt, void* recv, const std::vector<u64>& rcnt,
+                 cudaStream_t s) {
+    if (nc) {
+      mark(s);
+      nccl_alltoallv(nc, send, scnt.data(), recv, rcnt.data(), s);
+      mark(s);
+      return;
+    }
+    if (!c->alltoallv) fail(kInvalid, "lvn_comm without alltoallv: sharded aggregation needs it");
+    LVN_CUDA(cudaStreamSynchronize(s));
+    const auto t0 = Clock::now();
+    if (c->alltoallv(c->user, send, scnt.data(), recv, rcnt.data()) != 0) fail(kCuda, "alltoallv collective failed");
+    seconds += since(t0);
+  }
+  // device time of the NCCL collectives (the stream is idle when called)
+  void settle() {
+    for (size_t i = 0; i + 1 < ev.size(); i += 2) {
+      float ms = 0.f;
+      if (cudaEventElapsedTime(&ms, ev[i], ev[i + 1]) == cudaSuccess) seconds += ms * 1e-3;
+    }
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    ev.clear();
+  }
+  ~Comm() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
   }
 };
 
@@ -508,13 +556,8 @@ bool verbose() {
 }
 
 // ---- aggregation of a graph by a contiguous membership ----------------------
-// With a sharding comm, rank r emits the super-rows of communities
-// [cb[r], cb[r+1]) (split by member-degree budget) and the ranks allgather the
-// row lengths and then the rows, so every rank ends with the whole super-graph.
 void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
-                      u32* err, cudaStream_t s, bool canonical, Comm* comm = nullptr,
-                      const Bins* gbins = nullptr) {
-  const bool sh = comm && comm->on();
+                      u32* err, cudaStream_t s, bool canonical, const Bins* gbins = nullptr) {
   DBuf<u32> msize(count ? count : 1);
   DBuf<u64> budget(count + 1), coff(count + 1), boff(count + 1), hoff(count + 1), capped(count + 1),
       ext(count + 1);
@@ -538,14 +581,8 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   DBuf<u32> members(g.n ? g.n : 1), cursor(count ? count : 1);
   community_scatter(C, g.n, coff.p, count, cursor.p, members.p, s);
   msize.release();
-  std::vector<u32> cb;
-  u32 c0 = 0, c1 = count;
-  if (sh) {
-    cb = split_rows(boff.p, count, comm->size(), s);
-    c0 = cb[comm->rank()], c1 = cb[comm->rank() + 1];
-  }
   Bins ab;
-  compute_bins(boff.p + c0, c1 - c0, e, ab, s, ~u64(0), c0);  // synchronises
+  compute_bins(boff.p, count, e, ab, s);  // synchronises
   if (verbose()) {
     std::fprintf(stderr, "[lvn] aggregate %u communities, budget bins:", count);
     for (int b = 0; b < kBins; ++b) std::fprintf(stderr, " %llu", (unsigned long long)ab.count(b));
@@ -601,16 +638,7 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
                             std::to_string(h_coff[c + 1] - h_coff[c]) + ")");
     }
   }
-  // rows of other ranks' communities stay empty in `fill`; `fill_all` holds every row
-  DBuf<u32> fill_all;
   const u32* rows = fill.p;
-  if (sh) {
-    fill_all.alloc(count ? count : 1);
-    std::vector<u64> bytes(comm->size());
-    for (int k = 0; k < comm->size(); ++k) bytes[k] = 4ull * (cb[k + 1] - cb[k]);
-    comm->allgatherv(fill.p + c0, fill_all.p, bytes, s);
-    rows = fill_all.p;
-  }
   DBuf<u64> noff(count + 1);
   exclusive_scan_u32_to_u64(rows, noff.p, count, s);
   const u64 A = read_scalar(noff.p + count, s);
@@ -621,19 +649,6 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   out.w.alloc(A ? A : 1);
   DBuf<double> tw(1);
   compact_rows(hoff.p, htgt.p, hw.p, fill.p, out.off.p, count, out.tgt.p, out.w.p, tw.p, s);
-  if (sh) {
-    std::vector<u64> at(comm->size() + 1);
-    for (int k = 0; k <= comm->size(); ++k)
-      LVN_CUDA(cudaMemcpyAsync(ctx().pinned + k, out.off.p + cb[k], sizeof(u64), cudaMemcpyDeviceToHost, s));
-    LVN_CUDA(cudaStreamSynchronize(s));
-    for (int k = 0; k <= comm->size(); ++k) at[k] = ctx().pinned[k];
-    std::vector<u64> tb(comm->size()), wb(comm->size());
-    for (int k = 0; k < comm->size(); ++k) tb[k] = 4ull * (at[k + 1] - at[k]), wb[k] = tb[k];
-    const u64 mine = at[comm->rank()];
-    comm->allgatherv(out.tgt.p + mine, out.tgt.p, tb, s);
-    comm->allgatherv(out.w.p + mine, out.w.p, wb, s);
-    comm->allreduce(tw.p, 1, LVN_F64, LVN_SUM, s);
-  }
   if (canonical && A) {
     DBuf<u32> mx(1);
     reduce_max_u32(rows, count, mx.p, s);
@@ -647,6 +662,165 @@ double modularity_device(const DGraph& g, const Bins& b, const u32* C, u64 width
                          cudaStream_t s) {
   DBuf<double> tot(width ? width : 1), sums(2);
   modularity_terms(g, b, C, tot.p, width, sums.p, s, 2.0 * m);
+  double* h = reinterpret_cast<double*>(ctx().pinned);
+  LVN_CUDA(cudaMemcpyAsync(h, sums.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  return h[0] / (2.0 * m) - h[1];
+}
+
+// ---- sharded storage (lvn_louvain_sharded) --------------------------------------
+// Rank `rank` of `size` keeps the rows [v0, v1) of the input (lvn_partition_rows
+// rule): full-length offsets with the other rows empty, and only its own
+// targets / weights (borrowed slices of device input, uploaded slices of host input).
+void load_graph_shard(const lvn_csr* in, int rank, int size, cudaStream_t s, InGraph& out, u32& v0, u32& v1,
+                      double* h2d_seconds) {
+  check_csr_header(in);
+  const u32 n = in->num_vertices;
+  out.m = in->total_weight;
+  std::vector<u32> b(size + 1);
+  out.off.alloc(u64(n) + 1);
+  const auto t0 = Clock::now();
+  if (in->location == LVN_DEVICE) {
+    b = split_rows(in->offsets, n, size, s);
+  } else {
+    if (in->offsets[0] != 0 || in->offsets[n] != in->num_arcs)
+      fail(kInvalid, "offsets must start at 0 and end at num_arcs");
+    lvn_partition_rows(in->offsets, n, size, b.data());
+  }
+  v0 = b[rank], v1 = b[rank + 1];
+  const u64* goff = in->offsets;
+  DBuf<u64> up;
+  if (in->location != LVN_DEVICE) {
+    up.alloc(u64(n) + 1);
+    LVN_CUDA(cudaMemcpyAsync(up.p, in->offsets, (u64(n) + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+    goff = up.p;
+  }
+  shard_offsets(goff, n, v0, v1, out.off.p, s);
+  u64 a0, a1;
+  if (in->location == LVN_DEVICE) {
+    LVN_CUDA(cudaMemcpyAsync(ctx().pinned, in->offsets + v0, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaMemcpyAsync(ctx().pinned + 1, in->offsets + v1, sizeof(u64), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    a0 = ctx().pinned[0], a1 = ctx().pinned[1];
+    out.g = DGraph{n, a1 - a0, out.off.p, in->targets + a0, in->weights + a0};
+    return;
+  }
+  a0 = in->offsets[v0], a1 = in->offsets[v1];
+  const u64 a = a1 - a0;
+  out.tgt.alloc(a ? a : 1);
+  out.w.alloc(a ? a : 1);
+  if (a) {
+    LVN_CUDA(cudaMemcpyAsync(out.tgt.p, in->targets + a0, a * sizeof(u32), cudaMemcpyHostToDevice, s));
+    LVN_CUDA(cudaMemcpyAsync(out.w.p, in->weights + a0, a * sizeof(float), cudaMemcpyHostToDevice, s));
+  }
+  LVN_CUDA(cudaStreamSynchronize(s));
+  if (h2d_seconds) *h2d_seconds += since(t0);
+  out.g = DGraph{n, a, out.off.p, out.tgt.p, out.w.p};
+}
+
+// every rank gets rank 0's n elements of buf (device)
+void bcast_from0(Comm& cm, void* buf, u64 bytes, cudaStream_t s) {
+  std::vector<u64> counts(cm.size(), 0);
+  counts[0] = bytes;
+  cm.allgatherv(buf, buf, counts, s);
+}
+
+// Aggregation of a sharded pass by own rows (shard.cu): partial super-edges
+// routed to the owners of their super-rows, merged there. `out` receives this
+// rank's rows [cb[rank], cb[rank+1]) of the next graph (others empty);
+// cb = the next pass's row ranges, balanced by super-edge count.
+void aggregate_sharded(const DGraph& g, const u32* C, u32 count, u32 v0, u32 v1, Comm& cm, OwnedCsr& out,
+                       std::vector<u32>& cb, cudaStream_t s) {
+  const int P = cm.size(), me = cm.rank();
+  DBuf<ull> keys;
+  DBuf<double> vals;
+  const u64 m = partial_super_edges(g, C, v0, v1, keys, vals, s);
+  // super-edges per row over all ranks (upper bound of the merged row) -> row ranges
+  DBuf<u32> cnt(count ? count : 1);
+  super_row_counts(keys.p, m, count, cnt.p, s);
+  cm.allreduce(cnt.p, count, LVN_U32, LVN_SUM, s);
+  DBuf<u64> coff(u64(count) + 1);
+  exclusive_scan_u32_to_u64(cnt.p, coff.p, count, s);
+  cb = split_rows(coff.p, count, P, s);
+  // route the sorted entries: cut[k] = first entry of rank k's rows
+  DBuf<u32> dcb(P + 1);
+  DBuf<u64> cut(P + 1), mat(u64(P) * P);
+  std::memcpy(ctx().pinned, cb.data(), (P + 1) * sizeof(u32));
+  LVN_CUDA(cudaMemcpyAsync(dcb.p, ctx().pinned, (P + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
+  route_entries(keys.p, m, dcb.p, P, cut.p, s);
+  // entries this rank sends to each rank, then the whole P x P matrix
+  {
+    DBuf<u64> row(P);
+    std::vector<u64> h(P + 1);
+    LVN_CUDA(cudaMemcpyAsync(ctx().pinned, cut.p, (P + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(h.data(), ctx().pinned, (P + 1) * sizeof(u64));
+    for (int k = 0; k < P; ++k) ctx().pinned[k] = h[k + 1] - h[k];
+    LVN_CUDA(cudaMemcpyAsync(mat.p + u64(me) * P, ctx().pinned, P * sizeof(u64), cudaMemcpyHostToDevice, s));
+    cm.allgatherv(mat.p + u64(me) * P, mat.p, std::vector<u64>(P, 8ull * P), s);
+  }
+  std::vector<u64> M(u64(P) * P);
+  LVN_CUDA(cudaMemcpyAsync(ctx().pinned, mat.p, u64(P) * P * sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  std::memcpy(M.data(), ctx().pinned, u64(P) * P * sizeof(u64));
+  std::vector<u64> sk(P), sv(P), rk(P), rv(P);
+  u64 total = 0;
+  for (int k = 0; k < P; ++k) {
+    sk[k] = 8 * M[u64(me) * P + k], sv[k] = sk[k];
+    rk[k] = 8 * M[u64(k) * P + me], rv[k] = rk[k];
+    total += M[u64(k) * P + me];
+  }
+  DBuf<ull> rkeys(total ? total : 1);
+  DBuf<double> rvals(total ? total : 1);
+  cm.alltoallv(keys.p, sk, rkeys.p, rk, s);
+  cm.alltoallv(vals.p, sv, rvals.p, rv, s);
+  keys.release();
+  vals.release();
+  DBuf<double> tw(1);
+  merge_super_rows(rkeys, rvals, total, count, out, tw.p, s);
+  cm.allreduce(tw.p, 1, LVN_F64, LVN_SUM, s);
+  out.total_weight = read_scalar(tw.p, s) / 2.0;
+}
+
+// the whole graph on every rank from each rank's own rows (contiguous ranges
+// in rank order): row lengths summed over ranks, arcs gathered in rank order
+void gather_graph(OwnedCsr& g, Comm& cm, cudaStream_t s) {
+  const int P = cm.size();
+  const u32 n = g.n;
+  DBuf<u32> len(n ? n : 1);
+  row_lengths(g.off.p, n, len.p, s);
+  cm.allreduce(len.p, n, LVN_U32, LVN_SUM, s);
+  DBuf<u64> arcs(P);
+  LVN_CUDA(cudaMemcpyAsync(arcs.p + cm.rank(), &g.arcs, sizeof(u64), cudaMemcpyHostToDevice, s));
+  cm.allgatherv(arcs.p + cm.rank(), arcs.p, std::vector<u64>(P, 8), s);
+  std::vector<u64> a(P);
+  LVN_CUDA(cudaMemcpyAsync(ctx().pinned, arcs.p, P * sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  u64 A = 0;
+  for (int k = 0; k < P; ++k) a[k] = ctx().pinned[k], A += a[k];
+  OwnedCsr full;
+  full.n = n;
+  full.arcs = A;
+  full.total_weight = g.total_weight;
+  full.off.alloc(u64(n) + 1);
+  exclusive_scan_u32_to_u64(len.p, full.off.p, n, s);
+  full.tgt.alloc(A ? A : 1);
+  full.w.alloc(A ? A : 1);
+  std::vector<u64> bytes(P);
+  for (int k = 0; k < P; ++k) bytes[k] = 4 * a[k];
+  cm.allgatherv(g.tgt.p, full.tgt.p, bytes, s);
+  cm.allgatherv(g.w.p, full.w.p, bytes, s);
+  g = std::move(full);
+}
+
+// modularity of a sharded input: per-community terms of the own rows, summed over ranks
+double modularity_sharded(const DGraph& g, const Bins& b, const u32* C, u64 width, double m, Comm& cm,
+                          cudaStream_t s) {
+  DBuf<double> tot(width ? width : 1), sums(2);
+  modularity_rows(g, b, C, tot.p, width, sums.p, s);
+  cm.allreduce(tot.p, width, LVN_F64, LVN_SUM, s);
+  cm.allreduce(sums.p, 1, LVN_F64, LVN_SUM, s);
+  modularity_squares(tot.p, width, 2.0 * m, sums.p, s);
   double* h = reinterpret_cast<double*>(ctx().pinned);
   LVN_CUDA(cudaMemcpyAsync(h, sums.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
   LVN_CUDA(cudaStreamSynchronize(s));
@@ -726,9 +900,27 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   check_csr_header(in);
   const double m = in->total_weight;
   if (!(m > 0.0)) fail(kDegenerate, "cannot cluster a graph with zero total weight");
+  Comm solo;
+  Comm& cm = comm ? *comm : solo;
+  // Sharded runs: while a pass's graph has >= shard_min arcs
+  // every rank holds and sweeps only its own rows [v0, v1); below it the graph
+  // is gathered onto rank 0, which runs the rest alone (`idle` elsewhere).
+  const bool dist = cm.on();
+  const u64 shard_min = u64(1) << p.shard_min_arcs_log2;
+  bool sharded = dist && in->num_arcs >= shard_min;
+  const bool input_sharded = sharded;
+  bool idle = dist && !sharded && cm.rank() != 0;
+  bool collapsed = dist && !sharded;
+  const u32 N = in->num_vertices;
+  u32 v0 = 0, v1 = N;
   InGraph ig;
-  load_graph(in, s, ig, &r->h2d_seconds);
-  const u32 N = ig.g.n;
+  if (sharded) {
+    load_graph_shard(in, cm.rank(), cm.size(), s, ig, v0, v1, &r->h2d_seconds);
+  } else if (!idle) {
+    load_graph(in, s, ig, &r->h2d_seconds);
+  } else {
+    ig.g.n = N;
+  }
   const BinEdges edges = edges_of(p);
   Timing tm;
 
@@ -752,9 +944,6 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   std::vector<u32> vpp;
   std::vector<u64> app;
   int passes = 0, aggregations = 0, sharded_passes = 0;
-  Comm solo;
-  Comm& cm = comm ? *comm : solo;
-  Bins own_bins;
   DBuf<u32> mrec, mall, mcount;  // sharded: own move records (u, to), everyone's, per-rank counts
   struct Levels : std::vector<u32*> {  // dendrogram (p.keep_levels): local membership of every pass
     ~Levels() {
@@ -770,37 +959,79 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     levels.push_back(h);
   };
 
-  for (int pass = 0; pass < p.max_passes; ++pass) {
+  for (int pass = 0; pass < p.max_passes && !idle; ++pass) {
     const auto t_pass = Clock::now();
     const u32 nv = cur.n;
     Bins& B = pass == 0 ? in_bins : bins;
-    compute_bins(cur.off, nv, edges, B, s);
+    // sharded: the bins (and every sweep) cover the own rows only
+    if (sharded) compute_bins(cur.off + v0, v1 - v0, edges, B, s, ~u64(0), v0);
+    else compute_bins(cur.off, nv, edges, B, s);
     if (pass == 0) have_in_bins = true;
     size_t sp = tm.begin(LVN_STAT_RESET, s);
     pass_reset(cur, B, K.p, S.p, C.p, flags.p, s, uni.p);
     tm.end(sp, s, 4.0 * double(cur.arcs) + 29.0 * nv);
+    if (sharded) {
+      // K of every vertex from its owner; Sigma = K (singletons)
+      std::vector<u32> vb(cm.size() + 1);
+      std::vector<u64> kb(cm.size());
+      {
+        DBuf<u32> rb(cm.size() + 1);
+        std::vector<u64> four(cm.size(), 4);
+        LVN_CUDA(cudaMemcpyAsync(rb.p + cm.rank(), &v0, sizeof(u32), cudaMemcpyHostToDevice, s));
+        cm.allgatherv(rb.p + cm.rank(), rb.p, four, s);
+        LVN_CUDA(cudaMemcpyAsync(c.pinned, rb.p, cm.size() * sizeof(u32), cudaMemcpyDeviceToHost, s));
+        LVN_CUDA(cudaStreamSynchronize(s));
+        const u32* h = reinterpret_cast<const u32*>(c.pinned);
+        for (int k = 0; k < cm.size(); ++k) vb[k] = h[k];
+        vb[cm.size()] = nv;
+      }
+      for (int k = 0; k < cm.size(); ++k) kb[k] = 8ull * (vb[k + 1] - vb[k]);
+      cm.allgatherv(K.p + v0, K.p, kb, s);
+      LVN_CUDA(cudaMemcpyAsync(S.p, K.p, size_t(nv) * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    }
     // uniform arc weights (every unit-weight input's first pass): the sort
     // bins key on the community alone (LVN_UNIFORM=0 disables)
     bool uniform = false;
     float uniform_w = 0.f;
-    if (cur.arcs && !no_uniform()) {
-      uniform = read_scalar(uni.p, s) != 0;
-      if (uniform) uniform_w = read_scalar(cur.w, s);
+    if (!no_uniform()) {
+      if (sharded) {
+        // uniform on every rank, with the same weight: [0] = some rank differs,
+        // [1] = max weight bits, [2] = max of the complemented bits
+        DBuf<u32> u3(3);
+        const u32 mine = read_scalar(uni.p, s);
+        u32 h3[3];
+        float wf = 0.f;
+        if (cur.arcs) {
+          LVN_CUDA(cudaMemcpyAsync(c.pinned, cur.w, sizeof(float), cudaMemcpyDeviceToHost, s));
+          LVN_CUDA(cudaStreamSynchronize(s));
+          std::memcpy(&wf, c.pinned, sizeof(float));
+        }
+        u32 wb;
+        std::memcpy(&wb, &wf, sizeof(u32));
+        h3[0] = cur.arcs && mine == 0 ? 1u : 0u;
+        h3[1] = cur.arcs ? wb : 0u;
+        h3[2] = cur.arcs ? ~wb : 0u;
+        std::memcpy(c.pinned, h3, sizeof(h3));
+        LVN_CUDA(cudaMemcpyAsync(u3.p, c.pinned, sizeof(h3), cudaMemcpyHostToDevice, s));
+        cm.allreduce(u3.p, 3, LVN_U32, LVN_MAX, s);
+        LVN_CUDA(cudaMemcpyAsync(c.pinned, u3.p, sizeof(h3), cudaMemcpyDeviceToHost, s));
+        LVN_CUDA(cudaStreamSynchronize(s));
+        std::memcpy(h3, c.pinned, sizeof(h3));
+        uniform = h3[0] == 0 && h3[1] == ~h3[2];
+        if (uniform) std::memcpy(&uniform_w, &h3[1], sizeof(float));
+      } else if (cur.arcs) {
+        uniform = read_scalar(uni.p, s) != 0;
+        if (uniform) uniform_w = read_scalar(cur.w, s);
+      }
     }
 
-    // sharded pass: this rank decides the rows [v0, v1)
-    const bool shard = cm.on() && cur.arcs >= (u64(1) << p.shard_min_arcs_log2);
-    u32 v0 = 0, v1 = nv;
-    std::vector<u32> vb;
+    const bool shard = sharded;
     if (shard) {
-      vb = split_rows(cur.off, nv, cm.size(), s);
-      v0 = vb[cm.rank()], v1 = vb[cm.rank() + 1];
-      compute_bins(cur.off + v0, v1 - v0, edges, own_bins, s, ~u64(0), v0);
       mrec.ensure(2 * u64(std::max<u32>(v1 - v0, 1)));
       mcount.ensure(cm.size() + 1);
       ++sharded_passes;
     }
-    Bins& SB = shard ? own_bins : B;
+    Bins& SB = B;
     MoveArgs a;
     a.g = cur;
     a.C = C.p;
@@ -863,8 +1094,9 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
         move_sweep(a, views[k], p.value_bits, s);
         tm.end(sp, s, 0.0);
         if (shard) {
-          // every rank applies the other ranks' moves of this round (C, Sigma,
-          // neighbour marks) from their (u, to) records
+          // every rank applies the other ranks' moves of this round (C, Sigma)
+          // from their (u, to) records; marks of remote movers' neighbours are
+          // OR-reduced at the end of the iteration
           std::vector<u64> four(cm.size(), 4);
           cm.allgatherv(a.moves_n, mcount.p, four, s);
           u32* hn = reinterpret_cast<u32*>(c.pinned);
@@ -877,10 +1109,11 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
             bytes[j] = 8ull * hn[j];
             total += hn[j];
           }
+          const u64 own_n = hn[cm.rank()];
           if (total) {
             mall.ensure(2 * total);
             cm.allgatherv(mrec.p, mall.p, bytes, s);
-            apply_moves(mall.p, total, mine, mine + hn[cm.rank()], cur, C.p, K.p, S.p, flags.p, p.prune, s);
+            apply_moves(mall.p, total, mine, mine + own_n, cur, C.p, K.p, S.p, flags.p, 0, s);
           }
         }
       }
@@ -888,6 +1121,10 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       if (shard) {
         cm.allreduce(&rec.p->gain, 1, LVN_F64, LVN_SUM, s);
         cm.allreduce(&rec.p->verts, 4, LVN_U64, LVN_SUM, s);
+        if (p.prune) {
+          cm.allreduce(flags.p, nv, LVN_U8, LVN_MAX, s);
+          zero_outside(flags.p, nv, v0, v1, s);
+        }
       }
       if (p.prune)
         for (int k = 0; k < R; ++k)
@@ -944,9 +1181,28 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     const auto t1 = Clock::now();
     OwnedCsr& next = owned[pass & 1];
     sp = tm.begin(LVN_STAT_AGGREGATE, s);
-    aggregate_device(cur, C.p, count, edges, next, err.p, s, false, shard ? &cm : nullptr, &B);
+    if (shard) {
+      std::vector<u32> cb;
+      aggregate_sharded(cur, C.p, count, v0, v1, cm, next, cb, s);
+      v0 = cb[cm.rank()], v1 = cb[cm.rank() + 1];
+    } else {
+      aggregate_device(cur, C.p, count, edges, next, err.p, s, false, &B);
+    }
     tm.end(sp, s, 12.0 * double(cur.arcs) + 16.0 * nv + 8.0 * double(next.arcs) + 8.0 * (count + 1.0),
            nv, cur.arcs);
+    if (shard) {
+      // the collapse: a graph below shard_min continues on rank 0 alone
+      DBuf<u64> ta(1);
+      LVN_CUDA(cudaMemcpyAsync(ta.p, &next.arcs, sizeof(u64), cudaMemcpyHostToDevice, s));
+      cm.allreduce(ta.p, 1, LVN_U64, LVN_SUM, s);
+      if (read_scalar(ta.p, s) < shard_min) {
+        gather_graph(next, cm, s);
+        sharded = false;
+        collapsed = true;
+        idle = cm.rank() != 0;
+        v0 = 0, v1 = count;
+      }
+    }
     t_aggregate += since(t1);
     cur = next.view();
     check_graph("aggregated graph", cur, s);
@@ -958,14 +1214,48 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   }
   check_err(err.p, s);
 
+  // sharded runs: rank 0's membership (it ran the passes after the collapse alone)
+  if (dist && collapsed) bcast_from0(cm, global.p, 4ull * N, s);
   // final renumber (louvain_compact.cpp:394) and modularity on the input graph (:396)
   size_t sp = tm.begin(LVN_STAT_RENUMBER, s);
   const u32 count = renumber_device(global.p, N, N, used, rank, s, true);
   tm.end(sp, s, 24.0 * N);
-  if (!have_in_bins) compute_bins(ig.g.off, N, edges, in_bins, s);
+  double q = 0.0;
   sp = tm.begin(LVN_STAT_MODULARITY, s);
-  const double q = modularity_device(ig.g, in_bins, global.p, count, m, s);
+  if (input_sharded) {
+    if (!have_in_bins) compute_bins(ig.g.off + v0, v1 - v0, edges, in_bins, s, ~u64(0), v0);
+    q = modularity_sharded(ig.g, in_bins, global.p, count, m, cm, s);
+  } else if (!idle || !dist) {
+    if (!have_in_bins) compute_bins(ig.g.off, N, edges, in_bins, s);
+    q = modularity_device(ig.g, in_bins, global.p, count, m, s);
+  }
   tm.end(sp, s, 12.0 * double(ig.g.arcs) + 12.0 * N, N, ig.g.arcs);
+  if (dist) {
+    // every rank reports rank 0's run: Q and the per-pass record
+    const int MP = p.max_passes;
+    const size_t words = 3 + 4 * size_t(MP);
+    std::vector<double> pk(words, 0.0);
+    pk[0] = q, pk[1] = passes, pk[2] = aggregations;
+    for (int i = 0; i < passes && i < MP; ++i) {
+      pk[3 + i] = its[i], pk[3 + MP + i] = tols[i], pk[3 + 2 * MP + i] = vpp[i], pk[3 + 3 * MP + i] = double(app[i]);
+    }
+    DBuf<double> dpk(words);
+    std::memcpy(c.pinned, pk.data(), words * sizeof(double));
+    LVN_CUDA(cudaMemcpyAsync(dpk.p, c.pinned, words * sizeof(double), cudaMemcpyHostToDevice, s));
+    bcast_from0(cm, dpk.p, words * sizeof(double), s);
+    LVN_CUDA(cudaMemcpyAsync(c.pinned, dpk.p, words * sizeof(double), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    std::memcpy(pk.data(), c.pinned, words * sizeof(double));
+    q = pk[0];
+    if (cm.rank() != 0) {
+      passes = int(pk[1]), aggregations = int(pk[2]);
+      its.assign(passes, 0), tols.assign(passes, 0.0), vpp.assign(passes, 0), app.assign(passes, 0);
+      pass_secs.resize(passes, 0.0);
+      for (int i = 0; i < passes; ++i)
+        its[i] = int(pk[3 + i]), tols[i] = pk[3 + MP + i], vpp[i] = u32(pk[3 + 2 * MP + i]),
+        app[i] = u64(pk[3 + 3 * MP + i]);
+    }
+  }
 
   r->num_vertices = N;
   r->num_communities = count;
@@ -1007,6 +1297,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     for (size_t i = 0; i < levels.size(); ++i) r->levels[i] = levels[i];
     levels.clear();
   }
+  cm.settle();
   r->num_shards = cm.size();
   r->sharded_passes = sharded_passes;
   r->exchange_seconds = cm.seconds;
@@ -1016,6 +1307,9 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
 }
 
 thread_local std::string t_err;
+}  // namespace
+void set_error(const std::string& what) { t_err = what; }
+namespace {
 
 template <class F>
 int guard(F&& f) {

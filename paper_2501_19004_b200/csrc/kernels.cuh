@@ -185,6 +185,11 @@ void compact_rows(const u64* hoff, const u32* htgt, const float* hw, const u32* 
 // sums: [0] internal arc weight, [1] sum_c Sigma_c^2 ; tot (width entries) zeroed here
 void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width,
                       double* sums, cudaStream_t s, double two_m);
+// the two halves of modularity_terms (a sharded run allreduces tot and sums[0]
+// between them): the row pass (tot, sums zeroed here) and sums[1] += sum_c (tot_c / 2m)^2
+void modularity_rows(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width, double* sums,
+                     cudaStream_t s);
+void modularity_squares(const double* tot, u64 width, double two_m, double* sums, cudaStream_t s);
 // ext[c] = arcs from members of c to other communities (width entries, zeroed
 // here): bounds the distinct targets of super-row c (aggregation capacities)
 void external_arcs(const DGraph& g, const Bins& b, const u32* C, u64* ext, u64 width, cudaStream_t s);

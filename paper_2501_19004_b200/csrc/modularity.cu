@@ -251,17 +251,25 @@ void row_pass(const DGraph& g, const Bins& b, const u32* C, double* tot, double*
 
 }  // namespace
 
-void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width,
-                      double* sums, cudaStream_t s, double two_m) {
+void modularity_rows(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width, double* sums,
+                     cudaStream_t s) {
   LVN_CUDA(cudaMemsetAsync(tot, 0, width * sizeof(double), s));
   LVN_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), s));
   row_pass<false>(g, b, C, tot, sums, nullptr, s);
-  if (width) {
-    const int sms = sm_count();
-    const u64 blocks = std::min<u64>((width + 255) / 256, u64(sms) * 8);
-    sum_squares<<<unsigned(blocks), 256, 0, s>>>(tot, width, two_m, sums);
-    LVN_LAUNCH();
-  }
+}
+
+void modularity_squares(const double* tot, u64 width, double two_m, double* sums, cudaStream_t s) {
+  if (!width) return;
+  const int sms = sm_count();
+  const u64 blocks = std::min<u64>((width + 255) / 256, u64(sms) * 8);
+  sum_squares<<<unsigned(blocks), 256, 0, s>>>(tot, width, two_m, sums);
+  LVN_LAUNCH();
+}
+
+void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width,
+                      double* sums, cudaStream_t s, double two_m) {
+  modularity_rows(g, b, C, tot, width, sums, s);
+  modularity_squares(tot, width, two_m, sums, s);
 }
 
 void external_arcs(const DGraph& g, const Bins& b, const u32* C, u64* ext, u64 width, cudaStream_t s) {

@@ -55,11 +55,12 @@ class Collectives:
         self.location = location
         self.stage = location == "cuda" and self.backend == "gloo"
         self.errors: list[str] = []
-        self.calls = {"allreduce": 0, "allgatherv": 0}
+        self.calls = {"allreduce": 0, "allgatherv": 0, "alltoallv": 0}
         self.bytes = 0
         self._ar = N.ALLREDUCE_FN(self._allreduce)
         self._ag = N.ALLGATHERV_FN(self._allgatherv)
-        self.struct = N.lvn_comm(self.rank, self.size, None, self._ar, self._ag)
+        self._aa = N.ALLTOALLV_FN(self._alltoallv)
+        self.struct = N.lvn_comm(self.rank, self.size, None, self._ar, self._ag, self._aa)
 
     # -- views of engine buffers ------------------------------------------------------
     def _bytes(self, ptr: int, nbytes: int) -> torch.Tensor:
@@ -97,6 +98,32 @@ class Collectives:
                 recv[pos: pos + c].copy_(parts[k][:c])
             pos += c
 
+    def alltoallv_bytes(self, send: torch.Tensor, scounts: list[int], recv: torch.Tensor,
+                        rcounts: list[int]) -> None:
+        if self.stage or send.device.type == "cpu":
+            # gloo: all_to_all_single on host tensors
+            s_h = send.cpu() if send.device.type != "cpu" else send
+            r_h = torch.empty(sum(rcounts), dtype=torch.uint8)
+            dist.all_to_all_single(r_h, s_h, output_split_sizes=rcounts, input_split_sizes=scounts,
+                                   group=self.group)
+            recv.copy_(r_h)
+        else:
+            dist.all_to_all_single(recv, send, output_split_sizes=rcounts, input_split_sizes=scounts,
+                                   group=self.group)
+
+    def _alltoallv(self, user, send, scounts, recv, rcounts) -> int:
+        try:
+            self.calls["alltoallv"] += 1
+            sc = [int(scounts[k]) for k in range(self.size)]
+            rc = [int(rcounts[k]) for k in range(self.size)]
+            self.bytes += sum(sc)
+            self.alltoallv_bytes(self._bytes(send, sum(sc)), sc, self._bytes(recv, sum(rc)), rc)
+            self._sync()
+            return 0
+        except Exception:  # noqa: BLE001
+            self.errors.append(traceback.format_exc())
+            return 1
+
     def _allreduce(self, user, buf, count, dtype, op) -> int:
         try:
             self.calls["allreduce"] += 1
@@ -127,3 +154,42 @@ class Collectives:
         except Exception:  # noqa: BLE001
             self.errors.append(traceback.format_exc())
             return 1
+
+
+class NcclComm:
+    """The library's own NCCL communicator (lvn_comm_nccl_create): collectives
+    enqueued on the engine stream inside liblvn.so, no Python on the data path.
+    torch.distributed only ships the NCCL unique id from rank 0 (any process
+    group: the default one of torchrun)."""
+
+    def __init__(self, group=None):
+        if not dist.is_initialized():
+            raise RuntimeError("torch.distributed is not initialised")
+        self.rank = dist.get_rank(group)
+        self.size = dist.get_world_size(group)
+        L = N.lib()
+        uid = (C.c_ubyte * 128)()
+        if self.rank == 0 and L.lvn_nccl_unique_id(uid) != 0:
+            raise RuntimeError(N.last_error())
+        box = [bytes(uid)]
+        dist.broadcast_object_list(box, src=0, group=group)
+        uid = (C.c_ubyte * 128).from_buffer_copy(box[0])
+        ptr = C.POINTER(N.lvn_comm)()
+        if L.lvn_comm_nccl_create(self.rank, self.size, uid, C.byref(ptr)) != 0:
+            raise RuntimeError(N.last_error())
+        self._ptr = ptr
+        self.struct = ptr.contents
+        self.errors: list[str] = []
+        self.calls = {}
+
+    def close(self) -> None:
+        if self._ptr:
+            N.lib().lvn_comm_destroy(self._ptr)
+            self._ptr = None
+            self.struct = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001
+            pass

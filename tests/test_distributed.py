@@ -88,6 +88,19 @@ def _worker(rank, world, port, q):
         counts = (C.c_uint64 * world)(*[4 * (bounds[k + 1] - bounds[k]) for k in range(world)])
         assert st.allgatherv(None, C_.ctypes.data + 4 * lo, C_.ctypes.data, counts) == 0
         assert (C_ == np.arange(n, dtype=np.uint32) * 3).all()
+        # partial super-edges routed to row owners: rank r sends (r + 1) * (k + 1) u64
+        # entries to rank k, each tagged (sender, receiver, index)
+        scounts = [(rank + 1) * (k + 1) for k in range(world)]
+        rcounts = [(j + 1) * (rank + 1) for j in range(world)]
+        send = np.concatenate([np.array([(rank << 40) | (k << 20) | i for i in range(scounts[k])], np.uint64)
+                               for k in range(world)])
+        recv = np.zeros(sum(rcounts), np.uint64)
+        sb = (C.c_uint64 * world)(*[8 * x for x in scounts])
+        rb = (C.c_uint64 * world)(*[8 * x for x in rcounts])
+        assert st.alltoallv(None, send.ctypes.data, sb, recv.ctypes.data, rb) == 0
+        want = np.concatenate([np.array([(j << 40) | (rank << 20) | i for i in range(rcounts[j])], np.uint64)
+                               for j in range(world)])
+        assert (recv == want).all()
         # a failing collective is reported, not raised
         assert st.allreduce(None, d.ctypes.data, d.size, 99, N.LVN_SUM) == 1
         assert comm.errors
