@@ -165,6 +165,8 @@ typedef struct lvn_result {
                              device time of the library's NCCL collectives) */
   int num_levels;          /* dendrogram levels kept (lvn_params.keep_levels), else 0 */
   uint32_t** levels;       /* host arrays, level k has vertices_per_pass[k] entries */
+  uint64_t h2d_bytes;      /* bytes copied host -> device for the input (host input only;
+                              constant weights are verified on the host and filled on the device) */
 } lvn_result;
 
 /* ---- lifecycle -------------------------------------------------------- */

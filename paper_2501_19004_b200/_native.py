@@ -109,6 +109,7 @@ class lvn_result(C.Structure):
         ("exchange_seconds", C.c_double),
         ("num_levels", C.c_int),
         ("levels", C.POINTER(C.POINTER(C.c_uint32))),
+        ("h2d_bytes", C.c_uint64),
     ]
 
 

@@ -8,6 +8,7 @@
 #include <cstring>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "comm.hpp"
@@ -306,6 +307,7 @@ u64 sweep_chunk(const lvn_params& p, u32 nv) {
 struct InGraph {
   DGraph g;
   double m = 0.0;
+  u64 h2d_bytes = 0;
   DBuf<u64> off;
   DBuf<u32> tgt;
   DBuf<float> w;
@@ -317,6 +319,43 @@ void check_csr_header(const lvn_csr* in) {
   if (!in->offsets) fail(kInvalid, "null offsets");
   if (in->num_arcs && (!in->targets || !in->weights)) fail(kInvalid, "null targets/weights");
   if (in->location != LVN_HOST && in->location != LVN_DEVICE) fail(kInvalid, "bad location");
+}
+
+// Host weights -> device. Unit / constant-weight inputs (every unweighted
+// graph, and the paper's) are detected on the host while the targets are in
+// flight over PCIe: a multi-threaded bitwise scan of the host array against
+// its first weight. When every weight matches, the device array is filled on
+// the device (one kernel at HBM speed) instead of moving 4 B per arc over the
+// link; otherwise the array is copied. Either way the device holds exactly
+// the caller's bits.
+u64 upload_weights(const float* host, float* dev, u64 a, cudaStream_t s) {
+  if (!a) return 0;
+  u32 w0;
+  std::memcpy(&w0, host, sizeof(u32));
+  const u32* h = reinterpret_cast<const u32*>(host);
+  unsigned nt = std::thread::hardware_concurrency();
+  nt = std::max(1u, std::min(nt ? nt : 1u, 32u));
+  if (a < (u64(1) << 22)) nt = 1;
+  std::atomic<bool> differs{false};
+  std::vector<std::thread> pool;
+  auto scan = [&](u64 b, u64 e) {
+    constexpr u64 kStep = u64(1) << 20;
+    for (u64 c = b; c < e && !differs.load(std::memory_order_relaxed); c += kStep) {
+      const u64 ce = std::min(e, c + kStep);
+      u32 acc = 0;
+      for (u64 i = c; i < ce; ++i) acc |= h[i] ^ w0;
+      if (acc) differs.store(true, std::memory_order_relaxed);
+    }
+  };
+  for (unsigned t = 1; t < nt; ++t) pool.emplace_back(scan, a * t / nt, a * (t + 1) / nt);
+  scan(0, a / nt);
+  for (auto& th : pool) th.join();
+  if (differs.load()) {
+    LVN_CUDA(cudaMemcpyAsync(dev, host, a * sizeof(float), cudaMemcpyHostToDevice, s));
+    return a * sizeof(float);
+  }
+  fill_u32(reinterpret_cast<u32*>(dev), a, w0, s);
+  return 0;
 }
 
 void load_graph(const lvn_csr* in, cudaStream_t s, InGraph& out, double* h2d_seconds) {
@@ -336,8 +375,9 @@ void load_graph(const lvn_csr* in, cudaStream_t s, InGraph& out, double* h2d_sec
   LVN_CUDA(cudaMemcpyAsync(out.off.p, in->offsets, (n + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
   if (a) {
     LVN_CUDA(cudaMemcpyAsync(out.tgt.p, in->targets, a * sizeof(u32), cudaMemcpyHostToDevice, s));
-    LVN_CUDA(cudaMemcpyAsync(out.w.p, in->weights, a * sizeof(float), cudaMemcpyHostToDevice, s));
+    out.h2d_bytes += a * sizeof(u32) + upload_weights(in->weights, out.w.p, a, s);
   }
+  out.h2d_bytes += (n + 1) * sizeof(u64);
   LVN_CUDA(cudaStreamSynchronize(s));
   if (h2d_seconds) *h2d_seconds += since(t0);
   out.g = DGraph{u32(n), a, out.off.p, out.tgt.p, out.w.p};
@@ -693,6 +733,7 @@ void load_graph_shard(const lvn_csr* in, int rank, int size, cudaStream_t s, InG
   if (in->location != LVN_DEVICE) {
     up.alloc(u64(n) + 1);
     LVN_CUDA(cudaMemcpyAsync(up.p, in->offsets, (u64(n) + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+    out.h2d_bytes += (u64(n) + 1) * sizeof(u64);
     goff = up.p;
   }
   shard_offsets(goff, n, v0, v1, out.off.p, s);
@@ -711,7 +752,7 @@ void load_graph_shard(const lvn_csr* in, int rank, int size, cudaStream_t s, InG
   out.w.alloc(a ? a : 1);
   if (a) {
     LVN_CUDA(cudaMemcpyAsync(out.tgt.p, in->targets + a0, a * sizeof(u32), cudaMemcpyHostToDevice, s));
-    LVN_CUDA(cudaMemcpyAsync(out.w.p, in->weights + a0, a * sizeof(float), cudaMemcpyHostToDevice, s));
+    out.h2d_bytes += a * sizeof(u32) + upload_weights(in->weights + a0, out.w.p, a, s);
   }
   LVN_CUDA(cudaStreamSynchronize(s));
   if (h2d_seconds) *h2d_seconds += since(t0);
@@ -1298,6 +1339,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     levels.clear();
   }
   cm.settle();
+  r->h2d_bytes = ig.h2d_bytes;
   r->num_shards = cm.size();
   r->sharded_passes = sharded_passes;
   r->exchange_seconds = cm.seconds;

@@ -1115,8 +1115,13 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
 //   lm_hub_chunks  block per chunk: K_{u->c} of the chunk in an smem table (own
 //                  community privatised), flushed into the hub's HBM table
 //                  (claim by CAS, L2 reductions, live-slot list)
-//   lm_hub_decide  block per hub: rank the live entries, apply the validated
-//                  move, mark the neighbours, restore the table to empty
+//   lm_hub_rank    block per chunk-sized slice of a hub's live entries: best
+//                  candidate of the slice, slots restored to empty
+//   lm_hub_decide  warp per hub: best of its slices, the validated move
+//   lm_hub_mark    block per chunk: neighbour marks of the hubs that moved
+// Every phase spreads a hub over as many blocks as it has chunks: the
+// million-arc hubs of web graphs no longer leave one block ranking (or
+// marking) millions of entries while the rest of the GPU idles.
 constexpr u32 kHubChunk = 4096;  // <= 4096 distinct keys: fits the 8192-slot smem table
 
 __host__ __device__ __forceinline__ u64 hub_slots(u64 deg, u32 n) {
@@ -1217,31 +1222,49 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const
   }
 }
 
+// Best candidate of one slice of a hub's live entries (the slice of chunk v:
+// entries [(v - chunk_off[i]) kHubChunk, +kHubChunk) of hub i), so a hub with
+// millions of distinct communities is ranked by hundreds of blocks instead of
+// one; the slice's slots are restored to empty after the read.
+struct HubBest {
+  double g, k;
+  u32 c, pad;
+};
+
 template <class Tab, bool DRY>
-__global__ void __launch_bounds__(kBlockThreads) lm_hub_decide(MoveArgs x, const u32* __restrict__ hubs,
-                                                               u64 count) {
+__global__ void __launch_bounds__(kBlockThreads) lm_hub_rank(MoveArgs x, const u32* __restrict__ hubs, u64 count,
+                                                             const u64* __restrict__ chunk_off,
+                                                             HubBest* __restrict__ best) {
   using V = typename Tab::V;
   constexpr int W = kBlockThreads / 32;
   __shared__ double red_g[W], red_k[W];
   __shared__ u32 red_c[W];
-  __shared__ u32 bcast;
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  Tally tl;
-  for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
-    const u32 u = hubs[i];
+  const u64 total = chunk_off[count];
+  for (u64 v = blockIdx.x; v < total; v += gridDim.x) {
+    u64 lo = 0, hi = count;  // hub of chunk v
+    while (hi - lo > 1) {
+      const u64 mid = (lo + hi) / 2;
+      if (chunk_off[mid] <= v) lo = mid; else hi = mid;
+    }
+    const u32 u = hubs[lo];
     const u32 pi = x.hub_index[u];
-    const u64 lo = x.g.off[u], d = x.g.off[u + 1] - lo;
-    const u32 from = x.C[u];
-    const double own = double(static_cast<const V*>(x.hub_own)[pi]);
+    const u64 d = x.g.off[u + 1] - x.g.off[u];
     const u32 n = x.hub_live[pi];
+    const u64 j0 = (v - chunk_off[lo]) * kHubChunk;
+    double bg = -INFINITY, bk = 0.0;
+    u32 bc = kEmpty;
     const u64 slots = hub_slots(d, x.g.n);
     unsigned char* base = x.hub_tables + x.hub_tab_off[pi];
     const Tab gtab(base, slots);
     const u32* glive = reinterpret_cast<const u32*>(base + slots * Tab::kSlotBytes);
-    const double ku = x.K[u], sf = x.sigma[from];
-    double bg = -INFINITY, bk = 0.0;
-    u32 bc = kEmpty;
-    rank_live<kBatch, DRY>(x, gtab, glive, n, threadIdx.x, kBlockThreads, own, ku, sf, bg, bc, bk);
+    const u32 m = j0 < n ? u32(n - j0 < kHubChunk ? n - j0 : u64(kHubChunk)) : 0u;
+    if (m) {
+      const u32 from = x.C[u];
+      const double own = double(static_cast<const V*>(x.hub_own)[pi]);
+      const double ku = x.K[u], sf = x.sigma[from];
+      rank_live<kBatch, DRY>(x, gtab, glive + j0, m, threadIdx.x, kBlockThreads, own, ku, sf, bg, bc, bk);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       const double og = __shfl_xor_sync(0xffffffffu, bg, o);
@@ -1251,24 +1274,81 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_decide(MoveArgs x, const
     }
     if (lane == 0) red_g[wid] = bg, red_c[wid] = bc, red_k[wid] = bk;
     __syncthreads();
-    for (u32 j = threadIdx.x; j < n; j += kBlockThreads) gtab.clear(glive[j]);
+    for (u32 j = threadIdx.x; j < m; j += kBlockThreads) gtab.clear(glive[j0 + j]);
     if (threadIdx.x == 0) {
       for (int k = 1; k < W; ++k)
         if (better(red_g[k], red_c[k], bg, bc)) bg = red_g[k], bc = red_c[k], bk = red_k[k];
+      best[v] = HubBest{bg, bk, bc, m};
+    }
+    __syncthreads();
+  }
+}
+
+// Per hub (a warp each): the best of its slices, the validated move; the
+// hub's state (live count, own weight) is reset for the next sweep and
+// moved[i] tells lm_hub_mark whether to flag the hub's neighbours.
+template <class Tab, bool DRY>
+__global__ void lm_hub_decide(MoveArgs x, const u32* __restrict__ hubs, u64 count,
+                              const u64* __restrict__ chunk_off, const HubBest* __restrict__ best,
+                              u8* __restrict__ moved) {
+  using V = typename Tab::V;
+  const int lane = threadIdx.x & 31;
+  Tally tl;
+  const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
+  for (u64 i = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; i < count; i += warps) {
+    double bg = -INFINITY, bk = 0.0;
+    u32 bc = kEmpty, ranked = 0;
+    for (u64 v = chunk_off[i] + lane; v < chunk_off[i + 1]; v += 32) {
+      const HubBest h = best[v];
+      ranked += h.pad;
+      if (better(h.g, h.c, bg, bc)) bg = h.g, bc = h.c, bk = h.k;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      const double og = __shfl_xor_sync(0xffffffffu, bg, o);
+      const u32 oc = __shfl_xor_sync(0xffffffffu, bc, o);
+      const double ok = __shfl_xor_sync(0xffffffffu, bk, o);
+      ranked += __shfl_xor_sync(0xffffffffu, ranked, o);
+      if (better(og, oc, bg, bc)) bg = og, bc = oc, bk = ok;
+    }
+    if (lane == 0) {
+      const u32 u = hubs[i];
+      const u32 pi = x.hub_index[u];
+      const u64 d = x.g.off[u + 1] - x.g.off[u];
+      const u32 from = x.C[u];
+      const double own = double(static_cast<const V*>(x.hub_own)[pi]);
       x.hub_live[pi] = 0;
       static_cast<V*>(x.hub_own)[pi] = V(0);
       if (!DRY) x.flags[u] = 0;
       ++tl.verts;
       tl.arcs += d;
-      tl.rand += d + n;
-      bcast = decide<DRY>(x, u, from, ku, bc, bg, bk, own, tl);
+      tl.rand += d + ranked;
+      moved[i] = decide<DRY>(x, u, from, x.K[u], bc, bg, bk, own, tl) ? 1 : 0;
     }
-    __syncthreads();
-    if (!DRY && bcast && x.prune)
-      for (u64 a = lo + threadIdx.x; a < lo + d; a += kBlockThreads) x.flags[x.g.tgt[a]] = 1, ++tl.rand;
-    __syncthreads();
   }
   tl.flush(x);
+}
+
+// neighbour marks of the hubs that moved, chunk by chunk (louvain_compact.cpp:160-161)
+__global__ void lm_hub_mark(MoveArgs x, const u32* __restrict__ hubs, u64 count, const u64* __restrict__ chunk_off,
+                            const u8* __restrict__ moved) {
+  ull marks = 0;
+  const u64 total = chunk_off[count];
+  for (u64 v = blockIdx.x; v < total; v += gridDim.x) {
+    u64 lo = 0, hi = count;
+    while (hi - lo > 1) {
+      const u64 mid = (lo + hi) / 2;
+      if (chunk_off[mid] <= v) lo = mid; else hi = mid;
+    }
+    if (!moved[lo]) continue;
+    const u32 u = hubs[lo];
+    const u64 row = x.g.off[u], row_end = x.g.off[u + 1];
+    const u64 a0 = row + (v - chunk_off[lo]) * kHubChunk;
+    const u64 a1 = min(a0 + kHubChunk, row_end);
+    for (u64 a = a0 + threadIdx.x; a < a1; a += blockDim.x) x.flags[x.g.tgt[a]] = 1, ++marks;
+  }
+  marks = warp_sum(marks);
+  if ((threadIdx.x & 31) == 0 && marks) atomicAdd(&x.counters[3], marks);
 }
 
 // ---- launch plumbing ----------------------------------------------------------
@@ -1410,6 +1490,9 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         const u64 step = std::max<u64>(1, std::min(a.hub_chunk, all));
         DBuf<u32> chunks(std::min(step, all));
         DBuf<u64> coff(std::min(step, all) + 1);
+        // slices of every hub of a group: at most arcs / kHubChunk + hubs
+        DBuf<HubBest> hbest(a.g.arcs / kHubChunk + std::min(step, all) + 1);
+        DBuf<u8> hmoved(std::min(step, all));
         auto kc = lm_hub_chunks<Tab>;
         constexpr size_t smem = block_smem<Tab>();
         static const int occ = (set_smem(kc, smem), occupancy(kc, kBlockThreads, smem));
@@ -1422,8 +1505,15 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
           exclusive_scan_u32_to_u64(chunks.p, coff.p, cnt, s);
           kc<<<unsigned(sms * occ), kBlockThreads, smem, s>>>(a, hubs, cnt, coff.p);
           LVN_LAUNCH();
-          lm_hub_decide<Tab, DRY><<<unsigned(std::min<u64>(cnt, u64(sms) * 4)), kBlockThreads, 0, s>>>(a, hubs, cnt);
+          lm_hub_rank<Tab, DRY><<<unsigned(sms * 4), kBlockThreads, 0, s>>>(a, hubs, cnt, coff.p, hbest.p);
           LVN_LAUNCH();
+          lm_hub_decide<Tab, DRY><<<unsigned(std::min<u64>((cnt + 7) / 8, u64(sms) * 8)), 256, 0, s>>>(
+              a, hubs, cnt, coff.p, hbest.p, hmoved.p);
+          LVN_LAUNCH();
+          if (!DRY && a.prune) {
+            lm_hub_mark<<<unsigned(sms * 8), 256, 0, s>>>(a, hubs, cnt, coff.p, hmoved.p);
+            LVN_LAUNCH();
+          }
         }
         break;
       }

@@ -174,6 +174,7 @@ class LouvainResult:  # louvain.hpp:28-39 (+ device breakdown)
     vertices_per_pass: list = field(default_factory=list)
     arcs_per_pass: list = field(default_factory=list)
     h2d_seconds: float = 0.0
+    h2d_bytes: int = 0  # input bytes copied host -> device (constant weights are filled on the device)
     d2h_seconds: float = 0.0
     stats: dict = field(default_factory=dict)
     num_shards: int = 1
@@ -423,6 +424,7 @@ def _result(out) -> LouvainResult:
             vertices_per_pass=lst(r.vertices_per_pass),
             arcs_per_pass=lst(r.arcs_per_pass),
             h2d_seconds=r.h2d_seconds,
+            h2d_bytes=int(r.h2d_bytes),
             d2h_seconds=r.d2h_seconds,
             stats={name: KernelStats(s.seconds, s.bytes, s.launches, s.items, s.arcs, s.gathers)
                    for name, s in zip(N.STAT_NAMES, r.stats)},
