@@ -33,7 +33,7 @@ __device__ __forceinline__ int bin_of(u64 deg, const BinEdges& e) {
     return kBinSort256;
   }
   if (deg <= e.warp_max) return kBinWarp;
-  if (deg <= e.block_max) return kBinBlock;
+  if (deg <= e.block_max) return deg <= kBlockSplitDeg ? kBinBlockS : kBinBlock;
   return kBinGlobal;
 }
 
@@ -263,10 +263,10 @@ void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C
     reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinWarp), mid, K, sigma, uni);
     LVN_LAUNCH();
   }
-  const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
+  const u64 big = b.count(kBinBlockS) + b.count(kBinBlock) + b.count(kBinGlobal);
   if (big) {
     const u64 bb = std::min<u64>(big, u64(sms) * 4);
-    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(kBinBlock), big, K, sigma, uni);
+    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(kBinBlockS), big, K, sigma, uni);
     LVN_LAUNCH();
   }
 }

@@ -25,10 +25,14 @@ enum : int {
   kBinSort128 = 6,  // deg <= 128: 32 lanes x 4 registers
   kBinSort256 = 7,  // deg <= 256: 32 lanes x 8 registers
   kBinWarp = 8,     // deg <= warp_max: warp, smem hash table
-  kBinBlock = 9,    // deg <= block_max: block, smem hash table
-  kBinGlobal = 10,  // larger: block, global-memory hash table
-  kBins = 11
+  kBinBlockS = 9,   // deg <= min(block_max, kBlockSplitDeg): block sub-group, smem hash table
+  kBinBlock = 10,   // deg <= block_max: block, smem hash table
+  kBinGlobal = 11,  // larger: block, global-memory hash table
+  kBins = 12
 };
+// rows of the block class up to this degree share a block with three others
+// (own bin, so no kernel walks rows it does not take)
+constexpr unsigned long long kBlockSplitDeg = 1024;
 struct BinEdges {
   u32 thread_max = 4, group_max = 256, warp_max = 256, block_max = 4096;
 };

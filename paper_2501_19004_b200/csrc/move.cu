@@ -51,7 +51,7 @@ constexpr int kWarpCapLog = 9;     // 512 slots (warp_max <= 256)
 constexpr int kBlockCapLog = 13;   // 8192 slots (block_max <= 4096)
 constexpr int kBlockThreads = 512;
 constexpr int kBatch = 4;          // arcs (and ranked entries) in flight per lane
-constexpr u64 kBlockSplit = 1024;  // block bin: rows up to this many arcs use 4 sub-groups per block
+constexpr u64 kBlockSplit = kBlockSplitDeg;  // kBinBlockS rows: 4 sub-groups per block
 
 // ---- per-thread accounting, flushed once per thread at kernel exit ----------
 struct Tally {
@@ -1461,24 +1461,24 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         launch_chunks(k, a, b.of(bin), b.count(bin), T, T / 32, u64(sms) * occ, smem, s);
         break;
       }
+      case kBinBlockS:
       case kBinBlock: {
-        // rows of <= kBlockSplit arcs: four sub-groups per block; longer rows:
-        // the whole block (both kernels walk the bin's list, each takes its rows)
+        // rows of <= kBlockSplitDeg arcs: four sub-groups per block (four
+        // vertices in flight); longer rows: the whole block
         constexpr size_t smem = block_stage_smem<Tab>();
         auto k4 = lm_block<Tab, DRY, 4>;
         auto k1 = lm_block<Tab, DRY, 1>;
         static const int occ4 = (set_smem(k4, smem), occupancy(k4, kBlockThreads, smem));
         static const int occ1 = (set_smem(k1, smem), occupancy(k1, kBlockThreads, smem));
+        const int per = bin == kBinBlockS ? 4 : 1;
         const u64 chunk = std::min(a.chunk, a.hub_chunk);
         const u32* list = b.of(bin);
         const u64 cnt = b.count(bin);
         for (u64 off = 0; off < cnt; off += chunk) {
           const u64 c = std::min<u64>(chunk, cnt - off);
-          const u64 b4 = std::max<u64>(1, std::min<u64>((c + 3) / 4, u64(sms) * occ4));
-          k4<<<unsigned(b4), kBlockThreads, smem, s>>>(a, list + off, c, 0, kBlockSplit);
-          LVN_LAUNCH();
-          const u64 b1 = std::max<u64>(1, std::min<u64>(c, u64(sms) * occ1));
-          k1<<<unsigned(b1), kBlockThreads, smem, s>>>(a, list + off, c, kBlockSplit, ~u64(0));
+          const u64 nb = std::max<u64>(1, std::min<u64>((c + per - 1) / per, u64(sms) * (per == 4 ? occ4 : occ1)));
+          if (per == 4) k4<<<unsigned(nb), kBlockThreads, smem, s>>>(a, list + off, c, 0, kBlockSplit);
+          else k1<<<unsigned(nb), kBlockThreads, smem, s>>>(a, list + off, c, 0, ~u64(0));
           LVN_LAUNCH();
         }
         break;
