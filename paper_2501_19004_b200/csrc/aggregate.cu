@@ -40,6 +40,15 @@ constexpr int kBlockCapLog = 13;
 constexpr int kBlockThreads = 512;
 using Tab = SplitF64;
 
+// fp64 sum -> f32 super-graph weight (narrowed once, louvain_mc.cpp:95); a
+// narrowing that loses bits raises *x.inexact (then the engine computes the
+// final modularity on the input graph instead of the last super-graph)
+__device__ __forceinline__ float narrow(const AggArgs& x, double v) {
+  const float f = float(v);
+  if (x.inexact && double(f) != v) *x.inexact = 1u;
+  return f;
+}
+
 // Communities with budget <= N = G*K: element e = r*G + lane of the
 // community's member arcs (members in CSR order) is loaded into register r.
 template <int G, int K>
@@ -89,7 +98,7 @@ __global__ void __launch_bounds__(256) ag_sort(AggArgs x, const u32* __restrict_
         for (int r = 0; r < K; ++r) {
           if (tail[r] && key[r] != kEmpty) {
             x.htgt[hbase + pos] = key[r];
-            x.hw[hbase + pos] = float(val[r]);  // fp64 sum narrowed once
+            x.hw[hbase + pos] = narrow(x, val[r]);  // fp64 sum narrowed once
             ++pos;
           }
         }
@@ -201,7 +210,7 @@ __global__ void __launch_bounds__(256) ag_psort(AggArgs x, const u32* __restrict
         for (int r = 0; r < K; ++r) {
           if (tail[r] && ck[r] != kEmpty) {
             x.htgt[hbase + pos] = ck[r];
-            x.hw[hbase + pos] = float(val[r]);  // fp64 sum narrowed once
+            x.hw[hbase + pos] = narrow(x, val[r]);  // fp64 sum narrowed once
             ++pos;
           }
         }
@@ -267,14 +276,14 @@ __global__ void __launch_bounds__(THREADS) ag_group(AggArgs x, const u32* __rest
       if (live) {
         const u64 o = hbase + pos + __popc(bal & ((1u << lane) - 1u));
         x.htgt[o] = key;
-        x.hw[o] = float(val);
+        x.hw[o] = narrow(x, val);
       }
       pos += __popc(bal);
     }
     if (lane == 0) {
       if (own_seen) {
         x.htgt[hbase + pos] = c;
-        x.hw[hbase + pos] = float(own);
+        x.hw[hbase + pos] = narrow(x, own);
         ++pos;
       }
       if (pos > hcap) atomicOr(x.err, u32(kErrTable));
@@ -403,7 +412,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
     if (tab.read(s, key, val)) {
       const u32 o = atomicAdd(cursor, 1u);
       x.htgt[hbase + o] = key;
-      x.hw[hbase + o] = float(val);
+      x.hw[hbase + o] = narrow(x, val);
     }
   }
   __syncthreads();
@@ -414,7 +423,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
     u64 pos = *cursor;
     if (seen) {
       x.htgt[hbase + pos] = c;
-      x.hw[hbase + pos] = float(t);
+      x.hw[hbase + pos] = narrow(x, t);
       ++pos;
     }
     if (pos > hcap) atomicOr(x.err, u32(kErrTable));
@@ -785,7 +794,7 @@ __global__ void __launch_bounds__(256) ag_dense_scan(AggArgs x, BigState st, con
         const u32 o = wbase + __popc(bal & ((1u << lane) - 1u));
         if (o < hcap) {
           x.htgt[hbase + o] = u32(j);
-          x.hw[hbase + o] = float(__longlong_as_double((long long)bits));  // fp64 sum narrowed once
+          x.hw[hbase + o] = narrow(x, __longlong_as_double((long long)bits));  // fp64 sum narrowed once
         }
       }
     }
@@ -809,7 +818,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, BigState
       for (u32 j = threadIdx.x; j < n && j < hcap; j += kBlockThreads) {
         const BigSlot e = t[live[j]];
         x.htgt[hbase + j] = e.key;
-        x.hw[hbase + j] = float(e.val);  // fp64 sum narrowed once
+        x.hw[hbase + j] = narrow(x, e.val);  // fp64 sum narrowed once
       }
     }
     if (threadIdx.x == 0) {
@@ -818,7 +827,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, BigState
       } else {
         if (self) {
           x.htgt[hbase + n] = c;
-          x.hw[hbase + n] = float(st.own_sum[i]);
+          x.hw[hbase + n] = narrow(x, st.own_sum[i]);
         }
         x.fill[c] = n + self;
       }

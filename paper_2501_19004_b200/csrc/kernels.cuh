@@ -174,6 +174,7 @@ struct AggArgs {
   float* hw = nullptr;
   u32* fill = nullptr;           // entries written per row
   u32* err = nullptr;
+  u32* inexact = nullptr;        // set when a narrowing to f32 loses bits (may be null)
   int big_mode = 0;              // giant-community regions: 0 by size, 1 hash, 2 dense (LVN_BIG_MODE)
 };
 // Synchronises once when the kBinGlobal bin is non-empty (sizes its HBM tables).

@@ -1122,7 +1122,15 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
 // Every phase spreads a hub over as many blocks as it has chunks: the
 // million-arc hubs of web graphs no longer leave one block ranking (or
 // marking) millions of entries while the rest of the GPU idles.
-constexpr u32 kHubChunk = 4096;  // <= 4096 distinct keys: fits the 8192-slot smem table
+#ifndef LVN_HUB_CHUNK_LOG
+#define LVN_HUB_CHUNK_LOG 11
+#endif
+constexpr u32 kHubChunk = 1u << LVN_HUB_CHUNK_LOG;  // arcs of one chunk
+constexpr int kHubCapLog = LVN_HUB_CHUNK_LOG + 1;   // its smem table: 2 slots per arc
+template <class Tab>
+constexpr size_t hub_smem() {
+  return (size_t(1) << kHubCapLog) * Tab::kSlotBytes + (size_t(1) << (kHubCapLog - 1)) * 4;
+}
 
 __host__ __device__ __forceinline__ u64 hub_slots(u64 deg, u32 n) {
   const u64 distinct = deg < n ? deg : n;
@@ -1171,9 +1179,9 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 nlive;
   __shared__ V red[kBlockThreads / 32];
-  const Tab stab(smem, u64(1) << kBlockCapLog);
-  u32* slive = reinterpret_cast<u32*>(smem + (size_t(1) << kBlockCapLog) * Tab::kSlotBytes);
-  for (u32 s = threadIdx.x; s < (1u << kBlockCapLog); s += kBlockThreads) stab.clear(s);
+  const Tab stab(smem, u64(1) << kHubCapLog);
+  u32* slive = reinterpret_cast<u32*>(smem + (size_t(1) << kHubCapLog) * Tab::kSlotBytes);
+  for (u32 s = threadIdx.x; s < (1u << kHubCapLog); s += kBlockThreads) stab.clear(s);
   if (threadIdx.x == 0) nlive = 0;
   __syncthreads();
   const u64 total = chunk_off[count];
@@ -1190,7 +1198,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const
     const u64 a1 = min(a0 + kHubChunk, row_end);
     const u32 from = x.C[u];
     V own = V(0);
-    scan_arcs<kBatch, true>(x, stab, u32(kBlockCapLog), u, from, a0, a1, threadIdx.x, kBlockThreads, own, slive,
+    scan_arcs<kBatch, true>(x, stab, u32(kHubCapLog), u, from, a0, a1, threadIdx.x, kBlockThreads, own, slive,
                       &nlive);
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) own += __shfl_xor_sync(0xffffffffu, own, o);
@@ -1494,7 +1502,7 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         DBuf<HubBest> hbest(a.g.arcs / kHubChunk + std::min(step, all) + 1);
         DBuf<u8> hmoved(std::min(step, all));
         auto kc = lm_hub_chunks<Tab>;
-        constexpr size_t smem = block_smem<Tab>();
+        constexpr size_t smem = hub_smem<Tab>();
         static const int occ = (set_smem(kc, smem), occupancy(kc, kBlockThreads, smem));
         for (u64 h0 = 0; h0 < all; h0 += step) {
           const u64 cnt = std::min(step, all - h0);
