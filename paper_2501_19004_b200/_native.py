@@ -69,6 +69,7 @@ class lvn_params(C.Structure):
         ("shard_min_arcs_log2", C.c_int),
         ("shard_rounds", C.c_int),
         ("keep_levels", C.c_int),
+        ("first_range_arcs_log2", C.c_int),
     ]
 
 

@@ -126,6 +126,7 @@ struct Context {
   int sms = 148;
   size_t smem_optin = 227 * 1024;
   cudaStream_t stream = nullptr;
+  cudaStream_t copy = nullptr;  // host -> device input chunks (overlapped with the first sweep)
   Pool pool;
   HostCache host;
   u64* pinned = nullptr;  // 8192 u64 of pinned host scratch

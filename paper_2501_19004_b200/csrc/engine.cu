@@ -219,6 +219,7 @@ void init_context(int device) {
   c->sms = prop.multiProcessorCount;
   c->smem_optin = prop.sharedMemPerBlockOptin;
   LVN_CUDA(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+  LVN_CUDA(cudaStreamCreateWithFlags(&c->copy, cudaStreamNonBlocking));
   c->pool.bind(device, c->stream);
   LVN_CUDA(cudaMallocHost(&c->pinned, 8192 * sizeof(u64)));
   g_ctx = c;
@@ -238,6 +239,7 @@ void destroy_context() {
   g_ctx->pool.release_all();
   (void)cudaFreeHost(g_ctx->pinned);
   (void)cudaStreamDestroy(g_ctx->stream);
+  (void)cudaStreamDestroy(g_ctx->copy);
   delete g_ctx;
   g_ctx = nullptr;
 }
@@ -284,6 +286,8 @@ void validate(const lvn_params& p) {
   if (p.sweep_order != 0 && p.sweep_order != 1) fail(kInvalid, "sweep_order must be 0 or 1");
   if (p.shard_min_arcs_log2 < 0 || p.shard_min_arcs_log2 > 62) fail(kInvalid, "shard_min_arcs_log2 must be in [0, 62]");
   if (p.shard_rounds < 0 || p.shard_rounds > 64) fail(kInvalid, "shard_rounds must be in [0, 64]");
+  if (p.first_range_arcs_log2 < 0 || p.first_range_arcs_log2 > 62)
+    fail(kInvalid, "first_range_arcs_log2 must be in [0, 62]");
   if (!(p.bin_thread_max <= p.bin_group_max && p.bin_group_max <= p.bin_warp_max &&
         p.bin_warp_max <= p.bin_block_max))
     fail(kInvalid, "degree bin edges must be non-decreasing");
@@ -328,7 +332,7 @@ void check_csr_header(const lvn_csr* in) {
 // the device (one kernel at HBM speed) instead of moving 4 B per arc over the
 // link; otherwise the array is copied. Either way the device holds exactly
 // the caller's bits.
-u64 upload_weights(const float* host, float* dev, u64 a, cudaStream_t s) {
+u64 upload_weights(const float* host, float* dev, u64 a, cudaStream_t s, cudaStream_t fill_s = nullptr) {
   if (!a) return 0;
   u32 w0;
   std::memcpy(&w0, host, sizeof(u32));
@@ -354,7 +358,7 @@ u64 upload_weights(const float* host, float* dev, u64 a, cudaStream_t s) {
     LVN_CUDA(cudaMemcpyAsync(dev, host, a * sizeof(float), cudaMemcpyHostToDevice, s));
     return a * sizeof(float);
   }
-  fill_u32(reinterpret_cast<u32*>(dev), a, w0, s);
+  fill_u32(reinterpret_cast<u32*>(dev), a, w0, fill_s ? fill_s : s);
   return 0;
 }
 
@@ -381,6 +385,102 @@ void load_graph(const lvn_csr* in, cudaStream_t s, InGraph& out, double* h2d_sec
   LVN_CUDA(cudaStreamSynchronize(s));
   if (h2d_seconds) *h2d_seconds += since(t0);
   out.g = DGraph{u32(n), a, out.off.p, out.tgt.p, out.w.p};
+}
+
+// ---- pass 0's first sweep by id ranges, overlapped with the input upload ----
+// Large inputs: the first sweep of pass 0 visits R0 consecutive vertex-id
+// ranges of ~2^29 arcs each (each with its own degree bins, low degree first
+// within a range, like lvn_params.sweep_ranges), for host and device input
+// alike. With host input the ranges' targets travel as separate chunks on the
+// copy stream and the sweep of range k waits only for chunk k, so the first
+// sweep runs under the PCIe transfer instead of after it.
+std::vector<u32> split_rows(const u64* off, u32 n, int parts, cudaStream_t s);
+struct FirstSweep {
+  std::vector<u32> vb;          // range bounds (R0 + 1), empty: one range
+  std::vector<cudaEvent_t> ev;  // host input: targets of range k have landed
+  cudaEvent_t t0 = nullptr, t1 = nullptr;
+  FirstSweep() = default;
+  FirstSweep(const FirstSweep&) = delete;
+  FirstSweep& operator=(const FirstSweep&) = delete;
+  ~FirstSweep() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+    if (t0) cudaEventDestroy(t0);
+    if (t1) cudaEventDestroy(t1);
+  }
+  int ranges() const { return vb.empty() ? 1 : int(vb.size()) - 1; }
+};
+
+int first_range_count(u64 a, int log2) {
+  if (log2 <= 0 || log2 >= 63) return 1;
+  return int(std::min<u64>(16, a >> log2));
+}
+std::vector<u32> first_ranges(const u64* host_off, u32 n, u64 a, int log2) {
+  const int R0 = first_range_count(a, log2);
+  if (R0 < 2) return {};
+  std::vector<u32> vb(R0 + 1);
+  lvn_partition_rows(host_off, n, R0, vb.data());
+  return vb;
+}
+
+// load_graph with the targets of host input in first-sweep chunks on the copy
+// stream (the compute stream waits for the offsets here, for chunk k before
+// sweeping range k); device input: only the range bounds
+void load_graph_first(const lvn_csr* in, int log2, cudaStream_t s, InGraph& out, FirstSweep& fs,
+                      double* h2d_seconds) {
+  check_csr_header(in);
+  const u64 n = in->num_vertices, a = in->num_arcs;
+  if (in->location == LVN_DEVICE) {
+    load_graph(in, s, out, h2d_seconds);
+    const int R0 = first_range_count(a, log2);
+    if (R0 >= 2) fs.vb = split_rows(in->offsets, u32(n), R0, s);  // the lvn_partition_rows rule
+    return;
+  }
+  if (in->offsets[0] != 0 || in->offsets[n] != a)
+    fail(kInvalid, "offsets must start at 0 and end at num_arcs");
+  fs.vb = first_ranges(in->offsets, u32(n), a, log2);
+  if (fs.vb.empty()) {
+    load_graph(in, s, out, h2d_seconds);
+    return;
+  }
+  Context& c = ctx();
+  out.m = in->total_weight;
+  out.off.alloc(n + 1);
+  out.tgt.alloc(a);
+  out.w.alloc(a);
+  // the copy stream writes pool memory allocated (and maybe last used) on s
+  cudaEvent_t ready, off_ev;
+  LVN_CUDA(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  LVN_CUDA(cudaEventCreateWithFlags(&off_ev, cudaEventDisableTiming));
+  LVN_CUDA(cudaEventRecord(ready, s));
+  LVN_CUDA(cudaStreamWaitEvent(c.copy, ready));
+  LVN_CUDA(cudaEventCreate(&fs.t0));
+  LVN_CUDA(cudaEventCreate(&fs.t1));
+  LVN_CUDA(cudaEventRecord(fs.t0, c.copy));
+  LVN_CUDA(cudaMemcpyAsync(out.off.p, in->offsets, (n + 1) * sizeof(u64), cudaMemcpyHostToDevice, c.copy));
+  LVN_CUDA(cudaEventRecord(off_ev, c.copy));
+  const int R0 = fs.ranges();
+  fs.ev.resize(R0);
+  for (int k = 0; k < R0; ++k) {
+    const u64 a0 = in->offsets[fs.vb[k]], a1 = in->offsets[fs.vb[k + 1]];
+    if (a1 > a0)
+      LVN_CUDA(cudaMemcpyAsync(out.tgt.p + a0, in->targets + a0, (a1 - a0) * sizeof(u32), cudaMemcpyHostToDevice,
+                               c.copy));
+    LVN_CUDA(cudaEventCreateWithFlags(&fs.ev[k], cudaEventDisableTiming));
+    LVN_CUDA(cudaEventRecord(fs.ev[k], c.copy));
+  }
+  out.h2d_bytes += (n + 1) * sizeof(u64) + a * sizeof(u32);
+  LVN_CUDA(cudaStreamWaitEvent(s, off_ev));
+  // weights: verified on the host while the targets are in flight; copied
+  // (behind the targets on the copy stream, so the pass reset then waits for
+  // the whole input) only when they are not all equal
+  const u64 wb = upload_weights(in->weights, out.w.p, a, c.copy, s);
+  out.h2d_bytes += wb;
+  LVN_CUDA(cudaEventRecord(fs.t1, c.copy));
+  if (wb) LVN_CUDA(cudaStreamWaitEvent(s, fs.t1));
+  LVN_CUDA(cudaEventDestroy(ready));
+  LVN_CUDA(cudaEventDestroy(off_ev));
+  out.g = DGraph{u32(n), a, out.off.p, out.tgt.p, out.w.p};
+  (void)h2d_seconds;  // timed by the fs events once the run is done
 }
 
 // membership-like array on the device (borrowed or uploaded)
@@ -957,10 +1057,11 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   const u32 N = in->num_vertices;
   u32 v0 = 0, v1 = N;
   InGraph ig;
+  FirstSweep fs;
   if (sharded) {
     load_graph_shard(in, cm.rank(), cm.size(), s, ig, v0, v1, &r->h2d_seconds);
   } else if (!idle) {
-    load_graph(in, s, ig, &r->h2d_seconds);
+    load_graph_first(in, p.first_range_arcs_log2, s, ig, fs, &r->h2d_seconds);
   } else {
     ig.g.n = N;
   }
@@ -1126,6 +1227,11 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
                      u32(rbase[k]));
       views[k] = R > 1 ? rbins[k].view() : SB.view();
     }
+    // pass 0's first sweep by id ranges (FirstSweep), each waiting for its chunk
+    const int R0 = pass == 0 ? fs.ranges() : 1;
+    std::vector<Bins> fbins(R0 > 1 ? R0 : 0);
+    for (int k = 0; k < R0 && R0 > 1; ++k)
+      compute_bins(cur.off + fs.vb[k], fs.vb[k + 1] - fs.vb[k], edges, fbins[k], s, ~u64(0), fs.vb[k]);
     const auto t0 = Clock::now();
     int iterations = 0;
     // iteration 0 sweeps every row with arcs (all flagged); later iterations
@@ -1135,7 +1241,16 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       a.pickless = pick_less_active(it, p.pick_less_period);
       LVN_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(IterRecord), s));
       size_t sp0 = 0;
-      for (int k = 0; k < R; ++k) {
+      if (it == 0 && R0 > 1) {
+        for (int k = 0; k < R0; ++k) {
+          if (!fs.ev.empty()) LVN_CUDA(cudaStreamWaitEvent(s, fs.ev[k]));
+          sp = tm.begin(LVN_STAT_MOVE, s);
+          if (k == 0) sp0 = sp;
+          move_sweep(a, fbins[k].view(), p.value_bits, s);
+          tm.end(sp, s, 0.0);
+        }
+      }
+      for (int k = 0; k < R && !(it == 0 && R0 > 1); ++k) {
         if (shard) LVN_CUDA(cudaMemsetAsync(a.moves_n, 0, sizeof(u32), s));
         sp = tm.begin(LVN_STAT_MOVE, s);
         if (k == 0) sp0 = sp;
@@ -1193,6 +1308,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
           for (int b = 0; b < kBins; ++b) views[k].cnt[b] = h->active[k * kBins + b];
         }
     }
+    for (cudaEvent_t e : (pass == 0 ? fs.ev : std::vector<cudaEvent_t>())) LVN_CUDA(cudaStreamWaitEvent(s, e));
     t_move += since(t0);
     check_err(err.p, s);
     check_membership("after local moving", C.p, nv, nv, s);
@@ -1365,6 +1481,10 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     levels.clear();
   }
   cm.settle();
+  if (fs.t0) {
+    float ms = 0.f;
+    if (cudaEventElapsedTime(&ms, fs.t0, fs.t1) == cudaSuccess) r->h2d_seconds = ms * 1e-3;
+  }
   r->h2d_bytes = ig.h2d_bytes;
   r->num_shards = cm.size();
   r->sharded_passes = sharded_passes;
@@ -1462,6 +1582,7 @@ void lvn_params_default(lvn_params* p) {
   p->shard_min_arcs_log2 = 22;
   p->shard_rounds = 0;
   p->keep_levels = 0;
+  p->first_range_arcs_log2 = 29;
 }
 
 int lvn_init(int num_gpus, const int* devices) {

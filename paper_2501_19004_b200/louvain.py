@@ -129,6 +129,7 @@ class CompactOptions:  # louvain_compact.hpp:35-40
     singleton_rule: bool = False  # singleton joins singleton only toward the lower id
     shard_min_arcs_log2: int = 22  # louvain_sharded: shard passes with >= 2**this arcs
     shard_rounds: int = 0  # louvain_sharded: exchanges per iteration (rounds over own rows); 0 = 2 x ranks
+    first_range_arcs_log2: int = 29  # pass 0's first sweep in id ranges of 2**this arcs (upload overlap); 0 off
 
 
 @dataclass
@@ -326,6 +327,7 @@ def _params(params: LouvainParams | None, options: CompactOptions | None, on_dev
     p.shard_min_arcs_log2 = options.shard_min_arcs_log2
     p.shard_rounds = options.shard_rounds
     p.keep_levels = int(bool(keep_levels))
+    p.first_range_arcs_log2 = options.first_range_arcs_log2
     return p
 
 
