@@ -264,6 +264,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--shard-rounds", type=int, default=0, help="N>1: exchanges per local-moving iteration (0 = 2N)")
+    ap.add_argument("--shard-min-arcs-log2", type=int, default=22,
+                    help="N>1: passes with fewer arcs are gathered onto rank 0 (the collapse)")
     args = ap.parse_args()
     if args.warmup < 3:
         args.warmup = 3
@@ -304,14 +306,18 @@ def main():
     dg = lvn.generate(cfg["kind"], **{k: v for k, v in cfg.items() if k not in ("kind", "desc")})
     n, arcs = dg.num_vertices(), dg.num_arcs()
     log(f"[rank {rank}] {args.config}: {n} vertices, {arcs} arcs, generated in {time.time() - t0:.1f}s")
-    opts = lvn.CompactOptions(value_bits=args.value_bits, shard_rounds=args.shard_rounds)
+    opts = lvn.CompactOptions(value_bits=args.value_bits, shard_rounds=args.shard_rounds,
+                              shard_min_arcs_log2=args.shard_min_arcs_log2)
     # N > 1: one process per GPU, passes sharded by row range over NCCL
     # (SURVEY.md 8(e)); the whole job's work is fixed as N grows (strong scaling)
+    # The collectives are the library's own NCCL communicator (stream-ordered
+    # inside liblvn.so, no Python on the data path); LVN_DIST_BACKEND=gloo
+    # (several ranks sharing one GPU) goes through torch.distributed instead.
     comm = None
     if world > 1:
-        from paper_2501_19004_b200.distributed import Collectives
+        from paper_2501_19004_b200.distributed import Collectives, NcclComm
 
-        comm = Collectives(location="cuda")
+        comm = NcclComm() if os.environ.get("LVN_DIST_BACKEND", "nccl") == "nccl" else Collectives(location="cuda")
 
     def run(g, on_device):
         if comm is not None:

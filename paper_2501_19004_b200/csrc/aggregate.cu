@@ -76,7 +76,7 @@ __global__ void __launch_bounds__(256) ag_sort(AggArgs x, const u32* __restrict_
         if (e >= base && e < base + d) {
           const u64 a = lo + (e - base);
           key[r] = x.C[__ldcs(x.g.tgt + a)];
-          val[r] = double(__ldcs(x.g.w + a));
+          val[r] = double(arc_w(x.g, a));
         }
       }
       base += d;
@@ -165,7 +165,7 @@ __global__ void __launch_bounds__(256) ag_psort(AggArgs x, const u32* __restrict
         if (e < total) {
           const u64 a = lo_j + (e - st_j);
           key[r] = (x.C[__ldcs(x.g.tgt + a)] << LB) | u32(e);
-          gw[e] = __ldcs(x.g.w + a);
+          gw[e] = arc_w(x.g, a);
         }
       }
     } else {
@@ -179,7 +179,7 @@ __global__ void __launch_bounds__(256) ag_psort(AggArgs x, const u32* __restrict
           if (e >= base && e < base + d) {
             const u64 a = lo + (e - base);
             key[r] = (x.C[__ldcs(x.g.tgt + a)] << LB) | u32(e);
-            gw[e] = __ldcs(x.g.w + a);
+            gw[e] = arc_w(x.g, a);
           }
         }
         base += d;
@@ -227,7 +227,7 @@ __device__ __forceinline__ void merge_row(const AggArgs& x, const Tab& tab, u32 
   const u64 lo = x.g.off[v], hi = x.g.off[v + 1];
   for (u64 a = lo + lane; a < hi; a += stride) {
     const u32 key = x.C[x.g.tgt[a]];
-    const double w = double(x.g.w[a]);
+    const double w = double(arc_w(x.g, a));
     if (key == c) {
       own += w;
       own_seen = 1;
@@ -368,7 +368,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
         const u32 v = x.members[mlo + lo];
         const u64 a = x.g.off[v] + (e - pre[lo]);
         key = x.C[__ldcs(x.g.tgt + a)];
-        w = double(__ldcs(x.g.w + a));
+        w = double(arc_w(x.g, a));
       }
       ag_merge_round(tab, lg, c, key, w, lane, own, own_seen);
     }
@@ -382,7 +382,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
       for (u64 a0 = lo; a0 < hi; a0 += 32) {
         const u64 a = a0 + lane;
         const u32 key = a < hi ? x.C[__ldcs(x.g.tgt + a)] : kEmpty;
-        const double w = a < hi ? double(__ldcs(x.g.w + a)) : 0.0;
+        const double w = a < hi ? double(arc_w(x.g, a)) : 0.0;
         ag_merge_round(tab, lg, c, key, w, lane, own, own_seen);
       }
     }
@@ -396,7 +396,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
       }
       for (; __any_sync(0xffffffffu, a < hi); ++a) {
         const u32 key = a < hi ? x.C[x.g.tgt[a]] : kEmpty;
-        const double w = a < hi ? double(x.g.w[a]) : 0.0;
+        const double w = a < hi ? double(arc_w(x.g, a)) : 0.0;
         ag_merge_round(tab, lg, c, key, w, lane, own, own_seen);
       }
     }
@@ -701,7 +701,7 @@ __global__ void __launch_bounds__(kBigThreads) ag_big_arcs(AggArgs x, BigState s
       if (e < nA) {
         const u64 ga = s_base[s_own[e]] + lo + e;
         cp_async4(&s_tgt[e], x.g.tgt + ga);
-        cp_async4(&s_w[e], x.g.w + ga);
+        if (!x.g.uniform) cp_async4(&s_w[e], x.g.w + ga);
       }
     }
     cp_async_wait_all();
@@ -722,7 +722,7 @@ __global__ void __launch_bounds__(kBigThreads) ag_big_arcs(AggArgs x, BigState s
         const u32 o = s_own[e];
         c = s_c[o];
         pi = s_pi[o];
-        wt = double(s_w[e]);
+        wt = x.g.uniform ? double(x.g.uw) : double(s_w[e]);
         if (kk == c) {
           if (pi != own_pi) {
             if (seen) atomicAdd(&st.own_sum[own_pi], own), st.own_seen[own_pi] = 1;

@@ -1111,6 +1111,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   for (int pass = 0; pass < p.max_passes && !idle; ++pass) {
     const auto t_pass = Clock::now();
     const u32 nv = cur.n;
+    if (!sharded) v0 = 0, v1 = nv;  // a whole-graph pass owns every row
     Bins& B = pass == 0 ? in_bins : bins;
     // sharded: the bins (and every sweep) cover the own rows only
     if (sharded) compute_bins(cur.off + v0, v1 - v0, edges, B, s, ~u64(0), v0);
@@ -1173,6 +1174,10 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
         if (uniform) uniform_w = read_scalar(cur.w, s);
       }
     }
+    // kernels of this pass (sweeps, aggregation) take the constant weight
+    cur.uniform = uniform ? 1 : 0;
+    cur.uw = uniform_w;
+    if (pass == 0) ig.g.uniform = cur.uniform, ig.g.uw = uniform_w;
 
     const bool shard = sharded;
     if (shard) {
@@ -1978,6 +1983,8 @@ int evaluate_moves_impl(const lvn_csr* g, const uint32_t* membership, const doub
       if (ig.g.arcs && !no_uniform() && read_scalar(uni.p, s) != 0) {
         a.uniform = 1;
         a.uniform_w = read_scalar(ig.g.w, s);
+        a.g.uniform = 1;
+        a.g.uw = a.uniform_w;
       }
     }
     a.out_to = ot.p;

@@ -50,7 +50,7 @@ __global__ void mod_thread(DGraph g, const u32* __restrict__ list, u64 count,
         out += C[g.tgt[a]] != c;
         continue;
       }
-      const double w = double(g.w[a]);
+      const double w = double(arc_w(g, a));
       k += w;
       if (C[g.tgt[a]] == c) in += w;
     }
@@ -94,7 +94,7 @@ __global__ void __launch_bounds__(256) mod_group(DGraph g, const u32* __restrict
       for (int r = 0; r < K; ++r) {
         const u64 a = lo[j] + u64(r) * G + lane;
         t[j][r] = a < hi[j] ? __ldcs(g.tgt + a) : kEmpty;
-        w[j][r] = X ? 0.f : a < hi[j] ? __ldcs(g.w + a) : 0.f;
+        w[j][r] = X ? 0.f : a < hi[j] ? arc_w(g, a) : 0.f;
       }
     }
     u32 ct[2][K];
@@ -147,7 +147,7 @@ __global__ void mod_warp(DGraph g, const u32* __restrict__ list, u64 count,
       if (lane == 0 && out) atomicAdd(&ext[c], ull(out));
     } else {
       for (u64 a = g.off[v] + lane; a < g.off[v + 1]; a += 32) {
-        const double w = double(g.w[a]);
+        const double w = double(arc_w(g, a));
         k += w;
         if (C[g.tgt[a]] == c) in += w;
       }
@@ -181,7 +181,7 @@ __global__ void __launch_bounds__(512) mod_block(DGraph g, const u32* __restrict
     }
     double k = 0.0;
     for (u64 a = g.off[v] + threadIdx.x; a < g.off[v + 1]; a += blockDim.x) {
-      const double w = double(g.w[a]);
+      const double w = double(arc_w(g, a));
       k += w;
       if (C[g.tgt[a]] == c) internal += w;
     }

@@ -259,7 +259,7 @@ __device__ __forceinline__ void scan_arcs(const MoveArgs& x, const Tab& tab, u32
     for (int k = 0; k < B; ++k) {
       const u64 a = b0 + lane + u64(k) * stride;
       t[k] = a < hi ? __ldcs(x.g.tgt + a) : u;  // out of range reads as a self-loop: skipped
-      w[k] = a < hi ? V(__ldcs(x.g.w + a)) : V(0);
+      w[k] = a < hi ? V(arc_w(x.g, a)) : V(0);
     }
 #pragma unroll
     for (int k = 0; k < B; ++k) c[k] = t[k] != u ? x.C[t[k]] : kEmpty;
@@ -1010,7 +1010,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_block(MoveArgs x, const u32*
       for (int k = 0; k < kBatch; ++k) {
         const u64 e = b0 + lt + u64(k) * ST;
         t[k] = e < d ? __ldcs(x.g.tgt + lo + e) : kEmpty;
-        w[k] = e < d ? __ldcs(x.g.w + lo + e) : 0.f;
+        w[k] = e < d ? arc_w(x.g, lo + e) : 0.f;
       }
 #pragma unroll
       for (int k = 0; k < kBatch; ++k) {

@@ -305,6 +305,22 @@ def test_engine_chunked_hubs(lvn, port):
     assert r.modularity > 0.0
 
 
+@pytest.mark.parametrize("opts", [dict(sweep_ranges=4), dict(sweep_ranges=16), dict(sweep_order=1),
+                                  dict(singleton_rule=True), dict(sweep_chunk=1024), dict(value_bits=64),
+                                  dict(sweep_ranges=4, sweep_order=1)])
+def test_engine_sweep_options(lvn, port, opts):
+    # every sweep-order knob over a multi-pass run (hubs, block rows and sort
+    # bins in every range): Q recomputed by the oracle, contiguous ids, quality
+    # within the reference gate of the default sweep
+    g = hubs_graph(60000, 8, 30000, 400000, 2)
+    base = lvn.louvain_compact(G_(g, lvn)).modularity
+    r = lvn.louvain_compact(G_(g, lvn), None, lvn.CompactOptions(**opts))
+    m = np.asarray(r.membership, np.uint32)
+    assert_q(r.modularity, port.modularity(g, m))
+    assert set(np.unique(m)) == set(range(r.num_communities)) and r.passes >= 2
+    assert r.modularity >= base - 0.01
+
+
 # ------------------------------------------------------------ engine end to end
 def test_engine_fixture_optima(lvn):
     r = lvn.louvain_compact(G_(from_triples(TWO_TRIANGLES), lvn))
