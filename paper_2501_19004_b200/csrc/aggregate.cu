@@ -43,9 +43,14 @@ using Tab = SplitF64;
 // fp64 sum -> f32 super-graph weight (narrowed once, louvain_mc.cpp:95); a
 // narrowing that loses bits raises *x.inexact (then the engine computes the
 // final modularity on the input graph instead of the last super-graph)
-__device__ __forceinline__ float narrow(const AggArgs& x, double v) {
+__device__ __forceinline__ float narrow(const AggArgs& x, u32 key, u32 c, double v) {
   const float f = float(v);
-  if (x.inexact && double(f) != v) *x.inexact = 1u;
+  if (key == c) {
+    // the super-vertex self-loop (its internal weight) keeps its fp64 sum
+    if (x.self64) x.self64[c] = v;
+  } else if (x.inexact && double(f) != v) {
+    *x.inexact = 1u;
+  }
   return f;
 }
 
@@ -98,7 +103,7 @@ __global__ void __launch_bounds__(256) ag_sort(AggArgs x, const u32* __restrict_
         for (int r = 0; r < K; ++r) {
           if (tail[r] && key[r] != kEmpty) {
             x.htgt[hbase + pos] = key[r];
-            x.hw[hbase + pos] = narrow(x, val[r]);  // fp64 sum narrowed once
+            x.hw[hbase + pos] = narrow(x, key[r], c, val[r]);  // fp64 sum narrowed once
             ++pos;
           }
         }
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(256) ag_psort(AggArgs x, const u32* __restrict
         for (int r = 0; r < K; ++r) {
           if (tail[r] && ck[r] != kEmpty) {
             x.htgt[hbase + pos] = ck[r];
-            x.hw[hbase + pos] = narrow(x, val[r]);  // fp64 sum narrowed once
+            x.hw[hbase + pos] = narrow(x, ck[r], c, val[r]);  // fp64 sum narrowed once
             ++pos;
           }
         }
@@ -276,14 +281,14 @@ __global__ void __launch_bounds__(THREADS) ag_group(AggArgs x, const u32* __rest
       if (live) {
         const u64 o = hbase + pos + __popc(bal & ((1u << lane) - 1u));
         x.htgt[o] = key;
-        x.hw[o] = narrow(x, val);
+        x.hw[o] = narrow(x, key, c, val);
       }
       pos += __popc(bal);
     }
     if (lane == 0) {
       if (own_seen) {
         x.htgt[hbase + pos] = c;
-        x.hw[hbase + pos] = narrow(x, own);
+        x.hw[hbase + pos] = narrow(x, c, c, own);
         ++pos;
       }
       if (pos > hcap) atomicOr(x.err, u32(kErrTable));
@@ -412,7 +417,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
     if (tab.read(s, key, val)) {
       const u32 o = atomicAdd(cursor, 1u);
       x.htgt[hbase + o] = key;
-      x.hw[hbase + o] = narrow(x, val);
+      x.hw[hbase + o] = narrow(x, key, c, val);
     }
   }
   __syncthreads();
@@ -423,7 +428,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
     u64 pos = *cursor;
     if (seen) {
       x.htgt[hbase + pos] = c;
-      x.hw[hbase + pos] = narrow(x, t);
+      x.hw[hbase + pos] = narrow(x, c, c, t);
       ++pos;
     }
     if (pos > hcap) atomicOr(x.err, u32(kErrTable));
@@ -794,7 +799,7 @@ __global__ void __launch_bounds__(256) ag_dense_scan(AggArgs x, BigState st, con
         const u32 o = wbase + __popc(bal & ((1u << lane) - 1u));
         if (o < hcap) {
           x.htgt[hbase + o] = u32(j);
-          x.hw[hbase + o] = narrow(x, __longlong_as_double((long long)bits));  // fp64 sum narrowed once
+          x.hw[hbase + o] = narrow(x, u32(j), c, __longlong_as_double((long long)bits));  // fp64 sum narrowed once
         }
       }
     }
@@ -818,7 +823,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, BigState
       for (u32 j = threadIdx.x; j < n && j < hcap; j += kBlockThreads) {
         const BigSlot e = t[live[j]];
         x.htgt[hbase + j] = e.key;
-        x.hw[hbase + j] = narrow(x, e.val);  // fp64 sum narrowed once
+        x.hw[hbase + j] = narrow(x, e.key, c, e.val);  // fp64 sum narrowed once
       }
     }
     if (threadIdx.x == 0) {
@@ -827,7 +832,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, BigState
       } else {
         if (self) {
           x.htgt[hbase + n] = c;
-          x.hw[hbase + n] = narrow(x, st.own_sum[i]);
+          x.hw[hbase + n] = narrow(x, c, c, st.own_sum[i]);
         }
         x.fill[c] = n + self;
       }

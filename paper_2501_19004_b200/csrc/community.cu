@@ -255,4 +255,18 @@ void fill_u32(u32* p, u64 n, u32 v, cudaStream_t s) {
   LVN_LAUNCH();
 }
 
+__global__ void sum_by_community_k(const u32* __restrict__ C, const double* __restrict__ v, u64 n,
+                                   double* __restrict__ out) {
+  for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x)
+    if (v[u] != 0.0) atomicAdd(&out[C[u]], v[u]);
+}
+
+void sum_by_community(const u32* C, const double* v, u64 n, double* out, u32 count, cudaStream_t s) {
+  LVN_CUDA(cudaMemsetAsync(out, 0, size_t(count ? count : 1) * sizeof(double), s));
+  if (!n) return;
+  const u64 blocks = std::min<u64>((n + 255) / 256, u64(sm_count()) * 8);
+  sum_by_community_k<<<unsigned(blocks), 256, 0, s>>>(C, v, n, out);
+  LVN_LAUNCH();
+}
+
 }  // namespace lvn

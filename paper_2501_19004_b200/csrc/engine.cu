@@ -698,7 +698,7 @@ bool verbose() {
 // ---- aggregation of a graph by a contiguous membership ----------------------
 void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
                       u32* err, cudaStream_t s, bool canonical, const Bins* gbins = nullptr,
-                      u32* inexact = nullptr) {
+                      u32* inexact = nullptr, double* self64 = nullptr) {
   DBuf<u32> msize(count ? count : 1);
   DBuf<u64> budget(count + 1), coff(count + 1), boff(count + 1), hoff(count + 1), capped(count + 1),
       ext(count + 1);
@@ -747,6 +747,8 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   a.fill = fill.p;
   a.err = err;
   a.inexact = inexact;
+  a.self64 = self64;
+  if (self64) LVN_CUDA(cudaMemsetAsync(self64, 0, size_t(count ? count : 1) * sizeof(double), s));
   aggregate_rows(a, ab, s);
   if (check_mode()) {
     std::vector<u64> h_coff(count + 1), h_boff(count + 1), h_hoff(count + 1), h_off(u64(g.n) + 1);
@@ -1081,6 +1083,9 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   // break), else `cur` is the last aggregated graph (its vertices are the
   // final communities)
   bool ended_in_C = false;
+  // exact fp64 total degree and self-loop of every vertex of `cur` after an
+  // aggregation (for the final modularity on the last super-graph)
+  DBuf<double> kx_cur, kx_next, self_cur, self_next;
 
   Bins in_bins, bins;
   bool have_in_bins = false;
@@ -1357,7 +1362,12 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       aggregate_sharded(cur, C.p, count, v0, v1, cm, next, cb, s);
       v0 = cb[cm.rank()], v1 = cb[cm.rank() + 1];
     } else {
-      aggregate_device(cur, C.p, count, edges, next, err.p, s, false, &B, inexact.p);
+      self_next.ensure(count ? count : 1);
+      kx_next.ensure(count ? count : 1);
+      aggregate_device(cur, C.p, count, edges, next, err.p, s, false, &B, inexact.p, self_next.p);
+      sum_by_community(C.p, pass == 0 ? K.p : kx_cur.p, nv, kx_next.p, count, s);
+      std::swap(kx_cur, kx_next);
+      std::swap(self_cur, self_next);
     }
     tm.end(sp, s, 12.0 * double(cur.arcs) + 16.0 * nv + 8.0 * double(next.arcs) + 8.0 * (count + 1.0),
            nv, cur.arcs);
@@ -1398,20 +1408,24 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     if (!have_in_bins) compute_bins(ig.g.off + v0, v1 - v0, edges, in_bins, s, ~u64(0), v0);
     q = modularity_sharded(ig.g, in_bins, global.p, count, m, cm, s);
   } else if (!dist && aggregations > 0 && read_scalar(inexact.p, s) == 0) {
-    // Every super-graph weight is its fp64 sum exactly (no narrowing lost a
-    // bit), so the final communities' internal and total weights on the last
-    // graph equal those on the input (aggregation conserves them, the
-    // reference's own check: test_mc.cpp:209-219) and Q (quality.cpp:30-41)
-    // is evaluated there: 25.7 M arcs instead of 3.8 G on C5
-    Bins lb;
-    compute_bins(cur.off, cur.n, edges, lb, s);
+    // Aggregation conserves every community's internal and total weight (the
+    // super-vertex self-loop is the internal weight: test_mc.cpp:209-219), so
+    // Q of the final partition (quality.cpp:30-41) is evaluated on the last
+    // super-graph: its self-loops and vertex degrees in fp64 as the
+    // aggregations summed them, its other arcs exact (no narrowing of a
+    // non-self entry lost a bit). 25.7 M arcs instead of 3.8 G on C5.
     const u32* memb = C.p;
     if (!ended_in_C) {
       rank.ensure(cur.n ? cur.n : 1);
       iota_u32(rank.p, cur.n, s);
       memb = rank.p;
     }
-    q = modularity_device(cur, lb, memb, cur.n, m, s);
+    DBuf<double> tot(cur.n ? cur.n : 1), sums(2);
+    modularity_exact(cur, memb, kx_cur.p, self_cur.p, tot.p, cur.n, sums.p, s, 2.0 * m);
+    double* h = reinterpret_cast<double*>(c.pinned);
+    LVN_CUDA(cudaMemcpyAsync(h, sums.p, 2 * sizeof(double), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    q = h[0] / (2.0 * m) - h[1];
     q_arcs = cur.arcs, q_verts = cur.n;
   } else if (!idle || !dist) {
     if (!have_in_bins) compute_bins(ig.g.off, N, edges, in_bins, s);

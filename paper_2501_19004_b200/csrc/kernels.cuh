@@ -159,6 +159,8 @@ void community_scatter(const u32* C, u32 n, const u64* coff, u32 count, u32* cur
 void segmented_sort_u32(u32* keys, float* vals, const u64* off, u32 nseg, u64 max_seg,
                         cudaStream_t s);
 void iota_u32(u32* p, u64 n, cudaStream_t s);
+// out[c] = sum of v[u] over C[u] == c (fp64; out zeroed here, count entries)
+void sum_by_community(const u32* C, const double* v, u64 n, double* out, u32 count, cudaStream_t s);
 void fill_u32(u32* p, u64 n, u32 v, cudaStream_t s);
 
 // ---- aggregate.cu -----------------------------------------------------------
@@ -174,7 +176,8 @@ struct AggArgs {
   float* hw = nullptr;
   u32* fill = nullptr;           // entries written per row
   u32* err = nullptr;
-  u32* inexact = nullptr;        // set when a narrowing to f32 loses bits (may be null)
+  u32* inexact = nullptr;        // set when narrowing a non-self entry to f32 loses bits (may be null)
+  double* self64 = nullptr;      // fp64 self-loop (internal weight) of every super-vertex (may be null)
   int big_mode = 0;              // giant-community regions: 0 by size, 1 hash, 2 dense (LVN_BIG_MODE)
 };
 // Synchronises once when the kBinGlobal bin is non-empty (sizes its HBM tables).
@@ -195,6 +198,10 @@ void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot,
 void modularity_rows(const DGraph& g, const Bins& b, const u32* C, double* tot, u64 width, double* sums,
                      cudaStream_t s);
 void modularity_squares(const double* tot, u64 width, double two_m, double* sums, cudaStream_t s);
+// modularity_terms on a super-graph whose per-vertex total degree (kx) and
+// self-loop (self64) are given exactly in fp64 (the f32 arcs of self-loops are ignored)
+void modularity_exact(const DGraph& g, const u32* C, const double* kx, const double* self64, double* tot, u64 width,
+                      double* sums, cudaStream_t s, double two_m);
 // ext[c] = arcs from members of c to other communities (width entries, zeroed
 // here): bounds the distinct targets of super-row c (aggregation capacities)
 void external_arcs(const DGraph& g, const Bins& b, const u32* C, u64* ext, u64 width, cudaStream_t s);

@@ -272,6 +272,43 @@ void modularity_terms(const DGraph& g, const Bins& b, const u32* C, double* tot,
   modularity_squares(tot, width, two_m, sums, s);
 }
 
+// Q of the last super-graph with exact per-vertex terms: internal weight =
+// the fp64 self-loop self64[v] + the arcs to other members of v's community,
+// total degree Kx[v] (fp64); a warp per vertex
+__global__ void mod_exact_k(DGraph g, const u32* __restrict__ C, const double* __restrict__ kx,
+                            const double* __restrict__ self64, double* __restrict__ tot, double* __restrict__ sums) {
+  const u32 lane = threadIdx.x & 31;
+  const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
+  double internal = 0.0;
+  for (u64 v = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; v < g.n; v += warps) {
+    const u32 c = C[v];
+    double in = 0.0;
+    for (u64 a = g.off[v] + lane; a < g.off[v + 1]; a += 32) {
+      const u32 t = g.tgt[a];
+      if (t != v && C[t] == c) in += double(arc_w(g, a));
+    }
+    in = warp_sum(in);
+    if (lane == 0) {
+      internal += in + self64[v];
+      if (kx[v] != 0.0) atomicAdd(&tot[c], kx[v]);
+    }
+  }
+  internal = warp_sum(internal);
+  if (lane == 0 && internal != 0.0) atomicAdd(&sums[0], internal);
+}
+
+void modularity_exact(const DGraph& g, const u32* C, const double* kx, const double* self64, double* tot, u64 width,
+                      double* sums, cudaStream_t s, double two_m) {
+  LVN_CUDA(cudaMemsetAsync(tot, 0, (width ? width : 1) * sizeof(double), s));
+  LVN_CUDA(cudaMemsetAsync(sums, 0, 2 * sizeof(double), s));
+  if (g.n) {
+    const u64 blocks = std::min<u64>((u64(g.n) + 7) / 8, u64(sm_count()) * 8);
+    mod_exact_k<<<unsigned(blocks), 256, 0, s>>>(g, C, kx, self64, tot, sums);
+    LVN_LAUNCH();
+  }
+  modularity_squares(tot, width, two_m, sums, s);
+}
+
 void external_arcs(const DGraph& g, const Bins& b, const u32* C, u64* ext, u64 width, cudaStream_t s) {
   LVN_CUDA(cudaMemsetAsync(ext, 0, width * sizeof(u64), s));
   row_pass<true>(g, b, C, nullptr, nullptr, reinterpret_cast<ull*>(ext), s);

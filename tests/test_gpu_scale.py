@@ -98,3 +98,25 @@ def test_first_sweep_weighted_input_copies_weights(lvn, port):
     r = lvn.louvain_compact(G, None, lvn.CompactOptions(first_range_arcs_log2=18))
     assert abs(r.modularity - port.modularity(g, np.asarray(r.membership, np.uint32))) <= 1e-9
     assert r.h2d_bytes == 8 * (g.n + 1) + 8 * g.offsets[-1]
+
+
+def test_final_modularity_on_super_graph_with_lossy_self_loops(lvn, port):
+    """Two planted blocks of 500 K vertices (mean degree 48): every community's
+    internal weight exceeds 2^24, so the f32 self-loops of the super-graph are
+    rounded, while the arcs between communities stay exact. The engine
+    evaluates the final Q on the last super-graph with the fp64 self-loops and
+    degrees its aggregations summed; it must equal the oracle's Q on the input
+    graph within 1e-9."""
+    dg = lvn.generate("sbm", n=1_000_000, blocks=2, avg_degree=48, mu=0.1, seed=31)
+    h = dg.download()
+    r = lvn.louvain_compact(dg)
+    m = np.asarray(r.membership, np.uint32)
+    q = port.modularity(h, m)
+    assert abs(r.modularity - q) <= 1e-9 * abs(q)
+    assert r.aggregations >= 1
+    assert r.stats["modularity"].arcs < h.num_arcs()  # evaluated on the last super-graph
+    # the super-graph of the final partition does round its self-loops
+    sg = lvn.compact_aggregate(dg, m)
+    self_w = [float(sg.weights[k]) for c in range(sg.num_vertices())
+              for k in range(int(sg.offsets[c]), int(sg.offsets[c + 1])) if sg.targets[k] == c]
+    assert max(self_w) > 2 ** 24
