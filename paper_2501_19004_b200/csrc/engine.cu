@@ -705,10 +705,15 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   community_counts(g, C, count, msize.p, budget.p, s);
   exclusive_scan_u32_to_u64(msize.p, coff.p, count, s);
   exclusive_scan_u64(budget.p, boff.p, count, s);
-  // holey row capacity min(ext + 1, count): a super-row's distinct targets are
-  // at most its arcs to other communities plus the self-loop, and at most
-  // count (ext: one row pass over the graph, binned like the modularity pass)
-  {
+  // Holey row capacity: a super-row's distinct targets are at most its
+  // member arcs (the budget) and at most count (engine_detail.cpp:66-75).
+  // When those rows would take more than an eighth of the free device memory
+  // (C5's first aggregation: ~30 GB), the capacity is tightened to
+  // min(ext + 1, count), ext = the community's arcs to other communities
+  // (one row pass over the graph, binned like the modularity pass).
+  cap_budgets(budget.p, capped.p, count, s, false);
+  exclusive_scan_u64(capped.p, hoff.p, count, s);
+  if (read_scalar(hoff.p + count, s) * 8 > ctx().pool.available() / 8) {
     Bins local;
     const Bins* gb = gbins;
     if (!gb) {
@@ -716,9 +721,9 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
       gb = &local;
     }
     external_arcs(g, *gb, C, ext.p, count, s);
+    cap_budgets(ext.p, capped.p, count, s, true);
+    exclusive_scan_u64(capped.p, hoff.p, count, s);
   }
-  cap_budgets(ext.p, capped.p, count, s);
-  exclusive_scan_u64(capped.p, hoff.p, count, s);
   DBuf<u32> members(g.n ? g.n : 1), cursor(count ? count : 1);
   community_scatter(C, g.n, coff.p, count, cursor.p, members.p, s);
   msize.release();
@@ -1549,15 +1554,16 @@ struct DGraphHandle {
 // holey-row capacity kernel (used by aggregate_device)
 namespace lvn {
 // capped[c] = min(ext[c] + 1, count): holey row capacity
-__global__ void cap_budgets_k(const u64* __restrict__ ext, u64* __restrict__ capped, u32 count) {
+// capped[c] = min(x[c] + plus_one, count)
+__global__ void cap_budgets_k(const u64* __restrict__ x, u64* __restrict__ capped, u32 count, u32 plus_one) {
   for (u64 c = blockIdx.x * u64(blockDim.x) + threadIdx.x; c < count;
        c += u64(gridDim.x) * blockDim.x)
-    capped[c] = ext[c] + 1 < count ? ext[c] + 1 : u64(count);
+    capped[c] = x[c] + plus_one < count ? x[c] + plus_one : u64(count);
 }
-void cap_budgets(const u64* ext, u64* capped, u32 count, cudaStream_t s) {
+void cap_budgets(const u64* x, u64* capped, u32 count, cudaStream_t s, bool plus_one) {
   if (!count) return;
   const u64 blocks = std::min<u64>((u64(count) + 255) / 256, u64(sm_count()) * 8);
-  cap_budgets_k<<<unsigned(blocks), 256, 0, s>>>(ext, capped, count);
+  cap_budgets_k<<<unsigned(blocks), 256, 0, s>>>(x, capped, count, plus_one ? 1u : 0u);
   LVN_LAUNCH();
 }
 }  // namespace lvn

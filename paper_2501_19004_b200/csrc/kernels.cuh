@@ -182,8 +182,9 @@ struct AggArgs {
 };
 // Synchronises once when the kBinGlobal bin is non-empty (sizes its HBM tables).
 void aggregate_rows(const AggArgs& a, const Bins& bins, cudaStream_t s);
-// capped[c] = min(ext[c] + 1, count): holey row capacity (ext: external_arcs)
-void cap_budgets(const u64* ext, u64* capped, u32 count, cudaStream_t s);
+// capped[c] = min(x[c] + plus_one, count): holey row capacity from the budget
+// (plus_one false) or from the external arcs (ext + 1 with the self-loop)
+void cap_budgets(const u64* x, u64* capped, u32 count, cudaStream_t s, bool plus_one);
 // out rows = holey rows compacted (noff = scan of fill), total weight (fp64) into *tw
 void compact_rows(const u64* hoff, const u32* htgt, const float* hw, const u32* fill,
                   const u64* noff, u32 count, u32* otgt, float* ow, double* tw,
