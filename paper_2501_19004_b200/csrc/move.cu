@@ -1172,9 +1172,16 @@ __global__ void hub_chunk_counts_k(const u32* __restrict__ hubs, u64 count, cons
   }
 }
 
+// chunk_hub[v] = the hub of chunk v (chunks of hub i: [chunk_off[i], chunk_off[i+1]))
+__global__ void hub_chunk_owner_k(const u64* __restrict__ chunk_off, u64 count, u32* __restrict__ chunk_hub) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < count; i += u64(gridDim.x) * blockDim.x)
+    for (u64 v = chunk_off[i]; v < chunk_off[i + 1]; ++v) chunk_hub[v] = u32(i);
+}
+
 template <class Tab>
 __global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const u32* __restrict__ hubs,
-                                                               u64 count, const u64* __restrict__ chunk_off) {
+                                                               u64 count, const u64* __restrict__ chunk_off,
+                                                               const u32* __restrict__ chunk_hub) {
   using V = typename Tab::V;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 nlive;
@@ -1186,11 +1193,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const
   __syncthreads();
   const u64 total = chunk_off[count];
   for (u64 v = blockIdx.x; v < total; v += gridDim.x) {
-    u64 lo = 0, hi = count;  // hub of chunk v: last i with chunk_off[i] <= v
-    while (hi - lo > 1) {
-      const u64 mid = (lo + hi) / 2;
-      if (chunk_off[mid] <= v) lo = mid; else hi = mid;
-    }
+    const u64 lo = chunk_hub[v];  // hub of chunk v
     const u32 u = hubs[lo];
     const u32 pi = x.hub_index[u];
     const u64 row = x.g.off[u], row_end = x.g.off[u + 1];
@@ -1242,6 +1245,7 @@ struct HubBest {
 template <class Tab, bool DRY>
 __global__ void __launch_bounds__(kBlockThreads) lm_hub_rank(MoveArgs x, const u32* __restrict__ hubs, u64 count,
                                                              const u64* __restrict__ chunk_off,
+                                                             const u32* __restrict__ chunk_hub,
                                                              HubBest* __restrict__ best) {
   using V = typename Tab::V;
   constexpr int W = kBlockThreads / 32;
@@ -1250,11 +1254,7 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_rank(MoveArgs x, const u
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   const u64 total = chunk_off[count];
   for (u64 v = blockIdx.x; v < total; v += gridDim.x) {
-    u64 lo = 0, hi = count;  // hub of chunk v
-    while (hi - lo > 1) {
-      const u64 mid = (lo + hi) / 2;
-      if (chunk_off[mid] <= v) lo = mid; else hi = mid;
-    }
+    const u64 lo = chunk_hub[v];  // hub of chunk v
     const u32 u = hubs[lo];
     const u32 pi = x.hub_index[u];
     const u64 d = x.g.off[u + 1] - x.g.off[u];
@@ -1339,15 +1339,11 @@ __global__ void lm_hub_decide(MoveArgs x, const u32* __restrict__ hubs, u64 coun
 
 // neighbour marks of the hubs that moved, chunk by chunk (louvain_compact.cpp:160-161)
 __global__ void lm_hub_mark(MoveArgs x, const u32* __restrict__ hubs, u64 count, const u64* __restrict__ chunk_off,
-                            const u8* __restrict__ moved) {
+                            const u32* __restrict__ chunk_hub, const u8* __restrict__ moved) {
   ull marks = 0;
   const u64 total = chunk_off[count];
   for (u64 v = blockIdx.x; v < total; v += gridDim.x) {
-    u64 lo = 0, hi = count;
-    while (hi - lo > 1) {
-      const u64 mid = (lo + hi) / 2;
-      if (chunk_off[mid] <= v) lo = mid; else hi = mid;
-    }
+    const u64 lo = chunk_hub[v];  // hub of chunk v
     if (!moved[lo]) continue;
     const u32 u = hubs[lo];
     const u64 row = x.g.off[u], row_end = x.g.off[u + 1];
@@ -1500,6 +1496,7 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         DBuf<u64> coff(std::min(step, all) + 1);
         // slices of every hub of a group: at most arcs / kHubChunk + hubs
         DBuf<HubBest> hbest(a.g.arcs / kHubChunk + std::min(step, all) + 1);
+        DBuf<u32> owner(a.g.arcs / kHubChunk + std::min(step, all) + 1);
         DBuf<u8> hmoved(std::min(step, all));
         auto kc = lm_hub_chunks<Tab>;
         constexpr size_t smem = hub_smem<Tab>();
@@ -1511,15 +1508,18 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
               hubs, cnt, a.g.off, chunks.p);
           LVN_LAUNCH();
           exclusive_scan_u32_to_u64(chunks.p, coff.p, cnt, s);
-          kc<<<unsigned(sms * occ), kBlockThreads, smem, s>>>(a, hubs, cnt, coff.p);
+          hub_chunk_owner_k<<<unsigned(std::min<u64>((cnt + 255) / 256, u64(sms) * 4)), 256, 0, s>>>(coff.p, cnt,
+                                                                                                    owner.p);
           LVN_LAUNCH();
-          lm_hub_rank<Tab, DRY><<<unsigned(sms * 4), kBlockThreads, 0, s>>>(a, hubs, cnt, coff.p, hbest.p);
+          kc<<<unsigned(sms * occ), kBlockThreads, smem, s>>>(a, hubs, cnt, coff.p, owner.p);
+          LVN_LAUNCH();
+          lm_hub_rank<Tab, DRY><<<unsigned(sms * 4), kBlockThreads, 0, s>>>(a, hubs, cnt, coff.p, owner.p, hbest.p);
           LVN_LAUNCH();
           lm_hub_decide<Tab, DRY><<<unsigned(std::min<u64>((cnt + 7) / 8, u64(sms) * 8)), 256, 0, s>>>(
               a, hubs, cnt, coff.p, hbest.p, hmoved.p);
           LVN_LAUNCH();
           if (!DRY && a.prune) {
-            lm_hub_mark<<<unsigned(sms * 8), 256, 0, s>>>(a, hubs, cnt, coff.p, hmoved.p);
+            lm_hub_mark<<<unsigned(sms * 8), 256, 0, s>>>(a, hubs, cnt, coff.p, owner.p, hmoved.p);
             LVN_LAUNCH();
           }
         }

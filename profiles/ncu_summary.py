@@ -1,11 +1,14 @@
-"""Key counters of every kernel in an ncu report (raw page):
-python profiles/ncu_summary.py rep.ncu-rep"""
+"""Key counters of every kernel in an ncu report (raw page), or of a raw-page
+CSV export: python profiles/ncu_summary.py rep.ncu-rep|raw.csv"""
 import csv
 import io
 import subprocess
 import sys
 
-out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+if sys.argv[1].endswith(".csv"):
+    out = open(sys.argv[1]).read()
+else:
+    out = subprocess.run(["ncu", "-i", sys.argv[1], "--page", "raw", "--csv"], capture_output=True, text=True).stdout
 rows = list(csv.reader(io.StringIO(out)))
 h, units, data = rows[0], rows[1], rows[2:]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum", "lts__t_sector_hit_rate.pct",
