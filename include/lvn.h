@@ -44,9 +44,10 @@ enum lvn_status {
 /* where the arrays of an lvn_csr / a membership live */
 enum lvn_location { LVN_HOST = 0, LVN_DEVICE = 1 };
 
-/* Probing modes of the reference's slab tables (compact_hashtable.hpp:13-18).
- * Accepted and validated for option parity; the device tables use their own
- * power-of-two multiplicative-hash layout, which does not change results. */
+/* Probing modes of the reference's slab tables (compact_hashtable.hpp:13-18),
+ * applied by the device tables (power-of-two capacity, multiplicative hash)
+ * with the reference's stride recurrences (probe_advance,
+ * compact_hashtable.hpp:60-82); they change speed, never results. */
 enum lvn_probing { LVN_LINEAR = 0, LVN_QUADRATIC = 1, LVN_DOUBLE_HASH = 2, LVN_QUADRATIC_DOUBLE = 3 };
 
 /* Borrowed view of a CsrGraph (graph.hpp:38-54). Never freed by the library. */

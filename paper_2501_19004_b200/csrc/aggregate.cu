@@ -504,14 +504,17 @@ __device__ __forceinline__ u32 big_insert(BigSlot* t, u64 slots, u32 key, double
   const u32 lg = ceil_log2_u64(slots);
   const u32 mask = u32(slots - 1);
   u32 h = slot_hash(key, lg);
-  for (u64 probe = 0; probe < slots; ++probe) {
+  u32 stride = 1;
+  const u32 kmod = c_probing ? probe_kmod(key, lg) : 0u;
+  // the full walk: 2x slots probes in the mode, then a linear sweep of all slots
+  for (u64 probe = 0; probe < 3 * slots; ++probe) {
     const u32 cur = atomicCAS(&t[h].key, kEmpty, key);
     if (cur == kEmpty || cur == key) {
       atomicAdd(&t[h].val, w);
       fresh = cur == kEmpty;
       return h;
     }
-    h = (h + 1) & mask;
+    h = probe_next(h, mask, u32(probe), stride, kmod);
   }
   fresh = false;
   return ~0u;
@@ -1059,6 +1062,14 @@ void compact_rows(const u64* hoff, const u32* htgt, const float* hw, const u32* 
   const u64 blocks = std::min<u64>((u64(count) + 7) / 8, u64(sm_count()) * 16);
   compact_k<<<unsigned(blocks), 256, 0, s>>>(hoff, htgt, hw, fill, noff, count, otgt, ow, tw);
   LVN_LAUNCH();
+}
+
+// lvn_params.probing for the tables of this file (reference probe_advance,
+// compact_hashtable.hpp:60-82); stream-ordered
+void set_probing_aggregate(int mode, cudaStream_t s) {
+  static int value;  // pageable source: staged before the call returns
+  value = mode;
+  LVN_CUDA(cudaMemcpyToSymbolAsync(c_probing, &value, sizeof(int), 0, cudaMemcpyHostToDevice, s));
 }
 
 }  // namespace lvn

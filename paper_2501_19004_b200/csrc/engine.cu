@@ -1050,6 +1050,8 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   check_csr_header(in);
   const double m = in->total_weight;
   if (!(m > 0.0)) fail(kDegenerate, "cannot cluster a graph with zero total weight");
+  set_probing_move(p.probing, s);
+  set_probing_aggregate(p.probing, s);
   Comm solo;
   Comm& cm = comm ? *comm : solo;
   // Sharded runs: while a pass's graph has >= shard_min arcs
@@ -1900,6 +1902,7 @@ int lvn_aggregate(const lvn_csr* g, const uint32_t* membership, int membership_l
     const lvn_params& pp = p ? *p : def;
     validate(pp);
     cudaStream_t s = c.stream;
+    set_probing_aggregate(pp.probing, s);
     InGraph ig;
     load_graph(g, s, ig, nullptr);
     DevU32 m;
@@ -1955,6 +1958,7 @@ int evaluate_moves_impl(const lvn_csr* g, const uint32_t* membership, const doub
     if (!to || !gain || !vertex_w || !community_w) fail(kInvalid, "null argument");
     if (!(m > 0.0)) fail(kDegenerate, "m must be > 0");
     cudaStream_t s = c.stream;
+    set_probing_move(pp.probing, s);
     InGraph ig;
     load_graph(g, s, ig, nullptr);
     const u32 n = ig.g.n;

@@ -139,6 +139,9 @@ void hub_plan_build(const DGraph& g, const u32* hubs, u64 count, int value_bits,
 // K[u] from C[u] to `to`, and u's neighbours are flagged when prune is set
 void apply_moves(const u32* rec, u64 total, u64 skip_lo, u64 skip_hi, const DGraph& g, u32* C, const double* K,
                  double* sigma, u8* flags, int prune, cudaStream_t s);
+// table probing mode of the local-moving / aggregation kernels (lvn_probing)
+void set_probing_move(int mode, cudaStream_t s);
+void set_probing_aggregate(int mode, cudaStream_t s);
 // one sweep over the bins of `bins` (see the kBin* classes)
 void move_sweep(const MoveArgs& a, const BinView& bins, int value_bits, cudaStream_t s);
 

@@ -1615,4 +1615,12 @@ void move_sweep(const MoveArgs& a0, const BinView& b, int value_bits, cudaStream
   }
 }
 
+// lvn_params.probing for the tables of this file (reference probe_advance,
+// compact_hashtable.hpp:60-82); stream-ordered
+void set_probing_move(int mode, cudaStream_t s) {
+  static int value;  // pageable source: staged before the call returns
+  value = mode;
+  LVN_CUDA(cudaMemcpyToSymbolAsync(c_probing, &value, sizeof(int), 0, cudaMemcpyHostToDevice, s));
+}
+
 }  // namespace lvn

@@ -2,12 +2,12 @@
 study of Pick-Less period, scan-table value width, switch degrees and probing,
 PAPER.md:461-523, reproduced on B200). Run on the GPU box:
 
-    python profiles/ablation.py c1 c2 > profiles/r01_ablation.md
+    python profiles/ablation.py c1 c2 c3 c5 > profiles/r02_ablation.md
 
 Each row: mean modularity and mean device-resident wall time of 3 runs after a
-warm-up, relative to the default row. Probing modes are accepted for option
-parity but the device tables are power-of-two with linear probing, so the
-probing rows double as a noise estimate."""
+warm-up, relative to the default row. The probing rows run the device tables
+with the reference's probe recurrences (compact_hashtable.hpp:60-82; the
+default is quadratic-double, as in the reference)."""
 import os
 import statistics
 import sys
@@ -24,6 +24,7 @@ variants = [
     ("pick_less period 8", L(), O(pick_less=lvn.PickLessSchedule(period=8))),
     ("pick_less period 1000 (never)", L(), O(pick_less=lvn.PickLessSchedule(period=1000))),
     ("probing linear", L(), O(probing=lvn.Probing.linear)),
+    ("probing quadratic", L(), O(probing=lvn.Probing.quadratic)),
     ("probing double", L(), O(probing=lvn.Probing.double_hash)),
     ("bins: thread_max 0", L(), O(bins=lvn.DeviceBins(thread_max=0))),
     ("bins: thread_max 8", L(), O(bins=lvn.DeviceBins(thread_max=8))),

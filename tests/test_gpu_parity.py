@@ -227,11 +227,13 @@ def test_aggregate_planted(lvn, port):
 
 
 # ------------------------------------------------------------ move decisions
-def decisions_equal(lvn, port, g, memb, force=-1, value_bits=64, live=False):
+def decisions_equal(lvn, port, g, memb, force=-1, value_bits=64, live=False, probing=None):
     kw = port.vertex_weights(g)
     cw = np.zeros(g.n)
     np.add.at(cw, memb, kw)
     opts = lvn.CompactOptions(value_bits=value_bits)
+    if probing is not None:
+        opts.probing = probing
     to, gain = lvn.evaluate_moves(G_(g, lvn), memb, kw, cw, g.total_weight, opts, force, live)
     for u in range(g.n):
         want = port.evaluate_move(g, memb, kw, cw, g.total_weight, u, value_bits)
@@ -319,6 +321,25 @@ def test_engine_sweep_options(lvn, port, opts):
     assert_q(r.modularity, port.modularity(g, m))
     assert set(np.unique(m)) == set(range(r.num_communities)) and r.passes >= 2
     assert r.modularity >= base - 0.01
+
+
+@pytest.mark.parametrize("probing", ["linear", "quadratic", "double_hash", "quadratic_double"])
+def test_probing_modes_change_speed_not_results(lvn, port, probing):
+    # the reference's four probing recurrences (compact_hashtable.hpp:60-82)
+    # drive every device table: smem tables of the warp / block classes, the
+    # hubs' HBM tables, the giant-community regions of aggregation
+    mode = lvn.Probing[probing]
+    g = hubs_graph(25000, 5, 20000, 60000, 3)
+    memb = random_membership(g.n, 400, 9)
+    for force in (2, 3, 4):
+        decisions_equal(lvn, port, g, memb, force, 32, probing=mode)
+    m = random_membership(g.n, 50, 4)
+    agg_equal(lvn.compact_aggregate(G_(g, lvn), m, options=lvn.CompactOptions(probing=mode)), port.aggregate(g, m))
+    s = star(12000)
+    ms = np.arange(s.n, dtype=np.uint32)
+    agg_equal(lvn.compact_aggregate(G_(s, lvn), ms, options=lvn.CompactOptions(probing=mode)), port.aggregate(s, ms))
+    r = lvn.louvain_compact(G_(g, lvn), None, lvn.CompactOptions(probing=mode))
+    assert_q(r.modularity, port.modularity(g, np.asarray(r.membership, np.uint32)))
 
 
 # ------------------------------------------------------------ engine end to end
