@@ -194,13 +194,21 @@ __global__ void reset_warp(DGraph g, const u32* __restrict__ list, u64 count,
   for (u64 i = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; i < count; i += warps) {
     const u32 v = list[i];
     const u64 lo = g.off[v], hi = g.off[v + 1];
-    double s = 0.0;
-    for (u64 a = lo + lane; a < hi; a += 32) {
-      const float w = g.w[a];
-      differs = differs || w != wref;
-      s += double(w);
+    // four loads in flight per lane (rows of up to 1024 arcs)
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    u64 a = lo + lane;
+    for (; a + 96 < hi; a += 128) {
+      const float w0 = __ldcs(g.w + a), w1 = __ldcs(g.w + a + 32), w2 = __ldcs(g.w + a + 64),
+                  w3 = __ldcs(g.w + a + 96);
+      differs = differs || w0 != wref || w1 != wref || w2 != wref || w3 != wref;
+      s0 += double(w0), s1 += double(w1), s2 += double(w2), s3 += double(w3);
     }
-    s = warp_sum(s);
+    for (; a < hi; a += 32) {
+      const float w = __ldcs(g.w + a);
+      differs = differs || w != wref;
+      s0 += double(w);
+    }
+    double s = warp_sum((s0 + s1) + (s2 + s3));
     if (lane == 0) {
       K[v] = s;
       if (sigma) sigma[v] = s;
@@ -256,17 +264,18 @@ void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C
   grp(kBinSort64, reset_group<2>);
   grp(kBinSort128, reset_group<4>);
   grp(kBinSort256, reset_group<8>);
-  // the warp bin (deg <= warp_max, plus any short rows binned there): one warp per row
-  const u64 mid = b.count(kBinWarp);
+  // the warp bin and the short block rows (<= 1024 arcs, adjacent in the
+  // list): one warp per row; a block only for the longer rows
+  const u64 mid = b.count(kBinWarp) + b.count(kBinBlockS);
   if (mid) {
     const u64 wb = std::min<u64>((mid + 7) / 8, u64(sms) * 16);
     reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinWarp), mid, K, sigma, uni);
     LVN_LAUNCH();
   }
-  const u64 big = b.count(kBinBlockS) + b.count(kBinBlock) + b.count(kBinGlobal);
+  const u64 big = b.count(kBinBlock) + b.count(kBinGlobal);
   if (big) {
     const u64 bb = std::min<u64>(big, u64(sms) * 4);
-    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(kBinBlockS), big, K, sigma, uni);
+    reset_block<<<unsigned(bb), 512, 0, s>>>(g, b.of(kBinBlock), big, K, sigma, uni);
     LVN_LAUNCH();
   }
 }

@@ -411,10 +411,12 @@ def test_engine_quality_vs_reference_planted(lvn, t):
 def test_engine_quality_rmat16_c1(lvn, port, ref, value_bits):
     # config C1: RMAT scale 16, edge factor 16, dedupe, default parameters, against
     # the reference engines run on all host cores (5-run means, like the CPU
-    # baseline). The engine re-implements louvain_compact (ν-Louvain), so that is
-    # the tight gate; louvain_mc (GVE-Louvain) sweeps in vertex-id order and finds
-    # ~0.004 more on this skewed graph (the reference's own louvain_compact shows
-    # the same gap, "quality"), gated at 0.006.
+    # baseline). The engine re-implements louvain_compact (ν-Louvain), the entry
+    # point it replaces, so that is the two-sided 0.005 gate; louvain_mc
+    # (GVE-Louvain) sweeps in vertex-id order and finds ~0.005 more on this
+    # skewed graph (the reference's own louvain_compact shows the same gap, and
+    # the paper reports ν-Louvain below GVE-Louvain; DESIGN.md,
+    # "quality"), so against it the gate is one-sided at 0.006.
     g = rmat(16, 16, 1)
     compact = float(np.mean([ref.louvain(g, "compact").modularity for _ in range(5)]))
     mc = float(np.mean([ref.louvain(g, "mc").modularity for _ in range(5)]))
@@ -423,7 +425,7 @@ def test_engine_quality_rmat16_c1(lvn, port, ref, value_bits):
     for r in runs:
         assert_q(r.modularity, port.modularity(g, r.membership))
     q = float(np.mean([r.modularity for r in runs]))
-    assert q >= compact - Q_TOL, (q, compact)
+    assert abs(q - compact) <= Q_TOL, (q, compact)
     assert q >= mc - 0.006, (q, mc)
 
 
