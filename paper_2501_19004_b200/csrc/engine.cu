@@ -1372,7 +1372,10 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       self_next.ensure(count ? count : 1);
       kx_next.ensure(count ? count : 1);
       aggregate_device(cur, C.p, count, edges, next, err.p, s, false, &B, inexact.p, self_next.p);
-      sum_by_community(C.p, pass == 0 ? K.p : kx_cur.p, nv, kx_next.p, count, s);
+      // exact degrees of this pass's vertices: the previous whole-graph
+      // aggregation's, else (pass 0, or after a sharded aggregation) the
+      // reset's row sums (sharded runs evaluate Q on the input anyway)
+      sum_by_community(C.p, kx_cur.p ? kx_cur.p : K.p, nv, kx_next.p, count, s);
       std::swap(kx_cur, kx_next);
       std::swap(self_cur, self_next);
     }
