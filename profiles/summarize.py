@@ -2,7 +2,7 @@
 summaries: profiles/<round>_<cfg>.md and the roofline.traffic figure that
 bench.py reads from profiles/traffic.json.
 
-    python profiles/summarize.py r01 c2
+    python profiles/summarize.py r02 c5
 """
 import collections
 import csv
@@ -67,8 +67,11 @@ def full_capture(rep):
             "sm__throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
             "launch__registers_per_thread", "smsp__inst_executed.sum", "launch__grid_size"]
     try:
-        raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
-                             check=True).stdout
+        if rep.endswith(".csv"):
+            raw = open(rep).read()
+        else:
+            raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True,
+                                 check=True).stdout
     except Exception as e:  # noqa: BLE001
         return f"(ncu import failed: {e})"
     rows = list(csv.reader(raw.splitlines()))
@@ -119,8 +122,8 @@ def main():
           f"{move:.2f} ms = {100 * move / total:.1f}%)", "", table, "",
           f"## Local-moving DRAM traffic over one run: {n} launches, read {rd / 1e9:.3f} GB, "
           f"write {wr / 1e9:.3f} GB, {t:.2f} ms", "",
-          "## Full capture of the sort-bin kernels (first iteration of pass 0)", "",
-          full_capture(os.path.join(OUT, f"prof_lm_sort_{cfg}.ncu-rep")), ""]
+          "## Full capture of the dominant sort-bin kernel (pass 0, second sweep)", "",
+          full_capture(os.path.join(OUT, f"prof_lm_sort_{cfg}.raw.csv")), ""]
     path = os.path.join(ROOT, "profiles", f"{rnd}_{cfg}.md")
     open(path, "w").write("\n".join(md))
     print(path)
