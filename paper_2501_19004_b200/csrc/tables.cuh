@@ -50,11 +50,24 @@ struct PackedF32 {  // value_bits == 32: one 64-bit slot (key << 32 | float bits
   ull* s;
   __device__ PackedF32(void* base, u64 slots) : s(static_cast<ull*>(base)) { (void)slots; }
   __device__ __forceinline__ void clear(u32 i) const { s[i] = kEmptySlot64; }
+  // first probe inline; a collision continues out of line (keeps the probe
+  // state out of the callers' registers)
   __device__ __forceinline__ int insert(u32 log_size, u32 key, float w) const {
+    const u32 h = slot_hash(key, log_size);
+    const ull cur = reinterpret_cast<volatile ull*>(s)[h];
+    const u32 k = u32(cur >> 32);
+    if (k == key || k == kEmpty) {
+      const ull want = (ull(key) << 32) | __float_as_uint(__uint_as_float(u32(cur)) + w);
+      if (atomicCAS(&s[h], cur, want) == cur) return k == kEmpty ? int(h) : -1;
+      return insert_from(log_size, key, w, h, 0u);  // lost a race: retry the same slot
+    }
+    return insert_from(log_size, key, w, h, 1u);
+  }
+  __device__ __noinline__ int insert_from(u32 log_size, u32 key, float w, u32 h, u32 advance) const {
     const u32 mask = (1u << log_size) - 1u;
-    u32 h = slot_hash(key, log_size);
     u32 attempt = 0, stride = 1;
     const u32 kmod = c_probing ? probe_kmod(key, log_size) : 0u;
+    if (advance) h = probe_next(h, mask, attempt++, stride, kmod);
     while (true) {
       const ull cur = reinterpret_cast<volatile ull*>(s)[h];
       const u32 k = u32(cur >> 32);
@@ -88,10 +101,24 @@ struct SplitF64 {  // value_bits == 64: u32 key array + fp64 value array
     v[i] = 0.0;
   }
   __device__ __forceinline__ int insert(u32 log_size, u32 key, double w) const {
+    const u32 h = slot_hash(key, log_size);
+    u32 cur = reinterpret_cast<volatile u32*>(k)[h];
+    int claimed = -1;
+    if (cur == kEmpty) {
+      cur = atomicCAS(&k[h], kEmpty, key);
+      if (cur == kEmpty) cur = key, claimed = int(h);
+    }
+    if (cur == key) {
+      atomicAdd(&v[h], w);
+      return claimed;
+    }
+    return insert_from(log_size, key, w, h);
+  }
+  __device__ __noinline__ int insert_from(u32 log_size, u32 key, double w, u32 h) const {
     const u32 mask = (1u << log_size) - 1u;
-    u32 h = slot_hash(key, log_size);
     u32 attempt = 0, stride = 1;
     const u32 kmod = c_probing ? probe_kmod(key, log_size) : 0u;
+    h = probe_next(h, mask, attempt++, stride, kmod);
     while (true) {
       u32 cur = reinterpret_cast<volatile u32*>(k)[h];
       int claimed = -1;
