@@ -4,6 +4,7 @@
 // C-ABI entry point declared in include/lvn.h.
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -695,6 +696,15 @@ bool verbose() {
   return on;
 }
 
+// LVN_AGG_SORT=0: never aggregate by external arcs (A/B aid)
+bool agg_sort_off() {
+  static const bool off = [] {
+    const char* e = std::getenv("LVN_AGG_SORT");
+    return e && e[0] == '0';
+  }();
+  return off;
+}
+
 // ---- aggregation of a graph by a contiguous membership ----------------------
 void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
                       u32* err, cudaStream_t s, bool canonical, const Bins* gbins = nullptr,
@@ -703,6 +713,21 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   DBuf<u64> budget(count + 1), coff(count + 1), boff(count + 1), hoff(count + 1), capped(count + 1),
       ext(count + 1);
   community_counts(g, C, count, msize.p, budget.p, s);
+  // Uniform integer weights with few arcs between communities (a clustered
+  // unweighted graph's first aggregation): aggregate by the external arcs
+  // alone (aggsort.cu); the sample decides (<= 15 %: 17 vs 20 ms on the C2
+  // graph under its planted blocks; at C5's 27 % the sort of 1 G keys loses,
+  // 168-175 vs 156 ms, profiles/agg_ab.py), an overflow falls back here with
+  // the external-arc counts already made
+  bool ext_ready = false;
+  if (gbins && g.uniform && g.uw == std::floor(g.uw) && g.uw > 0.f && g.arcs >= (u64(1) << 20) && !agg_sort_off() &&
+      external_arcs_few(g, C, 0.15, s)) {
+    // key buffer: 45 % of the arcs, bounded by the memory the sort needs (~28 B per key)
+    const u64 cap = std::min<u64>(g.arcs * 45 / 100 + 4096, ctx().pool.available() / 32);
+    if (aggregate_by_external_arcs(g, *gbins, C, count, budget.p, ext.p, cap, out, inexact, self64, s))
+      return;
+    ext_ready = true;
+  }
   exclusive_scan_u32_to_u64(msize.p, coff.p, count, s);
   exclusive_scan_u64(budget.p, boff.p, count, s);
   // Holey row capacity: a super-row's distinct targets are at most its
@@ -711,9 +736,9 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   // (C5's first aggregation: ~30 GB), the capacity is tightened to
   // min(ext + 1, count), ext = the community's arcs to other communities
   // (one row pass over the graph, binned like the modularity pass).
-  cap_budgets(budget.p, capped.p, count, s, false);
+  cap_budgets(ext_ready ? ext.p : budget.p, capped.p, count, s, ext_ready);
   exclusive_scan_u64(capped.p, hoff.p, count, s);
-  if (read_scalar(hoff.p + count, s) * 8 > ctx().pool.available() / 8) {
+  if (!ext_ready && read_scalar(hoff.p + count, s) * 8 > ctx().pool.available() / 8) {
     Bins local;
     const Bins* gb = gbins;
     if (!gb) {
@@ -1921,8 +1946,19 @@ int lvn_aggregate(const lvn_csr* g, const uint32_t* membership, int membership_l
     }
     DBuf<u32> err(1);
     LVN_CUDA(cudaMemsetAsync(err.p, 0, sizeof(u32), s));
+    // the engine's pass view of the graph: degree bins and the uniform-weight
+    // test of the pass reset, so this API takes the aggregation path a pass
+    // of the engine would (by external arcs for clustered unit-weight graphs)
+    Bins gb;
+    compute_bins(ig.g.off, ig.g.n, edges_of(pp), gb, s);
+    if (ig.g.arcs && !no_uniform()) {
+      DBuf<double> k2(ig.g.n ? ig.g.n : 1);
+      DBuf<u32> uni(1);
+      pass_reset(ig.g, gb, k2.p, nullptr, nullptr, nullptr, s, uni.p);
+      if (read_scalar(uni.p, s) != 0) ig.g.uniform = 1, ig.g.uw = read_scalar(ig.g.w, s);
+    }
     OwnedCsr o;
-    aggregate_device(ig.g, m.p, count, edges_of(pp), o, err.p, s, canonical != 0);
+    aggregate_device(ig.g, m.p, count, edges_of(pp), o, err.p, s, canonical != 0, &gb);
     check_err(err.p, s);
     res = new lvn_graph_out;
     res->num_vertices = o.n;

@@ -235,4 +235,14 @@ void build_csr_device(u32 n, u64 T, const u32* src, const u32* dst, const double
 // sorted arc keys (source<<32 | target, ~0 = dropped) -> deduplicated unit-weight CSR
 void keys_to_csr(DBuf<ull>& keys, u64 nkeys, u64 n, OwnedCsr& out, cudaStream_t s);
 
+// ---- aggsort.cu: aggregation of a uniform integer-weight pass by external arcs
+// true when a sample of the arcs finds at most max_frac of them between communities
+bool external_arcs_few(const DGraph& g, const u32* C, double max_frac, cudaStream_t s);
+// the super-graph of g under C (count communities, budget = member arcs per
+// community) from the external arcs (ext receives their count per community;
+// cap = key buffer entries); false when more than cap arcs are external (out
+// untouched, ext complete). Rows come out sorted by target.
+bool aggregate_by_external_arcs(const DGraph& g, const Bins& b, const u32* C, u32 count, const u64* budget,
+                                u64* ext, u64 cap, OwnedCsr& out, u32* inexact, double* self64, cudaStream_t s);
+
 }  // namespace lvn
