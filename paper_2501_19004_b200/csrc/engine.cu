@@ -909,10 +909,11 @@ void aggregate_sharded(const DGraph& g, const u32* C, u32 count, u32 v0, u32 v1,
   const int P = cm.size(), me = cm.rank();
   DBuf<ull> keys;
   DBuf<double> vals;
-  const u64 m = partial_super_edges(g, C, v0, v1, keys, vals, s);
+  const u32 kb = key_bits(count);
+  const u64 m = partial_super_edges(g, C, v0, v1, kb, keys, vals, s);
   // super-edges per row over all ranks (upper bound of the merged row) -> row ranges
   DBuf<u32> cnt(count ? count : 1);
-  super_row_counts(keys.p, m, count, cnt.p, s);
+  super_row_counts(keys.p, m, count, kb, cnt.p, s);
   cm.allreduce(cnt.p, count, LVN_U32, LVN_SUM, s);
   DBuf<u64> coff(u64(count) + 1);
   exclusive_scan_u32_to_u64(cnt.p, coff.p, count, s);
@@ -922,10 +923,9 @@ void aggregate_sharded(const DGraph& g, const u32* C, u32 count, u32 v0, u32 v1,
   DBuf<u64> cut(P + 1), mat(u64(P) * P);
   std::memcpy(ctx().pinned, cb.data(), (P + 1) * sizeof(u32));
   LVN_CUDA(cudaMemcpyAsync(dcb.p, ctx().pinned, (P + 1) * sizeof(u32), cudaMemcpyHostToDevice, s));
-  route_entries(keys.p, m, dcb.p, P, cut.p, s);
+  route_entries(keys.p, m, dcb.p, P, kb, cut.p, s);
   // entries this rank sends to each rank, then the whole P x P matrix
   {
-    DBuf<u64> row(P);
     std::vector<u64> h(P + 1);
     LVN_CUDA(cudaMemcpyAsync(ctx().pinned, cut.p, (P + 1) * sizeof(u64), cudaMemcpyDeviceToHost, s));
     LVN_CUDA(cudaStreamSynchronize(s));
@@ -952,7 +952,7 @@ void aggregate_sharded(const DGraph& g, const u32* C, u32 count, u32 v0, u32 v1,
   keys.release();
   vals.release();
   DBuf<double> tw(1);
-  merge_super_rows(rkeys, rvals, total, count, out, tw.p, s);
+  merge_super_rows(rkeys, rvals, total, count, kb, out, tw.p, s);
   cm.allreduce(tw.p, 1, LVN_F64, LVN_SUM, s);
   out.total_weight = read_scalar(tw.p, s) / 2.0;
 }

@@ -8,7 +8,8 @@
 // Aggregation by own rows (the reference's per-community merge,
 // louvain_compact.cpp:214-310, distributed):
 //   1. partial_super_edges: every own arc (u, v, w) becomes the entry
-//      (C[u] << 32 | C[v], w as f64); entries are radix-sorted by key and
+//      (C[u] << kb | C[v], w as f64; kb = ceil(log2(count + 1)), so the radix
+//      sort covers 2 kb bits, not 64); entries are radix-sorted by key and
 //      summed per key in fp64 -> this rank's partial super-edges, sorted.
 //   2. the host routes the sorted entries to the owner of their row
 //      (community ranges [cb[k], cb[k+1])) with one all-to-all (NCCL).
@@ -40,7 +41,7 @@ __global__ void local_offsets_k(const u64* __restrict__ off, u32 n, u32 v0, u32 
   }
 }
 
-__global__ void entries_k(DGraph g, const u32* __restrict__ C, u32 v0, u32 v1, ull* __restrict__ keys,
+__global__ void entries_k(DGraph g, const u32* __restrict__ C, u32 v0, u32 v1, u32 kb, ull* __restrict__ keys,
                           double* __restrict__ vals) {
   // one thread per own arc; the row of arc a found by a binary search over the own offsets
   const u64 base = g.off[v0];
@@ -51,16 +52,16 @@ __global__ void entries_k(DGraph g, const u32* __restrict__ C, u32 v0, u32 v1, u
       const u32 mid = lo + (hi - lo) / 2;
       if (g.off[mid] <= base + a) lo = mid; else hi = mid;
     }
-    keys[a] = (ull(C[lo]) << 32) | C[g.tgt[base + a]];
-    vals[a] = double(g.w[base + a]);
+    keys[a] = (ull(C[lo]) << kb) | C[g.tgt[base + a]];
+    vals[a] = double(arc_w(g, base + a));
   }
 }
 
 // first index of a sorted key array whose row (key >> 32) reaches each bound
-__global__ void route_k(const ull* __restrict__ keys, u64 n, const u32* __restrict__ cb, int parts,
+__global__ void route_k(const ull* __restrict__ keys, u64 n, const u32* __restrict__ cb, int parts, u32 kb,
                         u64* __restrict__ cut) {
   for (int k = threadIdx.x; k <= parts; k += blockDim.x) {
-    const ull target = ull(cb[k]) << 32;
+    const ull target = ull(cb[k]) << kb;
     u64 lo = 0, hi = n;
     while (lo < hi) {
       const u64 mid = lo + (hi - lo) / 2;
@@ -70,16 +71,17 @@ __global__ void route_k(const ull* __restrict__ keys, u64 n, const u32* __restri
   }
 }
 
-__global__ void row_counts_k(const ull* __restrict__ keys, u64 n, u32* __restrict__ cnt) {
+__global__ void row_counts_k(const ull* __restrict__ keys, u64 n, u32 kb, u32* __restrict__ cnt) {
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x)
-    atomicAdd(&cnt[u32(keys[i] >> 32)], 1u);
+    atomicAdd(&cnt[u32(keys[i] >> kb)], 1u);
 }
 
-__global__ void emit_k(const ull* __restrict__ keys, const double* __restrict__ vals, u64 n,
+__global__ void emit_k(const ull* __restrict__ keys, const double* __restrict__ vals, u64 n, u32 kb,
                        u32* __restrict__ tgt, float* __restrict__ w, double* __restrict__ tw) {
   double acc = 0.0;
+  const ull mask = (ull(1) << kb) - 1;
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n; i += u64(gridDim.x) * blockDim.x) {
-    tgt[i] = u32(keys[i]);
+    tgt[i] = u32(keys[i] & mask);
     const float f = float(vals[i]);
     w[i] = f;
     acc += double(f);
@@ -90,18 +92,18 @@ __global__ void emit_k(const ull* __restrict__ keys, const double* __restrict__ 
 
 // sort (keys, vals) by key (stable) and sum equal keys in fp64 in that order;
 // returns the number of distinct keys, left at the front of keys / vals
-u64 sort_reduce(DBuf<ull>& keys, DBuf<double>& vals, u64 n, cudaStream_t s) {
+u64 sort_reduce(DBuf<ull>& keys, DBuf<double>& vals, u64 n, int bits, cudaStream_t s) {
   if (!n) return 0;
   DBuf<ull> k2(n);
   DBuf<double> v2(n);
   size_t bytes = 0;
-  LVN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, k2.p, vals.p, v2.p, n, 0, 64, s));
+  LVN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, keys.p, k2.p, vals.p, v2.p, n, 0, bits, s));
   size_t rbytes = 0;
   DBuf<u64> nout(1);
   LVN_CUDA(cub::DeviceReduce::ReduceByKey(nullptr, rbytes, k2.p, keys.p, v2.p, vals.p, nout.p, cuda::std::plus<>{},
                                           n, s));
   DBuf<unsigned char> tmp(std::max(bytes, rbytes));
-  LVN_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, k2.p, vals.p, v2.p, n, 0, 64, s));
+  LVN_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, keys.p, k2.p, vals.p, v2.p, n, 0, bits, s));
   LVN_CUDA(cub::DeviceReduce::ReduceByKey(tmp.p, rbytes, k2.p, keys.p, v2.p, vals.p, nout.p, cuda::std::plus<>{}, n,
                                           s));
   g_launches += 4;
@@ -117,43 +119,45 @@ void shard_offsets(const u64* off, u32 n, u32 v0, u32 v1, u64* out, cudaStream_t
   LVN_LAUNCH();
 }
 
-u64 partial_super_edges(const DGraph& g, const u32* C, u32 v0, u32 v1, DBuf<ull>& keys, DBuf<double>& vals,
+u32 key_bits(u32 count) { return std::max(1u, ceil_log2_u64(u64(count) + 1)); }
+
+u64 partial_super_edges(const DGraph& g, const u32* C, u32 v0, u32 v1, u32 kb, DBuf<ull>& keys, DBuf<double>& vals,
                         cudaStream_t s) {
   const u64 A = g.arcs;  // own arcs only: the other rows are empty
   keys.ensure(A ? A : 1);
   vals.ensure(A ? A : 1);
   if (!A || v1 <= v0) return 0;
-  entries_k<<<grid_for(A, 256, 16), 256, 0, s>>>(g, C, v0, v1, keys.p, vals.p);
+  entries_k<<<grid_for(A, 256, 16), 256, 0, s>>>(g, C, v0, v1, kb, keys.p, vals.p);
   LVN_LAUNCH();
-  return sort_reduce(keys, vals, A, s);
+  return sort_reduce(keys, vals, A, int(2 * kb), s);
 }
 
-void super_row_counts(const ull* keys, u64 n, u32 count, u32* cnt, cudaStream_t s) {
+void super_row_counts(const ull* keys, u64 n, u32 count, u32 kb, u32* cnt, cudaStream_t s) {
   LVN_CUDA(cudaMemsetAsync(cnt, 0, size_t(count ? count : 1) * sizeof(u32), s));
   if (!n) return;
-  row_counts_k<<<grid_for(n, 256, 16), 256, 0, s>>>(keys, n, cnt);
+  row_counts_k<<<grid_for(n, 256, 16), 256, 0, s>>>(keys, n, kb, cnt);
   LVN_LAUNCH();
 }
 
-void route_entries(const ull* keys, u64 n, const u32* cb, int parts, u64* cut, cudaStream_t s) {
-  route_k<<<1, 256, 0, s>>>(keys, n, cb, parts, cut);
+void route_entries(const ull* keys, u64 n, const u32* cb, int parts, u32 kb, u64* cut, cudaStream_t s) {
+  route_k<<<1, 256, 0, s>>>(keys, n, cb, parts, kb, cut);
   LVN_LAUNCH();
 }
 
-void merge_super_rows(DBuf<ull>& keys, DBuf<double>& vals, u64 n, u32 count, OwnedCsr& out, double* tw,
+void merge_super_rows(DBuf<ull>& keys, DBuf<double>& vals, u64 n, u32 count, u32 kb, OwnedCsr& out, double* tw,
                       cudaStream_t s) {
-  const u64 m = sort_reduce(keys, vals, n, s);
+  const u64 m = sort_reduce(keys, vals, n, int(2 * kb), s);
   out.n = count;
   out.arcs = m;
   out.off.alloc(u64(count) + 1);
   DBuf<u32> cnt(count ? count : 1);
-  super_row_counts(keys.p, m, count, cnt.p, s);
+  super_row_counts(keys.p, m, count, kb, cnt.p, s);
   exclusive_scan_u32_to_u64(cnt.p, out.off.p, count, s);
   out.tgt.alloc(m ? m : 1);
   out.w.alloc(m ? m : 1);
   LVN_CUDA(cudaMemsetAsync(tw, 0, sizeof(double), s));
   if (m) {
-    emit_k<<<grid_for(m, 256, 16), 256, 0, s>>>(keys.p, vals.p, m, out.tgt.p, out.w.p, tw);
+    emit_k<<<grid_for(m, 256, 16), 256, 0, s>>>(keys.p, vals.p, m, kb, out.tgt.p, out.w.p, tw);
     LVN_LAUNCH();
   }
 }
