@@ -72,6 +72,12 @@ class ClockSampler:
                  "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.t = threading.Thread(target=self._read, daemon=True)
             self.t.start()
+            # nvidia-smi's start-up (driver / NVML initialisation) stalls CUDA
+            # API calls of other processes for milliseconds: let it finish
+            # before the timed region (it keeps sampling during the region)
+            t0 = time.time()
+            while not self.lines and time.time() - t0 < 5.0:
+                time.sleep(0.01)
         except OSError:
             self.proc = None
         return self
