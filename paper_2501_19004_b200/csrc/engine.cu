@@ -612,7 +612,8 @@ struct Comm {
   NcclComm* nc = nullptr;  // library-owned NCCL communicator: stream-ordered, no host sync
   double seconds = 0.0;    // host time inside caller collectives / device time of NCCL ones
   std::vector<cudaEvent_t> ev;  // NCCL: (begin, end) event pairs, summed at the end of the run
-  bool on() const { return c && c->size > 1; }
+  bool force = false;       // LVN_SHARD_SINGLE: the sharded path at world size 1
+  bool on() const { return c && (c->size > 1 || force); }
   int rank() const { return c ? c->rank : 0; }
   int size() const { return c ? c->size : 1; }
   void mark(cudaStream_t s) {
@@ -1746,6 +1747,10 @@ int lvn_louvain_sharded(const lvn_csr* g, const lvn_params* p, const lvn_comm* c
   std::memset(r, 0, sizeof(*r));
   lvn::Comm cm;
   cm.c = comm;
+  cm.nc = nccl_of(comm);  // the library's NCCL communicator: stream-ordered collectives
+  // LVN_SHARD_SINGLE=1 (tests): a one-rank communicator still runs the
+  // sharded algorithm, so every collective of the path runs at world size 1
+  if (const char* e = std::getenv("LVN_SHARD_SINGLE")) cm.force = e[0] == '1';
   const int rc = guard([&](Context&) { run_louvain(g, p ? *p : def, r, &cm); });
   if (rc) {
     lvn_result_free(r);

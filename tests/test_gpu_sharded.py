@@ -154,25 +154,38 @@ def _nccl_worker(port, q):
         g = make("planted")
         G = lvn.CsrGraph(g.offsets, g.targets, g.weights, g.total_weight)
         r = lvn.louvain_sharded(G, comm)
+        # the sharded algorithm itself over the library's NCCL collectives
+        # (stream-ordered allgatherv / alltoallv / allreduce at world size 1):
+        # every pass sharded, then collapsed onto rank 0 below 2^16 arcs
+        os.environ["LVN_SHARD_SINGLE"] = "1"
+        r2 = lvn.louvain_sharded(G, comm, options=lvn.CompactOptions(shard_min_arcs_log2=0))
+        r3 = lvn.louvain_sharded(G, comm, options=lvn.CompactOptions(shard_min_arcs_log2=16))
+        del os.environ["LVN_SHARD_SINGLE"]
         comm.close()
-        q.put(("ok", r.modularity, np.asarray(r.membership)))
+        assert r2.sharded_passes >= 2 and r3.sharded_passes == 1, (r2.sharded_passes, r3.sharded_passes)
+        assert r2.exchange_seconds > 0.0
+        q.put(("ok", r.modularity, np.asarray(r.membership), r2.modularity, np.asarray(r2.membership),
+               r3.modularity, np.asarray(r3.membership)))
         dist.destroy_process_group()
     except Exception:  # noqa: BLE001
         import traceback
 
-        q.put((traceback.format_exc(), None, None))
+        q.put((traceback.format_exc(),) + (None,) * 6)
 
 
-def test_nccl_comm_world1(port):
+def test_nccl_comm_world1(port, lvn_single):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     p = ctx.Process(target=_nccl_worker, args=(free_port(), q))
     p.start()
-    st, qq, m = q.get(timeout=300)
+    st, qq, m, q2, m2, q3, m3 = q.get(timeout=300)
     p.join(timeout=60)
     assert st == "ok", st
     g = make("planted")
-    assert abs(qq - port.modularity(g, m)) <= 1e-9
+    single = lvn_single(g)
+    for qx, mx in ((qq, m), (q2, m2), (q3, m3)):
+        assert abs(qx - port.modularity(g, mx)) <= 1e-9
+        assert qx >= single - 0.01
 
 
 @pytest.fixture(scope="module")
