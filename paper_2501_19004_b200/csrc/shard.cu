@@ -23,6 +23,8 @@
 #include <cub/device/device_reduce.cuh>
 #include <cuda/std/functional>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 #include "shard.hpp"
 
@@ -41,19 +43,19 @@ __global__ void local_offsets_k(const u64* __restrict__ off, u32 n, u32 v0, u32 
   }
 }
 
-__global__ void entries_k(DGraph g, const u32* __restrict__ C, u32 v0, u32 v1, u32 kb, ull* __restrict__ keys,
-                          double* __restrict__ vals) {
-  // one thread per own arc; the row of arc a found by a binary search over the own offsets
+__global__ void entries_k(DGraph g, const u32* __restrict__ C, u32 v0, u32 v1, u32 kb, u64 e0, u64 e1,
+                          ull* __restrict__ keys, double* __restrict__ vals) {
+  // one thread per own arc of [e0, e1) (own-arc index); its row by a binary
+  // search over the own offsets
   const u64 base = g.off[v0];
-  const u64 A = g.off[v1] - base;
-  for (u64 a = blockIdx.x * u64(blockDim.x) + threadIdx.x; a < A; a += u64(gridDim.x) * blockDim.x) {
+  for (u64 a = e0 + blockIdx.x * u64(blockDim.x) + threadIdx.x; a < e1; a += u64(gridDim.x) * blockDim.x) {
     u32 lo = v0, hi = v1;  // last row u with off[u] <= base + a
     while (hi - lo > 1) {
       const u32 mid = lo + (hi - lo) / 2;
       if (g.off[mid] <= base + a) lo = mid; else hi = mid;
     }
-    keys[a] = (ull(C[lo]) << kb) | C[g.tgt[base + a]];
-    vals[a] = double(arc_w(g, base + a));
+    keys[a - e0] = (ull(C[lo]) << kb) | C[g.tgt[base + a]];
+    vals[a - e0] = double(arc_w(g, base + a));
   }
 }
 
@@ -121,15 +123,66 @@ void shard_offsets(const u64* off, u32 n, u32 v0, u32 v1, u64* out, cudaStream_t
 
 u32 key_bits(u32 count) { return std::max(1u, ceil_log2_u64(u64(count) + 1)); }
 
+// Own arcs in slices of at most kSlice entries: each slice sorted and reduced
+// on its own, the reduced slices appended and reduced once more, so the sort
+// buffers scale with a slice, not with the rank's arcs (C5 on 2 ranks: 1.9 G
+// arcs -> 8.6 GB of slice buffers instead of 61 GB)
+u64 slice_arcs() {  // LVN_SHARD_SLICE_LOG2 (tests: exercise the multi-slice merge on small graphs)
+  static const u64 v = [] {
+    const char* e = std::getenv("LVN_SHARD_SLICE_LOG2");
+    const int l = e ? std::atoi(e) : 28;
+    return u64(1) << (l >= 4 && l <= 40 ? l : 28);
+  }();
+  return v;
+}
+
 u64 partial_super_edges(const DGraph& g, const u32* C, u32 v0, u32 v1, u32 kb, DBuf<ull>& keys, DBuf<double>& vals,
                         cudaStream_t s) {
   const u64 A = g.arcs;  // own arcs only: the other rows are empty
-  keys.ensure(A ? A : 1);
-  vals.ensure(A ? A : 1);
-  if (!A || v1 <= v0) return 0;
-  entries_k<<<grid_for(A, 256, 16), 256, 0, s>>>(g, C, v0, v1, kb, keys.p, vals.p);
-  LVN_LAUNCH();
-  return sort_reduce(keys, vals, A, int(2 * kb), s);
+  const u64 kSlice = slice_arcs();
+  if (!A || v1 <= v0) {
+    keys.ensure(1);
+    vals.ensure(1);
+    return 0;
+  }
+  if (A <= kSlice) {
+    keys.ensure(A);
+    vals.ensure(A);
+    entries_k<<<grid_for(A, 256, 16), 256, 0, s>>>(g, C, v0, v1, kb, 0, A, keys.p, vals.p);
+    LVN_LAUNCH();
+    return sort_reduce(keys, vals, A, int(2 * kb), s);
+  }
+  DBuf<ull> acc_k;
+  DBuf<double> acc_v;
+  u64 n = 0;
+  DBuf<ull> sk(kSlice);
+  DBuf<double> sv(kSlice);
+  for (u64 e0 = 0; e0 < A; e0 += kSlice) {
+    const u64 e1 = std::min(A, e0 + kSlice);
+    entries_k<<<grid_for(e1 - e0, 256, 16), 256, 0, s>>>(g, C, v0, v1, kb, e0, e1, sk.p, sv.p);
+    LVN_LAUNCH();
+    const u64 m = sort_reduce(sk, sv, e1 - e0, int(2 * kb), s);
+    if (n + m > acc_k.n) {  // grow the accumulator (keeps what it holds)
+      const u64 cap = std::max<u64>(n + m, 2 * acc_k.n);
+      DBuf<ull> nk(cap);
+      DBuf<double> nv(cap);
+      if (n) {
+        LVN_CUDA(cudaMemcpyAsync(nk.p, acc_k.p, n * sizeof(ull), cudaMemcpyDeviceToDevice, s));
+        LVN_CUDA(cudaMemcpyAsync(nv.p, acc_v.p, n * sizeof(double), cudaMemcpyDeviceToDevice, s));
+      }
+      acc_k = std::move(nk);
+      acc_v = std::move(nv);
+    }
+    LVN_CUDA(cudaMemcpyAsync(acc_k.p + n, sk.p, m * sizeof(ull), cudaMemcpyDeviceToDevice, s));
+    LVN_CUDA(cudaMemcpyAsync(acc_v.p + n, sv.p, m * sizeof(double), cudaMemcpyDeviceToDevice, s));
+    n += m;
+  }
+  sk.release();
+  sv.release();
+  const u64 m = sort_reduce(acc_k, acc_v, n, int(2 * kb), s);
+  keys = std::move(acc_k);
+  vals = std::move(acc_v);
+  return m;
 }
 
 void super_row_counts(const ull* keys, u64 n, u32 count, u32 kb, u32* cnt, cudaStream_t s) {
