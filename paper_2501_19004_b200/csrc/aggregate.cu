@@ -1033,12 +1033,12 @@ void aggregate_rows(const AggArgs& a0, const Bins& b, cudaStream_t s) {
     k<<<unsigned(blocks), T, smem, s>>>(a, b.of(kBinWarp), b.count(kBinWarp));
     LVN_LAUNCH();
   }
-  const u64 nblk = b.count(kBinBlockS) + b.count(kBinBlock);  // adjacent segments
+  const u64 nblk = b.count(kBinBlockT) + b.count(kBinBlockS) + b.count(kBinBlock);  // adjacent segments
   if (nblk) {
     const size_t smem = (size_t(1) << kBlockCapLog) * Tab::kSlotBytes + (kPrefixCap + 1) * sizeof(u32);
     static const int occ = occupancy(ag_block, kBlockThreads, smem);
     const u64 blocks = std::min<u64>(nblk, u64(sms) * occ);
-    ag_block<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(kBinBlockS), nblk);
+    ag_block<<<unsigned(blocks), kBlockThreads, smem, s>>>(a, b.of(kBinBlockT), nblk);
     LVN_LAUNCH();
   }
   const u64 nbig = b.count(kBinGlobal);

@@ -33,7 +33,7 @@ __device__ __forceinline__ int bin_of(u64 deg, const BinEdges& e) {
     return kBinSort256;
   }
   if (deg <= e.warp_max) return kBinWarp;
-  if (deg <= e.block_max) return deg <= kBlockSplitDeg ? kBinBlockS : kBinBlock;
+  if (deg <= e.block_max) return deg <= kBlockSplitDeg / 2 ? kBinBlockT : deg <= kBlockSplitDeg ? kBinBlockS : kBinBlock;
   return kBinGlobal;
 }
 
@@ -266,7 +266,7 @@ void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C
   grp(kBinSort256, reset_group<8>);
   // the warp bin and the short block rows (<= 1024 arcs, adjacent in the
   // list): one warp per row; a block only for the longer rows
-  const u64 mid = b.count(kBinWarp) + b.count(kBinBlockS);
+  const u64 mid = b.count(kBinWarp) + b.count(kBinBlockT) + b.count(kBinBlockS);
   if (mid) {
     const u64 wb = std::min<u64>((mid + 7) / 8, u64(sms) * 16);
     reset_warp<<<unsigned(wb), 256, 0, s>>>(g, b.of(kBinWarp), mid, K, sigma, uni);

@@ -25,13 +25,15 @@ enum : int {
   kBinSort128 = 6,  // deg <= 128: 32 lanes x 4 registers
   kBinSort256 = 7,  // deg <= 256: 32 lanes x 8 registers
   kBinWarp = 8,     // deg <= warp_max: warp, smem hash table
-  kBinBlockS = 9,   // deg <= min(block_max, kBlockSplitDeg): block sub-group, smem hash table
-  kBinBlock = 10,   // deg <= block_max: block, smem hash table
-  kBinGlobal = 11,  // larger: block, global-memory hash table
-  kBins = 12
+  kBinBlockT = 9,   // deg <= min(block_max, kBlockSplitDeg / 2): eight sub-groups per block
+  kBinBlockS = 10,  // deg <= min(block_max, kBlockSplitDeg): four sub-groups per block
+  kBinBlock = 11,   // deg <= block_max: block, smem hash table
+  kBinGlobal = 12,  // larger: block, global-memory hash table
+  kBins = 13
 };
-// rows of the block class up to this degree share a block with three others
-// (own bin, so no kernel walks rows it does not take)
+// rows of the block class up to this degree share a block with three others,
+// up to half of it with seven others (own bins, so no kernel walks rows it
+// does not take)
 constexpr unsigned long long kBlockSplitDeg = 1024;
 struct BinEdges {
   u32 thread_max = 4, group_max = 256, warp_max = 256, block_max = 4096;

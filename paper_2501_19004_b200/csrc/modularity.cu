@@ -241,10 +241,10 @@ void row_pass(const DGraph& g, const Bins& b, const u32* C, double* tot, double*
     mod_warp<X><<<unsigned(blocks), 256, 0, s>>>(g, b.of(kBinWarp), mid, C, tot, sums, ext);
     LVN_LAUNCH();
   }
-  const u64 big = b.count(kBinBlockS) + b.count(kBinBlock) + b.count(kBinGlobal);
+  const u64 big = b.count(kBinBlockT) + b.count(kBinBlockS) + b.count(kBinBlock) + b.count(kBinGlobal);
   if (big) {
     const u64 blocks = std::min<u64>(big, u64(sms) * 4);
-    mod_block<X><<<unsigned(blocks), 512, 0, s>>>(g, b.of(kBinBlockS), big, C, tot, sums, ext);
+    mod_block<X><<<unsigned(blocks), 512, 0, s>>>(g, b.of(kBinBlockT), big, C, tot, sums, ext);
     LVN_LAUNCH();
   }
 }

@@ -1465,23 +1465,29 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         launch_chunks(k, a, b.of(bin), b.count(bin), T, T / 32, u64(sms) * occ, smem, s);
         break;
       }
+      case kBinBlockT:
       case kBinBlockS:
       case kBinBlock: {
-        // rows of <= kBlockSplitDeg arcs: four sub-groups per block (four
-        // vertices in flight); longer rows: the whole block
+        // rows of <= 512 arcs: eight sub-groups of 64 threads per block, <= 1024:
+        // four of 128 (vertices in flight per SM: 16 / 8 instead of 2); longer
+        // rows: the whole block
         constexpr size_t smem = block_stage_smem<Tab>();
+        auto k8 = lm_block<Tab, DRY, 8>;
         auto k4 = lm_block<Tab, DRY, 4>;
         auto k1 = lm_block<Tab, DRY, 1>;
+        static const int occ8 = (set_smem(k8, smem), occupancy(k8, kBlockThreads, smem));
         static const int occ4 = (set_smem(k4, smem), occupancy(k4, kBlockThreads, smem));
         static const int occ1 = (set_smem(k1, smem), occupancy(k1, kBlockThreads, smem));
-        const int per = bin == kBinBlockS ? 4 : 1;
+        const int per = bin == kBinBlockT ? 8 : bin == kBinBlockS ? 4 : 1;
+        const int occ = per == 8 ? occ8 : per == 4 ? occ4 : occ1;
         const u64 chunk = std::min(a.chunk, a.hub_chunk);
         const u32* list = b.of(bin);
         const u64 cnt = b.count(bin);
         for (u64 off = 0; off < cnt; off += chunk) {
           const u64 c = std::min<u64>(chunk, cnt - off);
-          const u64 nb = std::max<u64>(1, std::min<u64>((c + per - 1) / per, u64(sms) * (per == 4 ? occ4 : occ1)));
-          if (per == 4) k4<<<unsigned(nb), kBlockThreads, smem, s>>>(a, list + off, c, 0, kBlockSplit);
+          const u64 nb = std::max<u64>(1, std::min<u64>((c + per - 1) / per, u64(sms) * occ));
+          if (per == 8) k8<<<unsigned(nb), kBlockThreads, smem, s>>>(a, list + off, c, 0, kBlockSplit / 2);
+          else if (per == 4) k4<<<unsigned(nb), kBlockThreads, smem, s>>>(a, list + off, c, 0, kBlockSplit);
           else k1<<<unsigned(nb), kBlockThreads, smem, s>>>(a, list + off, c, 0, ~u64(0));
           LVN_LAUNCH();
         }
