@@ -226,13 +226,22 @@ __global__ void __launch_bounds__(512) reset_block(DGraph g, const u32* __restri
   for (u64 i = blockIdx.x; i < count; i += gridDim.x) {
     const u32 v = list[i];
     const u64 lo = g.off[v], hi = g.off[v + 1];
-    double s = 0.0;
-    for (u64 a = lo + threadIdx.x; a < hi; a += blockDim.x) {
-      const float w = g.w[a];
-      differs = differs || w != wref;
-      s += double(w);
+    // four loads in flight per thread
+    const u64 st = blockDim.x;
+    double s0 = 0.0, s1 = 0.0, s2 = 0.0, s3 = 0.0;
+    u64 a = lo + threadIdx.x;
+    for (; a + 3 * st < hi; a += 4 * st) {
+      const float w0 = __ldcs(g.w + a), w1 = __ldcs(g.w + a + st), w2 = __ldcs(g.w + a + 2 * st),
+                  w3 = __ldcs(g.w + a + 3 * st);
+      differs = differs || w0 != wref || w1 != wref || w2 != wref || w3 != wref;
+      s0 += double(w0), s1 += double(w1), s2 += double(w2), s3 += double(w3);
     }
-    s = warp_sum(s);
+    for (; a < hi; a += st) {
+      const float w = __ldcs(g.w + a);
+      differs = differs || w != wref;
+      s0 += double(w);
+    }
+    double s = warp_sum((s0 + s1) + (s2 + s3));
     if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = s;
     __syncthreads();
     if (threadIdx.x == 0) {
