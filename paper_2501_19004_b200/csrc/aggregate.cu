@@ -53,6 +53,12 @@ __device__ __forceinline__ float narrow(const AggArgs& x, u32 key, u32 c, double
   }
   return f;
 }
+// weight of a super-row entry: narrowed into hw, or (partial rows of a
+// sharded aggregation, hw64 set) kept in fp64 for the owner's merge
+__device__ __forceinline__ void put_w(const AggArgs& x, u64 i, u32 key, u32 c, double v) {
+  if (x.hw64) x.hw64[i] = v;
+  else x.hw[i] = narrow(x, key, c, v);
+}
 
 // Communities with budget <= N = G*K: element e = r*G + lane of the
 // community's member arcs (members in CSR order) is loaded into register r.
@@ -103,7 +109,7 @@ __global__ void __launch_bounds__(256) ag_sort(AggArgs x, const u32* __restrict_
         for (int r = 0; r < K; ++r) {
           if (tail[r] && key[r] != kEmpty) {
             x.htgt[hbase + pos] = key[r];
-            x.hw[hbase + pos] = narrow(x, key[r], c, val[r]);  // fp64 sum narrowed once
+            put_w(x, hbase + pos, key[r], c, val[r]);  // fp64 sum narrowed once
             ++pos;
           }
         }
@@ -215,7 +221,7 @@ __global__ void __launch_bounds__(256) ag_psort(AggArgs x, const u32* __restrict
         for (int r = 0; r < K; ++r) {
           if (tail[r] && ck[r] != kEmpty) {
             x.htgt[hbase + pos] = ck[r];
-            x.hw[hbase + pos] = narrow(x, ck[r], c, val[r]);  // fp64 sum narrowed once
+            put_w(x, hbase + pos, ck[r], c, val[r]);  // fp64 sum narrowed once
             ++pos;
           }
         }
@@ -281,14 +287,14 @@ __global__ void __launch_bounds__(THREADS) ag_group(AggArgs x, const u32* __rest
       if (live) {
         const u64 o = hbase + pos + __popc(bal & ((1u << lane) - 1u));
         x.htgt[o] = key;
-        x.hw[o] = narrow(x, key, c, val);
+        put_w(x, o, key, c, val);
       }
       pos += __popc(bal);
     }
     if (lane == 0) {
       if (own_seen) {
         x.htgt[hbase + pos] = c;
-        x.hw[hbase + pos] = narrow(x, c, c, own);
+        put_w(x, hbase + pos, c, c, own);
         ++pos;
       }
       if (pos > hcap) atomicOr(x.err, u32(kErrTable));
@@ -417,7 +423,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
     if (tab.read(s, key, val)) {
       const u32 o = atomicAdd(cursor, 1u);
       x.htgt[hbase + o] = key;
-      x.hw[hbase + o] = narrow(x, key, c, val);
+      put_w(x, hbase + o, key, c, val);
     }
   }
   __syncthreads();
@@ -428,7 +434,7 @@ __device__ void ag_block_one(const AggArgs& x, const Tab& tab, u32* pre, u32 c, 
     u64 pos = *cursor;
     if (seen) {
       x.htgt[hbase + pos] = c;
-      x.hw[hbase + pos] = narrow(x, c, c, t);
+      put_w(x, hbase + pos, c, c, t);
       ++pos;
     }
     if (pos > hcap) atomicOr(x.err, u32(kErrTable));
@@ -804,7 +810,7 @@ __global__ void __launch_bounds__(256) ag_dense_scan(AggArgs x, BigState st, con
         const u32 o = wbase + __popc(bal & ((1u << lane) - 1u));
         if (o < hcap) {
           x.htgt[hbase + o] = u32(j);
-          x.hw[hbase + o] = narrow(x, u32(j), c, __longlong_as_double((long long)bits));  // fp64 sum narrowed once
+          put_w(x, hbase + o, u32(j), c, __longlong_as_double((long long)bits));  // fp64 sum narrowed once
         }
       }
     }
@@ -828,7 +834,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, BigState
       for (u32 j = threadIdx.x; j < n && j < hcap; j += kBlockThreads) {
         const BigSlot e = t[live[j]];
         x.htgt[hbase + j] = e.key;
-        x.hw[hbase + j] = narrow(x, e.key, c, e.val);  // fp64 sum narrowed once
+        put_w(x, hbase + j, e.key, c, e.val);  // fp64 sum narrowed once
       }
     }
     if (threadIdx.x == 0) {
@@ -837,7 +843,7 @@ __global__ void __launch_bounds__(kBlockThreads) ag_big_emit(AggArgs x, BigState
       } else {
         if (self) {
           x.htgt[hbase + n] = c;
-          x.hw[hbase + n] = narrow(x, c, c, st.own_sum[i]);
+          put_w(x, hbase + n, c, c, st.own_sum[i]);
         }
         x.fill[c] = n + self;
       }

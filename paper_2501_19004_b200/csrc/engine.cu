@@ -706,10 +706,18 @@ bool agg_sort_off() {
   return off;
 }
 
+// holey super-rows with fp64 weights (the partial rows of a sharded aggregation)
+struct PartialRows {
+  DBuf<u64> hoff;
+  DBuf<u32> htgt, fill;
+  DBuf<double> hw64;
+};
+
 // ---- aggregation of a graph by a contiguous membership ----------------------
+// partial != null: the rows stay holey, in fp64 (partial->*), nothing is compacted
 void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& e, OwnedCsr& out,
                       u32* err, cudaStream_t s, bool canonical, const Bins* gbins = nullptr,
-                      u32* inexact = nullptr, double* self64 = nullptr) {
+                      u32* inexact = nullptr, double* self64 = nullptr, PartialRows* partial = nullptr) {
   DBuf<u32> msize(count ? count : 1);
   DBuf<u64> budget(count + 1), coff(count + 1), boff(count + 1), hoff(count + 1), capped(count + 1),
       ext(count + 1);
@@ -762,7 +770,8 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   }
   const u64 H = read_scalar(hoff.p + count, s);
   DBuf<u32> htgt(H ? H : 1), fill(count ? count : 1);
-  DBuf<float> hw(H ? H : 1);
+  DBuf<float> hw(partial ? 0 : (H ? H : 1));
+  DBuf<double> hw64(partial ? (H ? H : 1) : 0);
   // communities whose members have no arcs (bin 0) emit nothing and are never visited
   LVN_CUDA(cudaMemsetAsync(fill.p, 0, size_t(count ? count : 1) * sizeof(u32), s));
   AggArgs a;
@@ -775,6 +784,7 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   a.hoff = hoff.p;
   a.htgt = htgt.p;
   a.hw = hw.p;
+  a.hw64 = partial ? hw64.p : nullptr;
   a.fill = fill.p;
   a.err = err;
   a.inexact = inexact;
@@ -812,6 +822,13 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
                             " (budget " + std::to_string(deg) + ", members " +
                             std::to_string(h_coff[c + 1] - h_coff[c]) + ")");
     }
+  }
+  if (partial) {
+    partial->hoff = std::move(hoff);
+    partial->htgt = std::move(htgt);
+    partial->fill = std::move(fill);
+    partial->hw64 = std::move(hw64);
+    return;
   }
   const u32* rows = fill.p;
   DBuf<u64> noff(count + 1);
@@ -906,12 +923,28 @@ void bcast_from0(Comm& cm, void* buf, u64 bytes, cudaStream_t s) {
 // rank's rows [cb[rank], cb[rank+1]) of the next graph (others empty);
 // cb = the next pass's row ranges, balanced by super-edge count.
 void aggregate_sharded(const DGraph& g, const u32* C, u32 count, u32 v0, u32 v1, Comm& cm, OwnedCsr& out,
-                       std::vector<u32>& cb, cudaStream_t s) {
+                       std::vector<u32>& cb, const BinEdges& edges, u32* err, cudaStream_t s) {
   const int P = cm.size(), me = cm.rank();
   DBuf<ull> keys;
   DBuf<double> vals;
   const u32 kb = key_bits(count);
-  const u64 m = partial_super_edges(g, C, v0, v1, kb, keys, vals, s);
+  // this rank's partial super-rows: the single-GPU hash aggregation over its
+  // own rows (the other rows are empty) with fp64 weights, flattened to
+  // (row << kb | target, w) entries in row order (LVN_SHARD_AGG_SORT=1: by
+  // radix-sorting every own arc instead)
+  u64 m = 0;
+  static const bool by_sort = [] {
+    const char* e = std::getenv("LVN_SHARD_AGG_SORT");
+    return e && e[0] == '1';
+  }();
+  if (by_sort) {
+    m = partial_super_edges(g, C, v0, v1, kb, keys, vals, s);
+  } else {
+    PartialRows pr;
+    OwnedCsr unused;
+    aggregate_device(g, C, count, edges, unused, err, s, false, nullptr, nullptr, nullptr, &pr);
+    m = holey_entries(pr.hoff.p, pr.htgt.p, pr.hw64.p, pr.fill.p, count, kb, keys, vals, s);
+  }
   // super-edges per row over all ranks (upper bound of the merged row) -> row ranges
   DBuf<u32> cnt(count ? count : 1);
   super_row_counts(keys.p, m, count, kb, cnt.p, s);
@@ -1392,7 +1425,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     sp = tm.begin(LVN_STAT_AGGREGATE, s);
     if (shard) {
       std::vector<u32> cb;
-      aggregate_sharded(cur, C.p, count, v0, v1, cm, next, cb, s);
+      aggregate_sharded(cur, C.p, count, v0, v1, cm, next, cb, edges, err.p, s);
       v0 = cb[cm.rank()], v1 = cb[cm.rank() + 1];
     } else {
       self_next.ensure(count ? count : 1);

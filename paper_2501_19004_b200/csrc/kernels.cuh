@@ -179,6 +179,7 @@ struct AggArgs {
   const u64* hoff = nullptr;     // holey row offsets (scanned min(budget, count))
   u32* htgt = nullptr;           // holey targets / weights
   float* hw = nullptr;
+  double* hw64 = nullptr;        // sharded partial rows: fp64 weights instead of hw
   u32* fill = nullptr;           // entries written per row
   u32* err = nullptr;
   u32* inexact = nullptr;        // set when narrowing a non-self entry to f32 loses bits (may be null)

@@ -226,6 +226,38 @@ void row_lengths(const u64* off, u32 n, u32* len, cudaStream_t s) {
   LVN_LAUNCH();
 }
 
+__global__ void holey_entries_k(const u64* __restrict__ hoff, const u32* __restrict__ htgt,
+                                const double* __restrict__ hw64, const u32* __restrict__ fill,
+                                const u64* __restrict__ eoff, u32 count, u32 kb, ull* __restrict__ keys,
+                                double* __restrict__ vals) {
+  const u32 lane = threadIdx.x & 31;
+  const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
+  for (u64 c = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; c < count; c += warps) {
+    const u64 src = hoff[c], dst = eoff[c];
+    for (u32 j = lane; j < fill[c]; j += 32) {
+      keys[dst + j] = (ull(c) << kb) | htgt[src + j];
+      vals[dst + j] = hw64[src + j];
+    }
+  }
+}
+
+u64 holey_entries(const u64* hoff, const u32* htgt, const double* hw64, const u32* fill, u32 count, u32 kb,
+                  DBuf<ull>& keys, DBuf<double>& vals, cudaStream_t s) {
+  DBuf<u64> eoff(u64(count) + 1);
+  exclusive_scan_u32_to_u64(fill, eoff.p, count, s);
+  u64 n = 0;
+  LVN_CUDA(cudaMemcpyAsync(&n, eoff.p + count, sizeof(u64), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  keys.ensure(n ? n : 1);
+  vals.ensure(n ? n : 1);
+  if (count) {
+    holey_entries_k<<<grid_for(u64(count) * 32, 256, 8), 256, 0, s>>>(hoff, htgt, hw64, fill, eoff.p, count, kb,
+                                                                       keys.p, vals.p);
+    LVN_LAUNCH();
+  }
+  return n;
+}
+
 __global__ void zero_outside_k(u8* __restrict__ f, u32 n, u32 v0, u32 v1) {
   for (u64 u = blockIdx.x * u64(blockDim.x) + threadIdx.x; u < n; u += u64(gridDim.x) * blockDim.x)
     if (u < v0 || u >= v1) f[u] = 0;

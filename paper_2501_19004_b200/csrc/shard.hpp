@@ -14,6 +14,10 @@ u32 key_bits(u32 count);
 // sorted by key, distinct keys at the front of keys / vals; returns their number
 u64 partial_super_edges(const DGraph& g, const u32* C, u32 v0, u32 v1, u32 kb, DBuf<ull>& keys, DBuf<double>& vals,
                         cudaStream_t s);
+// holey partial super-rows (aggregate_device with PartialRows) flattened to
+// (row << kb | target, fp64 w) entries in row order; returns their number
+u64 holey_entries(const u64* hoff, const u32* htgt, const double* hw64, const u32* fill, u32 count, u32 kb,
+                  DBuf<ull>& keys, DBuf<double>& vals, cudaStream_t s);
 // cnt[c] = entries of row c among n sorted keys (cnt zeroed here, count entries)
 void super_row_counts(const ull* keys, u64 n, u32 count, u32 kb, u32* cnt, cudaStream_t s);
 // cut[k] = first entry whose row reaches cb[k] (k < parts), cut[parts] = n

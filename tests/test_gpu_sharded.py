@@ -124,9 +124,9 @@ def test_sharded_collapse_mid_run(lvn_single, port, world):
 
 
 def test_sharded_aggregation_in_slices(lvn_single, port):
-    # each rank's partial super-edges built from 4096-arc slices (the C5-scale
-    # memory bound) and merged: the same results as whole-rank sorts
-    out = run(2, "rmat", env={"LVN_SHARD_SLICE_LOG2": "12"})
+    # the sort variant of the partial super-edges, built from 4096-arc slices
+    # (the C5-scale memory bound) and merged
+    out = run(2, "rmat", env={"LVN_SHARD_AGG_SORT": "1", "LVN_SHARD_SLICE_LOG2": "12"})
     g = make("rmat")
     m0 = out[0]["m"]
     for v in out.values():
