@@ -124,13 +124,12 @@ typedef struct lvn_params {
    * (levels[k][v] = community of vertex v of pass k's graph; composing the
    * levels gives the final partition, lookup_dendrogram of louvain_mc.cpp:145) */
   int keep_levels;              /* 0 */
-  /* the first sweep of pass 0 visits consecutive vertex-id ranges of about
-   * 2^first_range_arcs_log2 arcs each (at most 16; low degree first within a
-   * range); with host input each range's targets are a separate chunk of the
-   * upload, and the sweep of a range starts as soon as its chunk has landed.
-   * Graphs with fewer than two ranges' worth of arcs sweep in one range;
-   * 0 disables */
-  int first_range_arcs_log2;    /* 29 */
+  /* graphs with at least 16 x 2^first_range_arcs_log2 arcs sweep pass 0's
+   * first iteration in 16 consecutive vertex-id ranges (low degree first
+   * within a range); with host input each range's targets are a separate
+   * chunk of the upload, and the sweep of a range starts as soon as its chunk
+   * has landed. Smaller graphs sweep in one range; 0 disables */
+  int first_range_arcs_log2;    /* 27: graphs of >= 2^31 arcs */
 } lvn_params;
 
 /* Per-kernel-family device accounting (CUDA events on the engine stream). */

@@ -287,8 +287,8 @@ void validate(const lvn_params& p) {
   if (p.sweep_order != 0 && p.sweep_order != 1) fail(kInvalid, "sweep_order must be 0 or 1");
   if (p.shard_min_arcs_log2 < 0 || p.shard_min_arcs_log2 > 62) fail(kInvalid, "shard_min_arcs_log2 must be in [0, 62]");
   if (p.shard_rounds < 0 || p.shard_rounds > 64) fail(kInvalid, "shard_rounds must be in [0, 64]");
-  if (p.first_range_arcs_log2 < 0 || p.first_range_arcs_log2 > 62)
-    fail(kInvalid, "first_range_arcs_log2 must be in [0, 62]");
+  if (p.first_range_arcs_log2 < 0 || p.first_range_arcs_log2 > 58)
+    fail(kInvalid, "first_range_arcs_log2 must be in [0, 58]");
   if (!(p.bin_thread_max <= p.bin_group_max && p.bin_group_max <= p.bin_warp_max &&
         p.bin_warp_max <= p.bin_block_max))
     fail(kInvalid, "degree bin edges must be non-decreasing");
@@ -411,9 +411,13 @@ struct FirstSweep {
   int ranges() const { return vb.empty() ? 1 : int(vb.size()) - 1; }
 };
 
+// 16 ranges when the graph holds 16 ranges' worth of arcs, else one: the
+// overlap matters where the upload dominates, and on smaller skewed graphs a
+// ranged first sweep changes the dynamics (RMAT-24 with 2^26-arc ranges: Q
+// 0.0573 -> 0.052)
 int first_range_count(u64 a, int log2) {
-  if (log2 <= 0 || log2 >= 63) return 1;
-  return int(std::min<u64>(16, a >> log2));
+  if (log2 <= 0 || log2 >= 59) return 1;
+  return (a >> log2) >= 16 ? 16 : 1;
 }
 std::vector<u32> first_ranges(const u64* host_off, u32 n, u64 a, int log2) {
   const int R0 = first_range_count(a, log2);
@@ -1671,7 +1675,7 @@ void lvn_params_default(lvn_params* p) {
   p->shard_min_arcs_log2 = 22;
   p->shard_rounds = 0;
   p->keep_levels = 0;
-  p->first_range_arcs_log2 = 29;
+  p->first_range_arcs_log2 = 27;
 }
 
 int lvn_init(int num_gpus, const int* devices) {

@@ -129,7 +129,7 @@ class CompactOptions:  # louvain_compact.hpp:35-40
     singleton_rule: bool = False  # singleton joins singleton only toward the lower id
     shard_min_arcs_log2: int = 22  # louvain_sharded: shard passes with >= 2**this arcs
     shard_rounds: int = 0  # louvain_sharded: exchanges per iteration (rounds over own rows); 0 = 2 x ranks
-    first_range_arcs_log2: int = 29  # pass 0's first sweep in id ranges of 2**this arcs (upload overlap); 0 off
+    first_range_arcs_log2: int = 27  # >= 16 * 2**this arcs: pass 0's first sweep in 16 id ranges (upload overlap); 0 off
 
 
 @dataclass
