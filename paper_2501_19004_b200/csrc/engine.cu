@@ -1169,6 +1169,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
   std::vector<u64> app;
   int passes = 0, aggregations = 0, sharded_passes = 0;
   DBuf<u32> mrec, mall, mcount;  // sharded: own move records (u, to), everyone's, per-rank counts
+  DBuf<u64> segbuf;              // sharded (NCCL): record block offsets of a round
   struct Levels : std::vector<u32*> {  // dendrogram (p.keep_levels): local membership of every pass
     ~Levels() {
       for (u32* q : *this) std::free(q);
@@ -1195,9 +1196,10 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     size_t sp = tm.begin(LVN_STAT_RESET, s);
     pass_reset(cur, B, K.p, S.p, C.p, flags.p, s, uni.p);
     tm.end(sp, s, 4.0 * double(cur.arcs) + 29.0 * nv);
+    std::vector<u32> vb;  // sharded: every rank's first row (and nv)
     if (sharded) {
       // K of every vertex from its owner; Sigma = K (singletons)
-      std::vector<u32> vb(cm.size() + 1);
+      vb.assign(cm.size() + 1, 0);
       std::vector<u64> kb(cm.size());
       {
         DBuf<u32> rb(cm.size() + 1);
@@ -1342,6 +1344,30 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
           // OR-reduced at the end of the iteration
           std::vector<u64> four(cm.size(), 4);
           cm.allgatherv(a.moves_n, mcount.p, four, s);
+          if (cm.nc) {
+            // library NCCL: no host round trip. Every rank's record block has
+            // the capacity of its round (one record per vertex of the round,
+            // known to all from the row bounds); the apply kernel reads the
+            // real counts from device memory.
+            const int P = cm.size();
+            std::vector<u64> bytes(P), segoff(P + 1, 0);
+            for (int j = 0; j < P; ++j) {
+              const u64 lo = vb[j] + u64(vb[j + 1] - vb[j]) * k / R;
+              const u64 hi = vb[j] + u64(vb[j + 1] - vb[j]) * (k + 1) / R;
+              bytes[j] = 8 * (hi - lo);
+              segoff[j + 1] = segoff[j] + (hi - lo);
+            }
+            if (segoff[P]) {
+              mall.ensure(2 * segoff[P]);
+              segbuf.ensure(P + 1);
+              // pageable source: staged before the call returns (no reuse race
+              // with the next round, which does not wait for this copy)
+              LVN_CUDA(cudaMemcpyAsync(segbuf.p, segoff.data(), (P + 1) * sizeof(u64), cudaMemcpyHostToDevice, s));
+              cm.allgatherv(mrec.p, mall.p, bytes, s);
+              apply_moves_segments(mall.p, segbuf.p, mcount.p, P, cm.rank(), segoff[P], C.p, K.p, S.p, s);
+            }
+            continue;
+          }
           u32* hn = reinterpret_cast<u32*>(c.pinned);
           LVN_CUDA(cudaMemcpyAsync(hn, mcount.p, cm.size() * sizeof(u32), cudaMemcpyDeviceToHost, s));
           LVN_CUDA(cudaStreamSynchronize(s));

@@ -144,6 +144,11 @@ void apply_moves(const u32* rec, u64 total, u64 skip_lo, u64 skip_hi, const DGra
 // table probing mode of the local-moving / aggregation kernels (lvn_probing)
 void set_probing_move(int mode, cudaStream_t s);
 void set_probing_aggregate(int mode, cudaStream_t s);
+// the same from per-rank record blocks of fixed capacity: block j holds
+// counts[j] (device) valid records from segoff[j] (device, P+1 entries); block
+// me is this rank's own (already applied)
+void apply_moves_segments(const u32* rec, const u64* segoff, const u32* counts, int P, int me, u64 total, u32* C,
+                          const double* K, double* sigma, cudaStream_t s);
 // one sweep over the bins of `bins` (see the kBin* classes)
 void move_sweep(const MoveArgs& a, const BinView& bins, int value_bits, cudaStream_t s);
 

@@ -1588,7 +1588,36 @@ __global__ void apply_moves_k(const u32* __restrict__ rec, u64 total, u64 skip_l
   }
 }
 
+// records in per-rank blocks of fixed capacity (segoff), only the first
+// counts[j] of block j valid; the own block (me) is skipped
+__global__ void apply_segments_k(const u32* __restrict__ rec, const u64* __restrict__ segoff,
+                                 const u32* __restrict__ counts, int P, int me, u64 total, u32* __restrict__ C,
+                                 const double* __restrict__ K, double* __restrict__ sigma) {
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < total; i += u64(gridDim.x) * blockDim.x) {
+    int lo = 0, hi = P;  // block of record i: last j with segoff[j] <= i
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) / 2;
+      if (segoff[mid] <= i) lo = mid; else hi = mid;
+    }
+    if (lo == me || i - segoff[lo] >= counts[lo]) continue;
+    const u32 u = rec[2 * i], to = rec[2 * i + 1];
+    const u32 from = C[u];
+    const double ku = K[u];
+    C[u] = to;
+    atomicAdd(&sigma[to], ku);
+    atomicAdd(&sigma[from], -ku);
+  }
+}
+
 }  // namespace
+
+void apply_moves_segments(const u32* rec, const u64* segoff, const u32* counts, int P, int me, u64 total, u32* C,
+                          const double* K, double* sigma, cudaStream_t s) {
+  if (!total) return;
+  const u64 blocks = std::min<u64>((total + 255) / 256, u64(sm_count()) * 8);
+  apply_segments_k<<<unsigned(blocks), 256, 0, s>>>(rec, segoff, counts, P, me, total, C, K, sigma);
+  LVN_LAUNCH();
+}
 
 void apply_moves(const u32* rec, u64 total, u64 skip_lo, u64 skip_hi, const DGraph& g, u32* C, const double* K,
                  double* sigma, u8* flags, int prune, cudaStream_t s) {
