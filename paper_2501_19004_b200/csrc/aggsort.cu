@@ -10,15 +10,19 @@
 // key (c, d) to a buffer; the keys are radix-sorted (2 x ceil(log2 count)
 // bits) and run-length encoded, and the runs ARE the super-graph's off-diagonal
 // entries, already in canonical (row, target) order; the self-loops are
-// inserted at their sorted position. On a web graph after its first pass only
-// ~12 % of the arcs cross communities (C5: 0.45 G of 3.79 G), so the merge
-// touches a fraction of the arcs and no hash table at all.
+// inserted at their sorted position. On a web graph after its first pass
+// about a quarter of the arcs cross communities (C5: 0.95 G of 3.79 G), so
+// the merge touches a fraction of the arcs and no hash table at all. Each
+// warp stages its keys in shared memory and reserves global space for them
+// with one atomic per ~224 keys (a single global counter per key ran at
+// 95 ms on C5; 30 ms staged).
 //
 // Integer counts times an integer weight are exact in fp64, so every entry is
 // the fp64 sum of the reference (louvain_mc.cpp:95) before the one narrowing:
-// bit-exact. The path is taken when a sample says the external arcs are few
-// (else the hash aggregation is cheaper) and falls back to it when the
+// bit-exact. The path is taken when a sample says at most 40 % of the arcs
+// are external (else the hash aggregation is cheaper) and falls back to it when the
 // buffer overflows (the counts it made are reused for the row capacities).
+#include <chrono>
 #include <cub/device/device_radix_sort.cuh>
 #include <cub/device/device_run_length_encode.cuh>
 
@@ -52,13 +56,32 @@ __global__ void ext_sample_k(DGraph g, const u32* __restrict__ C, u64 stride, ul
 
 // A row's arcs, G threads per row (32: a warp, kBlock: a block): count the
 // external arcs into ext[c] and append their keys (c << kb | d) at *n_out
-// (keys past cap are dropped; *n_out still counts them)
+// (keys past cap are dropped; *n_out still counts them). Each warp gathers
+// its keys in a shared-memory buffer and reserves global space once per
+// ~224 keys: one global counter took an atomic per 32-arc round from every
+// warp of the GPU and serialised the pass (C5: 95 ms)
+constexpr u32 kWarpBuf = 256;
+
 template <int G>
 __global__ void __launch_bounds__(G < 256 ? 256 : G) ext_emit_k(DGraph g, const u32* __restrict__ list, u64 count,
                                                                 const u32* __restrict__ C, ull* __restrict__ ext,
                                                                 ull* __restrict__ keys, u64 cap, ull* __restrict__ n_out,
                                                                 u32 kb) {
-  const u32 lane = threadIdx.x & 31;
+  constexpr int T = G < 256 ? 256 : G;
+  __shared__ ull buf[T / 32][kWarpBuf];
+  const u32 lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  ull* wb = buf[wid];
+  u32 nb = 0;  // keys in this warp's buffer (warp-uniform)
+  auto flush = [&]() {
+    ull base = 0;
+    if (lane == 0) base = atomicAdd(n_out, ull(nb));
+    base = __shfl_sync(0xffffffffu, base, 0);
+    __syncwarp();
+    for (u32 j = lane; j < nb; j += 32)
+      if (base + j < cap) keys[base + j] = wb[j];
+    __syncwarp();
+    nb = 0;
+  };
   const u64 groups = u64(gridDim.x) * (blockDim.x / G);
   for (u64 i = (blockIdx.x * u64(blockDim.x) + threadIdx.x) / G; i < count; i += groups) {
     const u32 u = list[i];
@@ -73,17 +96,14 @@ __global__ void __launch_bounds__(G < 256 ? 256 : G) ext_emit_k(DGraph g, const 
       const bool x = d != c;
       const u32 m = __ballot_sync(0xffffffffu, x);
       if (!m) continue;
-      ull base = 0;
-      if (lane == 0) base = atomicAdd(n_out, ull(__popc(m)));
-      base = __shfl_sync(0xffffffffu, base, 0);
-      if (x) {
-        const ull pos = base + __popc(m & ((1u << lane) - 1u));
-        if (pos < cap) keys[pos] = (ull(c) << kb) | d;
-      }
+      if (x) wb[nb + __popc(m & ((1u << lane) - 1u))] = (ull(c) << kb) | d;
+      nb += __popc(m);
       mine += __popc(m);
+      if (nb > kWarpBuf - 32) flush();
     }
     if (lane == 0 && mine) atomicAdd(&ext[c], mine);
   }
+  if (nb) flush();
 }
 
 __global__ void run_rows_k(const ull* __restrict__ ukeys, const u32* __restrict__ nruns_p, u32 kb, u32* __restrict__ cnt) {
@@ -157,7 +177,7 @@ T read_one(const T* dev, cudaStream_t s) {
 
 }  // namespace
 
-bool external_arcs_few(const DGraph& g, const u32* C, double max_frac, cudaStream_t s) {
+bool external_arcs_few(const DGraph& g, const u32* C, double max_frac, cudaStream_t s, double* sampled) {
   if (!g.arcs) return false;
   const u64 stride = 61;  // ~1.6 % of the arcs, coprime to the usual row lengths
   DBuf<ull> hits(1);
@@ -168,12 +188,21 @@ bool external_arcs_few(const DGraph& g, const u32* C, double max_frac, cudaStrea
   if (const char* e = std::getenv("LVN_VERBOSE"); e && *e && *e != '0')
     std::fprintf(stderr, "[lvn] aggregate: sampled external-arc fraction %.3f (by external arcs when <= %.2f)\n", frac,
                  max_frac);
+  if (sampled) *sampled = frac;
   return frac <= max_frac;
 }
 
 bool aggregate_by_external_arcs(const DGraph& g, const Bins& b, const u32* C, u32 count, const u64* budget,
                                 u64* ext, u64 cap, OwnedCsr& out, u32* inexact, double* self64, cudaStream_t s) {
   const u32 kb = std::max(1u, ceil_log2_u64(u64(count) + 1));
+  const bool trace = [] {
+    const char* v = std::getenv("LVN_VERBOSE");
+    return v && *v && *v != '0';
+  }();
+  const auto t0 = std::chrono::steady_clock::now();
+  auto ms = [&] {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  };
   LVN_CUDA(cudaMemsetAsync(ext, 0, size_t(count ? count : 1) * sizeof(u64), s));
   DBuf<ull> keys(cap ? cap : 1), nout(1);
   LVN_CUDA(cudaMemsetAsync(nout.p, 0, sizeof(ull), s));
@@ -191,25 +220,35 @@ bool aggregate_by_external_arcs(const DGraph& g, const Bins& b, const u32* C, u3
                                                                                        keys.p, cap, nout.p, kb);
   LVN_LAUNCH();
   const u64 n = read_one(nout.p, s);
+  if (trace)
+    std::fprintf(stderr, "[lvn] aggregate by external arcs: %llu keys (cap %llu) emitted at %.1f ms\n",
+                 (unsigned long long)n, (unsigned long long)cap, ms());
   if (n > cap) return false;  // the hash path takes over (ext is complete)
-  // sort + run-length encode the keys: the distinct off-diagonal entries
-  DBuf<ull> sorted(n ? n : 1), ukeys(n ? n : 1);
+  // sort + run-length encode the keys: the distinct off-diagonal entries.
+  // The sort ping-pongs between the key buffer and one n-key buffer (small
+  // CUB scratch); the run-length encoding writes into whichever is free.
+  DBuf<ull> alt(n ? n : 1);
   DBuf<u32> rcounts(n ? n : 1), nruns(1);
   LVN_CUDA(cudaMemsetAsync(nruns.p, 0, sizeof(u32), s));
+  ull* ukeys = alt.p;
   if (n) {
+    cub::DoubleBuffer<ull> db(keys.p, alt.p);
     size_t b1 = 0, b2 = 0;
-    LVN_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b1, keys.p, sorted.p, n, 0, int(2 * kb), s));
-    LVN_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, sorted.p, ukeys.p, rcounts.p, nruns.p, n, s));
+    LVN_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, b1, db, n, 0, int(2 * kb), s));
+    LVN_CUDA(cub::DeviceRunLengthEncode::Encode(nullptr, b2, db.Current(), db.Alternate(), rcounts.p, nruns.p, n, s));
     DBuf<unsigned char> tmp(std::max(b1, b2));
-    LVN_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, b1, keys.p, sorted.p, n, 0, int(2 * kb), s));
-    LVN_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, b2, sorted.p, ukeys.p, rcounts.p, nruns.p, n, s));
+    LVN_CUDA(cub::DeviceRadixSort::SortKeys(tmp.p, b1, db, n, 0, int(2 * kb), s));
+    ukeys = db.Alternate();
+    LVN_CUDA(cub::DeviceRunLengthEncode::Encode(tmp.p, b2, db.Current(), ukeys, rcounts.p, nruns.p, n, s));
     g_launches += 4;
   }
-  keys.release();
-  sorted.release();
+  if (ukeys == alt.p)
+    keys.release();
+  else
+    alt.release();
   DBuf<u32> cnt(count ? count : 1), len(count ? count : 1);
   LVN_CUDA(cudaMemsetAsync(cnt.p, 0, size_t(count ? count : 1) * sizeof(u32), s));
-  run_rows_k<<<grid_for(n + 1, 256, 8), 256, 0, s>>>(ukeys.p, nruns.p, kb, cnt.p);
+  run_rows_k<<<grid_for(n + 1, 256, 8), 256, 0, s>>>(ukeys, nruns.p, kb, cnt.p);
   LVN_LAUNCH();
   row_len_k<<<grid_for(count, 256, 8), 256, 0, s>>>(cnt.p, budget, e, count, len.p);
   LVN_LAUNCH();
@@ -224,10 +263,10 @@ bool aggregate_by_external_arcs(const DGraph& g, const Bins& b, const u32* C, u3
   out.tgt.alloc(A ? A : 1);
   out.w.alloc(A ? A : 1);
   if (runs)
-    place_runs_k<<<grid_for(runs, 256, 8), 256, 0, s>>>(ukeys.p, rcounts.p, nruns.p, kb, out.off.p, uoff.p, budget, e,
+    place_runs_k<<<grid_for(runs, 256, 8), 256, 0, s>>>(ukeys, rcounts.p, nruns.p, kb, out.off.p, uoff.p, budget, e,
                                                         g.uw, out.tgt.p, out.w.p, inexact);
   LVN_LAUNCH();
-  place_self_k<<<grid_for(count, 256, 8), 256, 0, s>>>(ukeys.p, kb, count, out.off.p, uoff.p, budget, e, g.uw,
+  place_self_k<<<grid_for(count, 256, 8), 256, 0, s>>>(ukeys, kb, count, out.off.p, uoff.p, budget, e, g.uw,
                                                        out.tgt.p, out.w.p, self64);
   LVN_LAUNCH();
   DBuf<double> tw(1);
@@ -237,6 +276,7 @@ bool aggregate_by_external_arcs(const DGraph& g, const Bins& b, const u32* C, u3
     LVN_LAUNCH();
   }
   out.total_weight = read_one(tw.p, s) / 2.0;
+  if (trace) std::fprintf(stderr, "[lvn] aggregate by external arcs: %u runs, done at %.1f ms\n", runs, ms());
   return true;
 }
 

@@ -701,6 +701,15 @@ bool verbose() {
   return on;
 }
 
+// LVN_AGG_SORT_FRAC=f: aggregate by external arcs when a sample finds at most f of them (0.4)
+double agg_sort_frac() {
+  static const double f = [] {
+    const char* e = std::getenv("LVN_AGG_SORT_FRAC");
+    return e ? std::atof(e) : 0.4;
+  }();
+  return f;
+}
+
 // LVN_AGG_SORT=0: never aggregate by external arcs (A/B aid)
 bool agg_sort_off() {
   static const bool off = [] {
@@ -728,15 +737,18 @@ void aggregate_device(const DGraph& g, const u32* C, u32 count, const BinEdges& 
   community_counts(g, C, count, msize.p, budget.p, s);
   // Uniform integer weights with few arcs between communities (a clustered
   // unweighted graph's first aggregation): aggregate by the external arcs
-  // alone (aggsort.cu); the sample decides (<= 15 %: 17 vs 20 ms on the C2
-  // graph under its planted blocks; at C5's 27 % the sort of 1 G keys loses,
-  // 168-175 vs 156 ms, profiles/agg_ab.py), an overflow falls back here with
-  // the external-arc counts already made
+  // alone (aggsort.cu) when a sample finds at most 40 % of them (C2 under
+  // its planted blocks, 10 %: 17 vs 20 ms; C5's first pass, 25 %: 101 vs
+  // 156 ms, profiles/r02_agg_ab.txt); an overflow of the key buffer falls
+  // back here with the external-arc counts already made
   bool ext_ready = false;
+  double frac = 0;
   if (gbins && g.uniform && g.uw == std::floor(g.uw) && g.uw > 0.f && g.arcs >= (u64(1) << 20) && !agg_sort_off() &&
-      external_arcs_few(g, C, 0.15, s)) {
-    // key buffer: 45 % of the arcs, bounded by the memory the sort needs (~28 B per key)
-    const u64 cap = std::min<u64>(g.arcs * 45 / 100 + 4096, ctx().pool.available() / 32);
+      external_arcs_few(g, C, agg_sort_frac(), s, &frac)) {
+    // key buffer: the sampled fraction with a 20 % margin, bounded by the
+    // memory the sort needs (~20 B per key: keys, their sort partner, counts)
+    const u64 cap = std::min<u64>(u64(double(g.arcs) * std::min(1.0, frac * 1.2 + 0.01)) + 4096,
+                                  ctx().pool.available() / 24);
     if (aggregate_by_external_arcs(g, *gbins, C, count, budget.p, ext.p, cap, out, inexact, self64, s))
       return;
     ext_ready = true;

@@ -245,7 +245,7 @@ void keys_to_csr(DBuf<ull>& keys, u64 nkeys, u64 n, OwnedCsr& out, cudaStream_t 
 
 // ---- aggsort.cu: aggregation of a uniform integer-weight pass by external arcs
 // true when a sample of the arcs finds at most max_frac of them between communities
-bool external_arcs_few(const DGraph& g, const u32* C, double max_frac, cudaStream_t s);
+bool external_arcs_few(const DGraph& g, const u32* C, double max_frac, cudaStream_t s, double* sampled = nullptr);
 // the super-graph of g under C (count communities, budget = member arcs per
 // community) from the external arcs (ext receives their count per community;
 // cap = key buffer entries); false when more than cap arcs are external (out
