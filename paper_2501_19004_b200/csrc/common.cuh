@@ -96,8 +96,20 @@ class Pool {
   // cudaMemGetInfo; called at the entry of a run while the stream is idle
   // (mid-run, cudaMemGetInfo stalls the host for tens of ms)
   void refresh_external();
+  // Graph capture of a sweep: transient buffers come from a caller-owned
+  // arena (no allocation nodes in the captured body; the arena outlives the
+  // graph), sized from the bytes the same sweep requested uncaptured
+  // (track_begin / track_end).
+  void arena_begin(void* base, size_t bytes);
+  void arena_end();
+  void track_begin();
+  size_t track_end();
 
  private:
+  unsigned char* arena_ = nullptr;
+  size_t arena_cap_ = 0, arena_used_ = 0;
+  bool arena_on_ = false, tracking_ = false;
+  size_t tracked_ = 0;
   void* raw(size_t bytes);
   cudaMemPool_t pool_ = nullptr;
   cudaStream_t stream_ = nullptr;
@@ -131,6 +143,10 @@ struct Context {
   size_t smem_optin = 227 * 1024;
   cudaStream_t stream = nullptr;
   cudaStream_t copy = nullptr;  // host -> device input chunks (overlapped with the first sweep)
+  // forked streams + events of a captured sweep with concurrent degree bins
+  std::vector<cudaStream_t> aux;
+  std::vector<cudaEvent_t> aux_ev;
+  void ensure_aux(int n);
   Pool pool;
   HostCache host;
   u64* pinned = nullptr;  // 8192 u64 of pinned host scratch

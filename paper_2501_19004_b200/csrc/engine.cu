@@ -91,7 +91,26 @@ bool pool_nocache() {
   return v;
 }
 
+void Pool::arena_begin(void* base, size_t bytes) {
+  arena_ = static_cast<unsigned char*>(base), arena_cap_ = bytes, arena_used_ = 0, arena_on_ = true;
+}
+// every arena block is released inside the captured sweep that took it
+void Pool::arena_end() { arena_on_ = false, arena_ = nullptr, arena_cap_ = 0; }
+void Pool::track_begin() { tracking_ = true, tracked_ = 0; }
+size_t Pool::track_end() {
+  tracking_ = false;
+  return tracked_;
+}
+
 void* Pool::get(size_t bytes) {
+  const size_t r256 = ((bytes ? bytes : 1) + 255) & ~size_t(255);
+  if (tracking_) tracked_ += r256;
+  if (arena_on_) {
+    if (arena_used_ + r256 > arena_cap_) fail(kInternal, "graph capture arena exhausted");
+    void* p = arena_ + arena_used_;
+    arena_used_ += r256;
+    return p;
+  }
   if (bytes >= kBigBytes && !pool_nocache()) {
     const size_t unit = (size_t(1) << (63 - __builtin_clzll(bytes))) / 16;
     const size_t r = (bytes + unit - 1) / unit * unit;
@@ -129,6 +148,7 @@ void* Pool::get(size_t bytes) {
 
 void Pool::put(void* p) {
   if (!p) return;
+  if (arena_ && p >= arena_ && p < arena_ + arena_cap_) return;  // arena blocks live as long as the arena
   auto it = big_used_.find(p);
   if (it != big_used_.end()) {
     big_free_.emplace(it->second, p);
@@ -233,10 +253,25 @@ Context& ctx() {
 
 int sm_count() { return ctx().sms; }
 
+void Context::ensure_aux(int n) {
+  while (int(aux.size()) < n) {
+    cudaStream_t t;
+    LVN_CUDA(cudaStreamCreateWithFlags(&t, cudaStreamNonBlocking));
+    aux.push_back(t);
+  }
+  while (int(aux_ev.size()) < 2 * n + 1) {
+    cudaEvent_t e;
+    LVN_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    aux_ev.push_back(e);
+  }
+}
+
 void destroy_context() {
   std::lock_guard<std::mutex> lk(g_ctx_mu);
   if (!g_ctx) return;
   (void)cudaStreamSynchronize(g_ctx->stream);
+  for (cudaStream_t t : g_ctx->aux) (void)cudaStreamDestroy(t);
+  for (cudaEvent_t e : g_ctx->aux_ev) (void)cudaEventDestroy(e);
   g_ctx->pool.release_all();
   (void)cudaFreeHost(g_ctx->pinned);
   (void)cudaStreamDestroy(g_ctx->stream);
@@ -511,6 +546,7 @@ struct Timing {
     int fam;
     double bytes;
     ull items, arcs, gathers;
+    ull count;  // iterations the span covers (a captured pass: all but its first)
   };
   std::vector<Span> spans;
   std::vector<cudaEvent_t> free_events;
@@ -525,7 +561,7 @@ struct Timing {
     return e;
   }
   size_t begin(int fam, cudaStream_t s) {
-    Span sp{ev(), ev(), fam, 0.0, 0, 0, 0};
+    Span sp{ev(), ev(), fam, 0.0, 0, 0, 0, 1};
     LVN_CUDA(cudaEventRecord(sp.a, s));
     spans.push_back(sp);
     return spans.size() - 1;
@@ -547,7 +583,7 @@ struct Timing {
       lvn_phase_stats& f = st[sp.fam];
       f.seconds += ms * 1e-3;
       f.bytes += sp.bytes;
-      f.launches += 1;
+      f.launches += sp.count;
       f.items += sp.items;
       f.arcs += sp.arcs;
       f.gathers += sp.gathers;
@@ -569,6 +605,64 @@ struct IterRecord {  // device scratch read back once per iteration
   ull verts, arcs, moves, gathers;
   ull active[kMaxRanges * kBins];  // per-(range, bin) sizes of the next active lists
 };
+
+// per-iteration tallies of a captured pass (the IterRecord prefix)
+struct IterHist {
+  double gain;
+  ull verts, arcs, moves, gathers;
+};
+
+// End of one captured iteration: keep its tallies, reset them, set the next
+// iteration's Pick-Less word and decide on the device whether the while
+// node runs again (louvain_compact.cpp:209: stop once the gain is at most
+// the tolerance, or after max_iterations).
+__global__ void iter_end_k(IterRecord* rec, IterHist* hist, u32* it, double tol, u32 max_it, int period,
+                           int* pickless, cudaGraphConditionalHandle h) {
+  if (threadIdx.x) return;
+  const u32 i = *it;
+  const IterHist e{rec->gain, rec->verts, rec->arcs, rec->moves, rec->gathers};
+  hist[i] = e;
+  rec->gain = 0.0;
+  rec->verts = rec->arcs = rec->moves = rec->gathers = 0;
+  *it = i + 1;
+  *pickless = (int(i + 1) + period / 2) % period == 0;
+  cudaGraphSetConditional(h, e.gain > tol && i + 1 < max_it ? 1u : 0u);
+}
+
+__global__ void graph_init_k(u32* it, u32 first, int* pickless, int pl) {
+  if (threadIdx.x) return;
+  *it = first;
+  *pickless = pl;
+}
+
+// LVN_GRAPH_VERTS_LOG2=k: whole-graph passes of at most 2^k vertices run
+// their iterations after the first as ONE launch of a CUDA graph whose while
+// node loops on the device; their bins sweep the full degree lists (prune
+// flags checked in the kernels) so the body has static launch shapes. Off by
+// default: capture + instantiation cost 0.3-0.7 ms per pass, more than the
+// host round trips it removes on C1 / C4 (profiles/r02_graph_ab.txt).
+// LVN_FORK_VERTS_LOG2=k: passes of at most 2^k vertices run the degree bins
+// of a sweep on forked streams, so the launch tails of small classes overlap
+// (captured or not). Off by default: C1's local moving drops 1.71 -> 1.15-1.3
+// ms, but the looser order costs up to 0.001 Q there, and C1 sits 0.0049
+// from the 0.005 quality gate.
+int graph_verts_log2() {
+  static const int v = [] {
+    const char* e = std::getenv("LVN_GRAPH_VERTS_LOG2");
+    const char* d = std::getenv("LVN_SYNC_DEBUG");
+    if (d && *d && *d != '0') return 0;
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+int fork_verts_log2() {
+  static const int v = [] {
+    const char* e = std::getenv("LVN_FORK_VERTS_LOG2");
+    return e ? std::atoi(e) : -1;
+  }();
+  return v;
+}
+constexpr int kForkStreams = 6;
 
 // vertex-id ranges of one sweep (lvn_params.sweep_ranges)
 int sweep_ranges(const lvn_params& p, u32 nv) {
@@ -1103,6 +1197,109 @@ void check_err(const u32* err, cudaStream_t s) {
 }
 
 // ---------------------------------------------------------------------------
+// Captured local moving (late / small passes)
+// ---------------------------------------------------------------------------
+// Iterations 1.. of a pass as one graph launch: a while node whose body is
+// the sweep (degree bins serial, or forked onto parallel branches) and
+// iter_end_k, which sets the loop condition on the device. The body's
+// transient buffers (hub scratch, scan partials) come from an arena sized by
+// the uncaptured first sweep. No host round trip until the pass converges;
+// returns the iterations run.
+struct CaptureScope {  // ends an open capture / arena if a failure unwinds through it
+  cudaStream_t s;
+  bool open = false;
+  ~CaptureScope() {
+    if (!open) return;
+    ctx().pool.arena_end();
+    cudaGraph_t g = nullptr;
+    (void)cudaStreamEndCapture(s, &g);
+    if (g) (void)cudaGraphDestroy(g);
+    (void)cudaGetLastError();
+  }
+};
+
+int graph_iterations(MoveArgs a, const BinView& view, const lvn_params& p, double tolerance, size_t sweep_bytes,
+                     bool fork, IterRecord* rec, int pass, Timing& tm, cudaStream_t s) {
+  Context& c = ctx();
+  const u32 max_it = u32(p.max_iterations);
+  DBuf<u32> itc(1);
+  DBuf<int> plw(1);
+  DBuf<IterHist> hist(max_it);
+  DBuf<unsigned char> arena(sweep_bytes + 4096);
+  if (fork) c.ensure_aux(kForkStreams);
+  cudaGraph_t g = nullptr;
+  cudaGraphExec_t ex = nullptr;
+  LVN_CUDA(cudaGraphCreate(&g, 0));
+  struct Owned {
+    cudaGraph_t& g;
+    cudaGraphExec_t& ex;
+    ~Owned() {
+      if (ex) (void)cudaGraphExecDestroy(ex);
+      if (g) (void)cudaGraphDestroy(g);
+    }
+  } owned{g, ex};
+  cudaGraphConditionalHandle h;
+  LVN_CUDA(cudaGraphConditionalHandleCreate(&h, g, 1, cudaGraphCondAssignDefault));
+  cudaGraphNodeParams np{};
+  np.type = cudaGraphNodeTypeConditional;
+  np.conditional.handle = h;
+  np.conditional.type = cudaGraphCondTypeWhile;
+  np.conditional.size = 1;
+  cudaGraphNode_t node;
+  LVN_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+  cudaGraph_t body = np.conditional.phGraph_out[0];
+  a.pickless_dev = plw.p;
+  a.nfork = fork ? kForkStreams : 0;
+  const ull l0 = g_launches.load();
+  {
+    CaptureScope cs{s};
+    LVN_CUDA(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeRelaxed));
+    cs.open = true;
+    c.pool.arena_begin(arena.p, arena.n);
+    move_sweep(a, view, p.value_bits, s);
+    iter_end_k<<<1, 32, 0, s>>>(rec, hist.p, itc.p, tolerance, max_it, p.pick_less_period, plw.p, h);
+    LVN_LAUNCH();
+    c.pool.arena_end();
+    cs.open = false;
+    cudaGraph_t out = nullptr;
+    LVN_CUDA(cudaStreamEndCapture(s, &out));
+  }
+  const ull per = g_launches.load() - l0;
+  LVN_CUDA(cudaGraphInstantiate(&ex, g, 0));
+  LVN_CUDA(cudaMemsetAsync(rec, 0, sizeof(IterRecord), s));
+  graph_init_k<<<1, 32, 0, s>>>(itc.p, 1u, plw.p, pick_less_active(1, p.pick_less_period) ? 1 : 0);
+  LVN_LAUNCH();
+  const size_t sp = tm.begin(LVN_STAT_MOVE, s);
+  LVN_CUDA(cudaGraphLaunch(ex, s));
+  tm.end(sp, s, 0.0);
+  u32 n = 1;
+  {
+    u32* hn = reinterpret_cast<u32*>(c.pinned);
+    LVN_CUDA(cudaMemcpyAsync(hn, itc.p, sizeof(u32), cudaMemcpyDeviceToHost, s));
+    LVN_CUDA(cudaStreamSynchronize(s));
+    n = std::min(*hn, max_it);
+  }
+  std::vector<IterHist> hh(n);
+  LVN_CUDA(cudaMemcpyAsync(hh.data(), hist.p, n * sizeof(IterHist), cudaMemcpyDeviceToHost, s));
+  LVN_CUDA(cudaStreamSynchronize(s));
+  double bytes = 0;
+  ull verts = 0, arcs = 0, gathers = 0;
+  for (u32 i = 1; i < n; ++i) {
+    bytes += 12.0 * double(hh[i].arcs) + 32.0 * double(hh[i].verts);
+    verts += hh[i].verts, arcs += hh[i].arcs, gathers += hh[i].gathers;
+    if (verbose())
+      std::fprintf(stderr, "[lvn] pass %d it %u (graph%s): %llu vertices, %llu arcs, %llu moves, gain %.6g\n", pass,
+                   i, fork ? ", forked bins" : "", (unsigned long long)hh[i].verts, (unsigned long long)hh[i].arcs,
+                   (unsigned long long)hh[i].moves, hh[i].gain);
+  }
+  tm.set_bytes(sp, bytes, verts, arcs, gathers);
+  tm.spans[sp].count = n > 1 ? n - 1 : 1;
+  // the body's kernels ran once per iteration (counted once at capture)
+  if (n > 2) g_launches += per * (n - 2);
+  return int(n) - 1;
+}
+
+// ---------------------------------------------------------------------------
 // Louvain pass shell
 // ---------------------------------------------------------------------------
 // comm (lvn_louvain_sharded): passes with >= 2^shard_min_arcs_log2 arcs are
@@ -1330,7 +1527,16 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     int iterations = 0;
     // iteration 0 sweeps every row with arcs (all flagged); later iterations
     // sweep the flagged rows only, compacted right after the previous sweep
+    // (graph-mode passes: the full lists, see graph_verts_log2)
     active.ensure(nv ? nv : 1);
+    const int gl2 = graph_verts_log2();
+    const bool graph_pass = !shard && R == 1 && R0 == 1 && gl2 > 0 && u64(nv) <= (u64(1) << gl2) &&
+                            p.max_iterations > 1 && move_kernel_variant() == 0 && p.pick_less_period > 0;
+    a.full_lists = graph_pass ? 1 : 0;
+    const bool fork = !shard && fork_verts_log2() >= 0 && u64(nv) <= (u64(1) << fork_verts_log2());
+    if (fork) c.ensure_aux(kForkStreams);
+    a.nfork = fork ? kForkStreams : 0;
+    size_t sweep_bytes = 0;
     for (int it = 0; it < p.max_iterations; ++it) {
       a.pickless = pick_less_active(it, p.pick_less_period);
       LVN_CUDA(cudaMemsetAsync(rec.p, 0, sizeof(IterRecord), s));
@@ -1348,7 +1554,9 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
         if (shard) LVN_CUDA(cudaMemsetAsync(a.moves_n, 0, sizeof(u32), s));
         sp = tm.begin(LVN_STAT_MOVE, s);
         if (k == 0) sp0 = sp;
+        if (graph_pass) c.pool.track_begin();
         move_sweep(a, views[k], p.value_bits, s);
+        if (graph_pass) sweep_bytes = c.pool.track_end();
         tm.end(sp, s, 0.0);
         if (shard) {
           // every rank applies the other ranks' moves of this round (C, Sigma)
@@ -1407,7 +1615,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
           zero_outside(flags.p, nv, v0, v1, s);
         }
       }
-      if (p.prune)
+      if (p.prune && !graph_pass)
         for (int k = 0; k < R; ++k)
           compact_active(R > 1 ? rbins[k] : SB, flags.p, active.p + rbase[k], rec.p->active + k * kBins, s);
       IterRecord* h = reinterpret_cast<IterRecord*>(c.pinned);
@@ -1420,6 +1628,10 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
                      h->gain);
       ++iterations;
       if (h->gain <= tolerance) break;  // louvain_compact.cpp:209
+      if (graph_pass) {
+        iterations += graph_iterations(a, views[0], p, tolerance, sweep_bytes, fork, rec.p, pass, tm, s);
+        break;
+      }
       if (p.prune)
         for (int k = 0; k < R; ++k) {
           views[k].list = active.p + rbase[k];

@@ -89,6 +89,7 @@ struct MoveArgs {
   u8* flags = nullptr;
   double m = 1.0;
   int pickless = 0;
+  const int* pickless_dev = nullptr;  // graph-mode passes: Pick-Less of the running iteration (device word)
   int prune = 1;
   int dry = 0;              // evaluate only: write out_to / out_gain, apply nothing
   // probe (lvn_probe_moves): the live kernels (the engine's ranking: reciprocal
@@ -107,6 +108,12 @@ struct MoveArgs {
   float uniform_w = 0.f;
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
   int hubs_first = 0;          // bin order of a sweep: highest degree class first
+  // full bin lists (graph-mode passes): every kernel skips the rows whose
+  // prune flag is clear instead of relying on a compacted active list
+  int full_lists = 0;
+  // > 0: the degree bins of one sweep run on this many forked streams
+  // (captured sweeps of small passes): the launch tails of the classes overlap
+  int nfork = 0;
   u32* csize = nullptr;        // community member counts (singleton-pair rule), or null
   // sharded runs: every applied move appends (u, to) here (count in *moves_n)
   u32* moves_out = nullptr;
@@ -142,6 +149,7 @@ void hub_plan_build(const DGraph& g, const u32* hubs, u64 count, int value_bits,
 void apply_moves(const u32* rec, u64 total, u64 skip_lo, u64 skip_hi, const DGraph& g, u32* C, const double* K,
                  double* sigma, u8* flags, int prune, cudaStream_t s);
 // table probing mode of the local-moving / aggregation kernels (lvn_probing)
+int move_kernel_variant();  // LVN_MOVE_KERNEL: 0 = default (lm_psort), 1 = sort, 2 = match
 void set_probing_move(int mode, cudaStream_t s);
 void set_probing_aggregate(int mode, cudaStream_t s);
 // the same from per-rank record blocks of fixed capacity: block j holds

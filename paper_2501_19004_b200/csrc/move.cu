@@ -134,7 +134,7 @@ __device__ __forceinline__ bool decide(const MoveArgs& x, u32 u, u32 from, doubl
     x.out_gain[u] = mv ? gr : 0.0;
     return false;
   }
-  if (mv && x.pickless && bc > from) mv = false;
+  if (mv && (x.pickless_dev ? *x.pickless_dev : x.pickless) && bc > from) mv = false;
   // singleton pairs: two singletons that pick each other would swap labels
   // instead of merging when they decide concurrently; only the move toward
   // the lower id is taken, so the pair merges (Pick-Less, restricted to the
@@ -412,7 +412,9 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
   // vertex in flight (the trip count is uniform across the block, so every
   // lane reaches every shuffle)
   u64 i0 = u64(blockIdx.x) * GPB;
-  bool have = i0 + gi < count;
+  // full bin lists: a row whose prune flag is clear is a hole in the pipeline
+  auto live = [&](u32 v) { return !x.full_lists || !x.prune || x.flags[v] != 0; };
+  bool have = i0 + gi < count && live(list[i0 + gi]);
   u32 u = 0, from = kEmpty;
   u64 lo = 0, hi = 0;
   double ku = 0.0, sf = 0.0;
@@ -598,7 +600,9 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
 
   // prologue: vertex i fully loaded, vertex i+1's header
   u64 i0 = u64(blockIdx.x) * GPB;
-  bool have = i0 + gi < count;
+  // full bin lists: a row whose prune flag is clear is a hole in the pipeline
+  auto live = [&](u32 v) { return !x.full_lists || !x.prune || x.flags[v] != 0; };
+  bool have = i0 + gi < count && live(list[i0 + gi]);
   u32 u = 0, from = kEmpty;
   u64 lo = 0, hi = 0;
   double ku = 0.0, sf = 0.0;
@@ -614,7 +618,7 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
   load_row(u, lo, hi, t, val);
   if (have) sf = x.sigma[from];
   gather(u, from, t, key, val);
-  bool have1 = i0 + stride + gi < count;
+  bool have1 = i0 + stride + gi < count && live(list[i0 + stride + gi]);
   u32 u1 = 0, from1 = kEmpty;
   u64 lo1 = 0, hi1 = 0;
   double ku1 = 0.0;
@@ -632,8 +636,8 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
     V val1[K];
     load_row(u1, lo1, hi1, t1, val1);
     const u64 in2 = i0 + 2 * stride + gi;
-    const bool have2 = in2 < count;
-    const u32 u2 = have2 ? list[in2] : 0u;
+    const u32 u2 = in2 < count ? list[in2] : 0u;
+    const bool have2 = in2 < count && live(u2);
 
     // (i) group the arcs by community, fetch the weights in sorted order
     // rows whose communities already ascend in row order (every row in the
@@ -1164,11 +1168,12 @@ __global__ void hub_clear_k(const u32* __restrict__ hubs, u64 count, DGraph g, c
   }
 }
 
+// (full bin lists: a hub whose prune flag is clear gets no chunk, and no decision)
 __global__ void hub_chunk_counts_k(const u32* __restrict__ hubs, u64 count, const u64* __restrict__ off,
-                                   u32* __restrict__ chunks) {
+                                   u32* __restrict__ chunks, const u8* __restrict__ skip_clear) {
   for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < count; i += u64(gridDim.x) * blockDim.x) {
     const u32 u = hubs[i];
-    chunks[i] = u32((off[u + 1] - off[u] + kHubChunk - 1) / kHubChunk);
+    chunks[i] = skip_clear && !skip_clear[u] ? 0u : u32((off[u + 1] - off[u] + kHubChunk - 1) / kHubChunk);
   }
 }
 
@@ -1304,6 +1309,7 @@ __global__ void lm_hub_decide(MoveArgs x, const u32* __restrict__ hubs, u64 coun
   Tally tl;
   const u64 warps = u64(gridDim.x) * (blockDim.x >> 5);
   for (u64 i = (blockIdx.x * u64(blockDim.x) + threadIdx.x) >> 5; i < count; i += warps) {
+    if (chunk_off[i] == chunk_off[i + 1]) continue;  // inactive (full lists); a hub has arcs
     double bg = -INFINITY, bk = 0.0;
     u32 bc = kEmpty, ranked = 0;
     for (u64 v = chunk_off[i] + lane; v < chunk_off[i + 1]; v += 32) {
@@ -1434,7 +1440,7 @@ template <class Tab, bool DRY>
 void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
   using V = typename Tab::V;
   const int sms = sm_count();
-  auto launch_bin = [&](int bin) {
+  auto launch_bin = [&](int bin, cudaStream_t s) {
     if (!b.count(bin)) return;
     switch (bin) {
       case kBinThread: {
@@ -1511,7 +1517,7 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
           const u64 cnt = std::min(step, all - h0);
           const u32* hubs = b.of(bin) + h0;
           hub_chunk_counts_k<<<unsigned(std::min<u64>((cnt + 255) / 256, u64(sms) * 4)), 256, 0, s>>>(
-              hubs, cnt, a.g.off, chunks.p);
+              hubs, cnt, a.g.off, chunks.p, a.full_lists && a.prune && !DRY ? a.flags : nullptr);
           LVN_LAUNCH();
           exclusive_scan_u32_to_u64(chunks.p, coff.p, cnt, s);
           hub_chunk_owner_k<<<unsigned(std::min<u64>((cnt + 255) / 256, u64(sms) * 4)), 256, 0, s>>>(coff.p, cnt,
@@ -1537,10 +1543,34 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
   // hubs first: the highest-degree vertices settle before the rows that follow
   // them (on power-law graphs this is what a sequential id-order sweep does,
   // since hubs carry low ids); the reference compact engine sweeps low degree first
-  if (a.hubs_first)
-    for (int bin = kBinGlobal; bin >= kBinThread; --bin) launch_bin(bin);
-  else
-    for (int bin = kBinThread; bin <= kBinGlobal; ++bin) launch_bin(bin);
+  int order[kBins], nb = 0;
+  if (a.hubs_first) {
+    for (int bin = kBinGlobal; bin >= kBinThread; --bin)
+      if (b.count(bin)) order[nb++] = bin;
+  } else {
+    for (int bin = kBinThread; bin <= kBinGlobal; ++bin)
+      if (b.count(bin)) order[nb++] = bin;
+  }
+  // concurrent bins: every class but the hubs forks onto an aux stream behind
+  // one event of s and joins back into s; the hub chain stays on s, where its
+  // scratch buffers are allocated and stream-ordered freed (inside a capture:
+  // parallel graph branches)
+  int others = 0;
+  for (int j = 0; j < nb; ++j) others += order[j] != kBinGlobal;
+  if (a.nfork <= 0 || others <= 1) {
+    for (int j = 0; j < nb; ++j) launch_bin(order[j], s);
+    return;
+  }
+  Context& c = ctx();
+  const int nf = std::min(a.nfork, others);
+  if (int(c.aux.size()) < nf || int(c.aux_ev.size()) < nf + 1) fail(kInternal, "forked sweep streams not provisioned");
+  LVN_CUDA(cudaEventRecord(c.aux_ev[0], s));
+  for (int k = 0; k < nf; ++k) LVN_CUDA(cudaStreamWaitEvent(c.aux[k], c.aux_ev[0]));
+  for (int j = 0, k = 0; j < nb; ++j) launch_bin(order[j], order[j] == kBinGlobal ? s : c.aux[k++ % nf]);
+  for (int k = 0; k < nf; ++k) {
+    LVN_CUDA(cudaEventRecord(c.aux_ev[1 + k], c.aux[k]));
+    LVN_CUDA(cudaStreamWaitEvent(s, c.aux_ev[1 + k]));
+  }
 }
 
 template <class Tab>
@@ -1610,6 +1640,8 @@ __global__ void apply_segments_k(const u32* __restrict__ rec, const u64* __restr
 }
 
 }  // namespace
+
+int move_kernel_variant() { return move_kernel_choice(); }
 
 void apply_moves_segments(const u32* rec, const u64* segoff, const u32* counts, int P, int me, u64 total, u32* C,
                           const double* K, double* sigma, cudaStream_t s) {
