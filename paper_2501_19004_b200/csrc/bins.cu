@@ -290,25 +290,45 @@ void reset_impl(const DGraph& g, const Bins& b, double* K, double* sigma, u32* C
 }
 
 // active vertices of every bin segment, packed at the front of the segment
-__global__ void compact_active_k(const u32* __restrict__ list, u64 n, BinView v,
-                                 const u8* __restrict__ flags, u32* __restrict__ out,
-                                 ull* __restrict__ counts) {
-  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < n;
-       i += u64(gridDim.x) * blockDim.x) {
-    const u32 u = list[i];
-    int b = kBins - 1;
-    while (b > 0 && i < v.off[b]) --b;
-    const bool on = b != kBinIso && flags[u];
-    const u32 act = __activemask();
-    const u32 key = on ? u32(b) : 0xFFFFFFFFu;
-    const u32 peers = __match_any_sync(act, key);
-    if (!on) continue;
-    const int lane = threadIdx.x & 31;
-    const int leader = __ffs(peers) - 1;
-    ull base = 0;
-    if (lane == leader) base = atomicAdd(&counts[b], ull(__popc(peers)));
-    base = __shfl_sync(peers, base, leader);
-    out[v.off[b] + base + __popc(peers & ((1u << lane) - 1u))] = u;
+// Tiles of 1024 list entries per block: warp-aggregated shared counters per
+// bin, then ONE global reservation per (tile, bin) instead of one per warp
+// (a lattice pass puts every vertex in one bin: 24 M / 32 same-address
+// atomics per iteration made this the third-largest kernel on C4).
+constexpr int kCompactItems = 4;
+__global__ void __launch_bounds__(256) compact_active_k(const u32* __restrict__ list, u64 n, BinView v,
+                                                        const u8* __restrict__ flags, u32* __restrict__ out,
+                                                        ull* __restrict__ counts) {
+  __shared__ u32 cnt[kBins];
+  __shared__ ull base[kBins];
+  constexpr u64 kTile = 256 * kCompactItems;
+  const int lane = threadIdx.x & 31;
+  for (u64 t0 = blockIdx.x * kTile; t0 < n; t0 += u64(gridDim.x) * kTile) {
+    if (threadIdx.x < kBins) cnt[threadIdx.x] = 0;
+    __syncthreads();
+    u32 u[kCompactItems], pos[kCompactItems];
+    int bin[kCompactItems];
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k) {
+      const u64 i = t0 + u64(k) * 256 + threadIdx.x;
+      u[k] = i < n ? list[i] : 0u;
+      int b = kBins - 1;
+      while (b > 0 && i < v.off[b]) --b;
+      const bool on = i < n && b != kBinIso && flags[u[k]];
+      bin[k] = on ? b : -1;
+      const u32 peers = __match_any_sync(0xffffffffu, on ? u32(b) : 0xFFFFFFFFu);
+      const int leader = __ffs(peers) - 1;
+      u32 wb = 0;
+      if (on && lane == leader) wb = atomicAdd(&cnt[b], u32(__popc(peers)));
+      wb = __shfl_sync(0xffffffffu, wb, leader);
+      pos[k] = wb + __popc(peers & ((1u << lane) - 1u));
+    }
+    __syncthreads();
+    if (threadIdx.x < kBins && cnt[threadIdx.x]) base[threadIdx.x] = atomicAdd(&counts[threadIdx.x], ull(cnt[threadIdx.x]));
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < kCompactItems; ++k)
+      if (bin[k] >= 0) out[v.off[bin[k]] + base[bin[k]] + pos[k]] = u[k];
+    __syncthreads();
   }
 }
 
@@ -318,7 +338,7 @@ void compact_active(const Bins& b, const u8* flags, u32* out_list, ull* counts, 
   LVN_CUDA(cudaMemsetAsync(counts, 0, kBins * sizeof(ull), s));
   const u64 n = b.start[kBins];
   if (!n) return;
-  const u64 blocks = std::min<u64>((n + 255) / 256, u64(sm_count()) * 8);
+  const u64 blocks = std::min<u64>((n + 1023) / 1024, u64(sm_count()) * 8);
   compact_active_k<<<unsigned(blocks), 256, 0, s>>>(b.list.p, n, b.view(), flags, out_list, counts);
   LVN_LAUNCH();
 }
