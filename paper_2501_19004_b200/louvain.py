@@ -410,7 +410,18 @@ def _result(out) -> LouvainResult:
             membership = np.empty(0, np.uint32)
             dev_ptr = C.cast(r.membership, C.c_void_p).value
         else:
-            membership = np.ctypeslib.as_array(r.membership, (max(r.num_vertices, 1),))[: r.num_vertices].copy()
+            # zero-copy view of the library's pinned result block: the block
+            # goes back to the library (lvn_result_free) when the last array
+            # viewing it is collected (a 50 M-vertex copy costs 20-40 ms)
+            n = r.num_vertices
+            addr = C.cast(r.membership, C.c_void_p).value
+            if n and addr:
+                buf = (C.c_uint32 * n).from_address(addr)
+                buf._lvn_handle = _ResultHandle(out)
+                keep = True
+                membership = np.frombuffer(buf, dtype=np.uint32, count=n)
+            else:
+                membership = np.empty(0, np.uint32)
             dev_ptr = None
         res = LouvainResult(
             membership=membership,
