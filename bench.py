@@ -346,18 +346,47 @@ def main():
     for _ in range(args.warmup):
         run(dg, True)
     sampler = ClockSampler(local)
-    results = []
+    # only the last result stays alive: each holds its device membership, and
+    # holding every step's would drain the pool's block cache mid-run (C3:
+    # steps 3-5 at 240-400 ms instead of 185 ms); a caller looping over runs
+    # drops them too
+    results, walls = [], []
+
+    def keep(res):
+        walls.append(res.wall_seconds)
+        results[:] = [res]
     l0 = lvn.launch_count()
     barrier()
+    # inputs that fit a few L2s (C1: 15 MB): the L2 is flushed between timed
+    # steps by a 512 MB write outside the timed intervals (per-step events)
+    l2 = torch.cuda.get_device_properties(local).L2_cache_size
+    csr_bytes = 8 * (n + 1) + 8 * arcs
+    flush = csr_bytes < 4 * l2
+    scratch = torch.empty(512 << 20, dtype=torch.uint8, device="cuda") if flush else None
     with sampler:
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        for _ in range(args.steps):
-            results.append(run(dg, True))
-        e1.record()
-        barrier()
+        if flush:
+            elapsed_ms = 0.0
+            for i in range(args.steps):
+                scratch.fill_(i & 0xFF)
+                torch.cuda.synchronize()
+                a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                a.record()
+                keep(run(dg, True))
+                b.record()
+                b.synchronize()
+                elapsed_ms += a.elapsed_time(b)
+            barrier()
+        else:
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for _ in range(args.steps):
+                keep(run(dg, True))
+            e1.record()
+            barrier()
+            elapsed_ms = e0.elapsed_time(e1)
+    scratch = None
     launches = (lvn.launch_count() - l0) // args.steps
-    elapsed = max_over_ranks(e0.elapsed_time(e1) / 1e3)
+    elapsed = max_over_ranks(elapsed_ms / 1e3)
     step_s = elapsed / args.steps
     value = arcs / step_s
     clocks = sampler.summary()
@@ -369,7 +398,7 @@ def main():
     traffic = traffic_from_profile(args.config)
     gpeak = gather_peak()
 
-    step_ms = [round(x.wall_seconds * 1e3, 2) for x in results]
+    step_ms = [round(x * 1e3, 2) for x in walls]
     # ---- e2e: host (pinned) buffers through the public API ------------------------
     e2e = None
     if not args.no_e2e:
@@ -381,7 +410,6 @@ def main():
         # the device copy and the value leg's device memberships are not part
         # of this leg: release them so the host-input runs see the device as a
         # user's first call would (else 30+ GB stay pinned in the pool)
-        step_ms = [round(x.wall_seconds * 1e3, 2) for x in results]
         results = [r]
         dg.close()
         assert hg.offsets.ctypes.data == off_pinned.ctypes.data
@@ -424,7 +452,10 @@ def main():
             "data": "synthetic (device-generated, seeded)",
             "config": {"workload": args.config, "desc": cfg["desc"], "vertices": n, "arcs": arcs,
                        "parallelism": f"row-sharded x{world} over NCCL" if world > 1 else "single GPU",
-                       "l2_flush": "not needed: CSR >> 126 MB L2"},
+                       "l2_flush": (f"512 MB write between timed steps (input {csr_bytes / 1e6:.0f} MB < 4 x L2)"
+                                    if flush else f"not needed: input {csr_bytes / 1e9:.1f} GB >> {l2 / 1e6:.0f} MB L2")},
+            # the CLI's undirected rate (num_arcs / 2 / wall, louvain_cli.cpp:177), labelled
+            "undirected_edges_per_s": value / 2,
             "modularity": r.modularity, "num_communities": r.num_communities, "passes": r.passes,
             "sharded_passes": r.sharded_passes, "exchange_seconds": r.exchange_seconds,
             "iterations_per_pass": r.iterations_per_pass,
@@ -448,6 +479,7 @@ def main():
                                     "frac": mv.gathers_per_second / gpeak if gpeak else None,
                                     "per_arc": mv.gathers / mv.arcs if mv.arcs else None}},
             "cpu_baseline": cpu, "cpu_modularity": cpu_q,
+            "modularity_minus_cpu": (r.modularity - cpu_q) if cpu_q is not None else None,
             "e2e": e2e, "gpu_launches": launches, "clocks": clocks,
         }
         print(json.dumps(out))

@@ -136,7 +136,7 @@ typedef struct lvn_params {
 typedef struct lvn_phase_stats {
   double seconds;        /* summed device time of the family's launches */
   double bytes;          /* algorithmic bytes (SURVEY.md 8(d) formulas) */
-  uint64_t launches;
+  uint64_t launches;      /* timed spans; local moving: one per iteration (sweep) */
   uint64_t items;        /* vertices processed */
   uint64_t arcs;         /* arcs scanned */
   uint64_t gathers;      /* random element accesses: C[t] and Sigma[c] gathers, neighbour marks */

@@ -1546,6 +1546,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
           if (!fs.ev.empty()) LVN_CUDA(cudaStreamWaitEvent(s, fs.ev[k]));
           sp = tm.begin(LVN_STAT_MOVE, s);
           if (k == 0) sp0 = sp;
+          else tm.spans[sp].count = 0;  // stats count one launch per iteration (sweep)
           move_sweep(a, fbins[k].view(), p.value_bits, s);
           tm.end(sp, s, 0.0);
         }
@@ -1554,6 +1555,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
         if (shard) LVN_CUDA(cudaMemsetAsync(a.moves_n, 0, sizeof(u32), s));
         sp = tm.begin(LVN_STAT_MOVE, s);
         if (k == 0) sp0 = sp;
+        else tm.spans[sp].count = 0;
         if (graph_pass) c.pool.track_begin();
         move_sweep(a, views[k], p.value_bits, s);
         if (graph_pass) sweep_bytes = c.pool.track_end();
