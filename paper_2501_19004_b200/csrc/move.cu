@@ -1403,9 +1403,38 @@ int move_kernel_choice() {
 }
 bool use_match() { return move_kernel_choice() == 2; }
 
+// LVN_SORT16=mask: uniform-weight sort bins on 16 lanes per vertex with twice
+// the registers per lane (bit 0: rows of 33-64 arcs, bit 1: 65-128), so the
+// per-vertex work (header loads, ranking reductions, the decision) is shared
+// by fewer lanes (tuning aid; unit sums are exact in any lane layout)
+int sort16_mask() {
+  static const int v = [] {
+    const char* e = std::getenv("LVN_SORT16");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+template <int G, int K, class V, bool DRY>
+void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s);
+
+// the same bin on 16 lanes per vertex (uniform weights only, see sort16_mask)
+template <int K, class V, bool DRY>
+bool launch_sort16(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
+  const int bit = K == 2 ? 1 : 2;
+  if (DRY || !a.uniform || move_kernel_choice() != 0 || !(sort16_mask() & bit)) return false;
+  constexpr int T = 256;
+  auto k = lm_psort<16, K * 2, V, DRY, true>;
+  static const int occ = occupancy(k, T, 0);
+  launch_chunks(k, a, b.of(bin), b.count(bin), T, T / 16, u64(sm_count()) * occ, 0, s);
+  return true;
+}
+
 template <int G, int K, class V, bool DRY>
 void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
   if (!b.count(bin)) return;
+  if constexpr (G == 32 && (K == 2 || K == 4) && !DRY) {
+    if (launch_sort16<K, V, DRY>(a, b, bin, s)) return;
+  }
   constexpr int T = 256;
   constexpr int LB = ilog2<G * K>();
   // community-only keys for uniform weights; packed keys need (n - 1) << LB | (N - 1) < 0xFFFFFFFF
