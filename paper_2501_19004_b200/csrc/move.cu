@@ -1403,14 +1403,17 @@ int move_kernel_choice() {
 }
 bool use_match() { return move_kernel_choice() == 2; }
 
-// LVN_SORT16=mask: uniform-weight sort bins on 16 lanes per vertex with twice
-// the registers per lane (bit 0: rows of 33-64 arcs, bit 1: 65-128), so the
-// per-vertex work (header loads, ranking reductions, the decision) is shared
-// by fewer lanes (tuning aid; unit sums are exact in any lane layout)
+// Uniform-weight sort bins run on 16 lanes per vertex with twice the
+// registers per lane (lm_psort<16, 2K>), so the per-vertex work (header
+// loads, ranking reductions, the decision) is shared by half as many lanes and
+// twice as many vertices are in flight per warp; unit sums are exact in any
+// lane layout, so decisions do not depend on the layout. LVN_SORT16=mask
+// picks the bins (bit 0: rows of 17-32 arcs, bit 1: 33-64, bit 2: 65-128);
+// default 6 (C5 local moving 450 -> 412 ms; C2, C3 unchanged).
 int sort16_mask() {
   static const int v = [] {
     const char* e = std::getenv("LVN_SORT16");
-    return e ? std::atoi(e) : 0;
+    return e ? std::atoi(e) : 6;
   }();
   return v;
 }
@@ -1420,7 +1423,7 @@ void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s);
 // the same bin on 16 lanes per vertex (uniform weights only, see sort16_mask)
 template <int K, class V, bool DRY>
 bool launch_sort16(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
-  const int bit = K == 2 ? 1 : 2;
+  const int bit = K == 1 ? 1 : K == 2 ? 2 : 4;
   if (DRY || !a.uniform || move_kernel_choice() != 0 || !(sort16_mask() & bit)) return false;
   constexpr int T = 256;
   auto k = lm_psort<16, K * 2, V, DRY, true>;
@@ -1432,7 +1435,7 @@ bool launch_sort16(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s)
 template <int G, int K, class V, bool DRY>
 void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
   if (!b.count(bin)) return;
-  if constexpr (G == 32 && (K == 2 || K == 4) && !DRY) {
+  if constexpr (G == 32 && K <= 4 && !DRY) {
     if (launch_sort16<K, V, DRY>(a, b, bin, s)) return;
   }
   constexpr int T = 256;

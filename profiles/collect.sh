@@ -19,7 +19,7 @@ LVN_POOL_NOCACHE=1 timeout 900 ncu --metrics dram__bytes_read.sum,dram__bytes_wr
   python profiles/prof_run.py "$cfg" 1 > gpurun_out/move_traffic_$cfg.log 2>&1
 # 4. full capture of the dominant sort-bin kernel (pass 0, second sweep), raw page only
 LVN_POOL_NOCACHE=1 timeout 900 ncu --set full --clock-control none --import-source on --kernel-name-base demangled \
-  -k 'regex:lm_psort<.int.32, .int.2' --launch-skip 8 --launch-count 1 -o gpurun_out/prof_lm_sort_$cfg -f \
+  -k 'regex:lm_psort<.int.16, .int.4' --launch-skip 16 --launch-count 1 -o gpurun_out/prof_lm_sort_$cfg -f \
   python profiles/prof_run.py "$cfg" 1 > gpurun_out/prof_lm_sort_$cfg.log 2>&1
 ncu -i gpurun_out/prof_lm_sort_$cfg.ncu-rep --page raw --csv > gpurun_out/prof_lm_sort_$cfg.raw.csv 2>/dev/null
 rm -f gpurun_out/prof_lm_sort_$cfg.ncu-rep
