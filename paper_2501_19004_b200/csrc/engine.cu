@@ -5,6 +5,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <new>
@@ -12,12 +13,35 @@
 #include <thread>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "comm.hpp"
 #include "kernels.cuh"
 #include "lvn.h"
 #include "shard.hpp"
 
 namespace lvn {
+
+// NVTX ranges (header-only NVTX v3: free unless a tool such as nsys/ncu is
+// attached) for the run, each pass and its local-moving / aggregation phases,
+// so a timeline shows the reference's phase structure
+struct Nvtx {
+  nvtxRangeId_t id = 0;
+  bool open = false;
+  explicit Nvtx(const char* name) : id(nvtxRangeStartA(name)), open(true) {}
+  Nvtx(const char* fmt, int k) {
+    char buf[48];
+    std::snprintf(buf, sizeof buf, fmt, k);
+    id = nvtxRangeStartA(buf);
+    open = true;
+  }
+  void end() {
+    if (open) nvtxRangeEnd(id), open = false;
+  }
+  ~Nvtx() { end(); }
+  Nvtx(const Nvtx&) = delete;
+  Nvtx& operator=(const Nvtx&) = delete;
+};
 
 std::atomic<unsigned long long> g_launches{0};
 
@@ -1395,6 +1419,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
 
   for (int pass = 0; pass < p.max_passes && !idle; ++pass) {
     const auto t_pass = Clock::now();
+    Nvtx r_pass("pass %d", pass);
     const u32 nv = cur.n;
     if (!sharded) v0 = 0, v1 = nv;  // a whole-graph pass owns every row
     Bins& B = pass == 0 ? in_bins : bins;
@@ -1524,6 +1549,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     for (int k = 0; k < R0 && R0 > 1; ++k)
       compute_bins(cur.off + fs.vb[k], fs.vb[k + 1] - fs.vb[k], edges, fbins[k], s, ~u64(0), fs.vb[k]);
     const auto t0 = Clock::now();
+    Nvtx r_move("local moving");
     int iterations = 0;
     // iteration 0 sweeps every row with arcs (all flagged); later iterations
     // sweep the flagged rows only, compacted right after the previous sweep
@@ -1642,6 +1668,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     }
     for (cudaEvent_t e : (pass == 0 ? fs.ev : std::vector<cudaEvent_t>())) LVN_CUDA(cudaStreamWaitEvent(s, e));
     t_move += since(t0);
+    r_move.end();
     check_err(err.p, s);
     check_membership("after local moving", C.p, nv, nv, s);
     ++passes;
@@ -1677,6 +1704,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     lookup(global.p, N, C.p, nv, err.p, s);     // lookup_dendrogram (louvain_compact.cpp:383)
     tm.end(sp, s, 12.0 * nv + 12.0 * N);
     const auto t1 = Clock::now();
+    Nvtx r_agg("aggregation");
     OwnedCsr& next = owned[pass & 1];
     sp = tm.begin(LVN_STAT_AGGREGATE, s);
     if (shard) {
@@ -1710,6 +1738,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
       }
     }
     t_aggregate += since(t1);
+    r_agg.end();
     cur = next.view();
     check_graph("aggregated graph", cur, s);
     ++aggregations;
@@ -2078,7 +2107,10 @@ int lvn_louvain(const lvn_csr* g, const lvn_params* p, lvn_result** out) {
   lvn_params_default(&def);
   auto* r = new lvn_result;
   std::memset(r, 0, sizeof(*r));
-  const int rc = guard([&](Context&) { run_louvain(g, p ? *p : def, r); });
+  const int rc = guard([&](Context&) {
+    Nvtx range("lvn_louvain");
+    run_louvain(g, p ? *p : def, r);
+  });
   if (rc) {
     lvn_result_free(r);
     return rc;

@@ -1408,7 +1408,8 @@ bool use_match() { return move_kernel_choice() == 2; }
 // loads, ranking reductions, the decision) is shared by half as many lanes and
 // twice as many vertices are in flight per warp; unit sums are exact in any
 // lane layout, so decisions do not depend on the layout. LVN_SORT16=mask
-// picks the bins (bit 0: rows of 17-32 arcs, bit 1: 33-64, bit 2: 65-128);
+// picks the bins (bit 0: rows of 17-32 arcs, bit 1: 33-64, bit 2: 65-128,
+// bit 3: 129-256);
 // default 6 (C5 local moving 450 -> 412 ms; C2, C3 unchanged).
 int sort16_mask() {
   static const int v = [] {
@@ -1423,7 +1424,7 @@ void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s);
 // the same bin on 16 lanes per vertex (uniform weights only, see sort16_mask)
 template <int K, class V, bool DRY>
 bool launch_sort16(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
-  const int bit = K == 1 ? 1 : K == 2 ? 2 : 4;
+  const int bit = K == 1 ? 1 : K == 2 ? 2 : K == 4 ? 4 : 8;
   if (DRY || !a.uniform || move_kernel_choice() != 0 || !(sort16_mask() & bit)) return false;
   constexpr int T = 256;
   auto k = lm_psort<16, K * 2, V, DRY, true>;
@@ -1435,7 +1436,7 @@ bool launch_sort16(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s)
 template <int G, int K, class V, bool DRY>
 void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s) {
   if (!b.count(bin)) return;
-  if constexpr (G == 32 && K <= 4 && !DRY) {
+  if constexpr (G == 32 && K <= 8 && !DRY) {
     if (launch_sort16<K, V, DRY>(a, b, bin, s)) return;
   }
   constexpr int T = 256;
