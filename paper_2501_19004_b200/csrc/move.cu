@@ -36,6 +36,8 @@
 
 #include <cmath>
 
+#include <cub/device/device_radix_sort.cuh>
+
 #include "kernels.cuh"
 #include "psort.cuh"
 #include "sortnet.cuh"
@@ -1183,10 +1185,31 @@ __global__ void hub_chunk_owner_k(const u64* __restrict__ chunk_off, u64 count, 
     for (u64 v = chunk_off[i]; v < chunk_off[i + 1]; ++v) chunk_hub[v] = u32(i);
 }
 
+// Chunk schedule interleaving the hubs by position in their rows (opt-in,
+// LVN_HUB_INTERLEAVE=1): key = the chunk's fractional position in its hub's
+// row, so chunks in flight together cover the same target-id range of every
+// hub (rows are sorted by target) and their C / Sigma gathers share L2 lines;
+// entries past the last chunk sort last
+__global__ void hub_order_keys_k(const u64* __restrict__ chunk_off, const u32* __restrict__ chunk_hub, u64 count,
+                                 u64 cap, u32* __restrict__ key, u32* __restrict__ val) {
+  const u64 total = chunk_off[count];
+  for (u64 i = blockIdx.x * u64(blockDim.x) + threadIdx.x; i < cap; i += u64(gridDim.x) * blockDim.x) {
+    u32 k = 0xFFFFFFFFu;
+    if (i < total) {
+      const u64 h = chunk_hub[i];
+      const u64 c0 = chunk_off[h], nc = chunk_off[h + 1] - c0;
+      k = u32(((i - c0) << 24) / nc);
+    }
+    key[i] = k;
+    val[i] = u32(i);
+  }
+}
+
 template <class Tab>
 __global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const u32* __restrict__ hubs,
                                                                u64 count, const u64* __restrict__ chunk_off,
-                                                               const u32* __restrict__ chunk_hub) {
+                                                               const u32* __restrict__ chunk_hub,
+                                                               const u32* __restrict__ order) {
   using V = typename Tab::V;
   extern __shared__ __align__(16) unsigned char smem[];
   __shared__ u32 nlive;
@@ -1197,7 +1220,8 @@ __global__ void __launch_bounds__(kBlockThreads) lm_hub_chunks(MoveArgs x, const
   if (threadIdx.x == 0) nlive = 0;
   __syncthreads();
   const u64 total = chunk_off[count];
-  for (u64 v = blockIdx.x; v < total; v += gridDim.x) {
+  for (u64 i = blockIdx.x; i < total; i += gridDim.x) {
+    const u64 v = order ? order[i] : i;
     const u64 lo = chunk_hub[v];  // hub of chunk v
     const u32 u = hubs[lo];
     const u32 pi = x.hub_index[u];
@@ -1418,6 +1442,14 @@ int sort16_mask() {
   }();
   return v;
 }
+int hub_interleave() {
+  static const int v = [] {
+    const char* e = std::getenv("LVN_HUB_INTERLEAVE");
+    return e ? std::atoi(e) : 0;
+  }();
+  return v;
+}
+
 template <int G, int K, class V, bool DRY>
 void launch_sort(const MoveArgs& a, const BinView& b, int bin, cudaStream_t s);
 
@@ -1543,6 +1575,7 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
         DBuf<HubBest> hbest(a.g.arcs / kHubChunk + std::min(step, all) + 1);
         DBuf<u32> owner(a.g.arcs / kHubChunk + std::min(step, all) + 1);
         DBuf<u8> hmoved(std::min(step, all));
+        DBuf<u32> hkey, hval, hkey2, hval2;  // interleaved chunk schedule (hub_interleave)
         auto kc = lm_hub_chunks<Tab>;
         constexpr size_t smem = hub_smem<Tab>();
         static const int occ = (set_smem(kc, smem), occupancy(kc, kBlockThreads, smem));
@@ -1556,7 +1589,20 @@ void sweep(const MoveArgs& a, const BinView& b, cudaStream_t s) {
           hub_chunk_owner_k<<<unsigned(std::min<u64>((cnt + 255) / 256, u64(sms) * 4)), 256, 0, s>>>(coff.p, cnt,
                                                                                                     owner.p);
           LVN_LAUNCH();
-          kc<<<unsigned(sms * occ), kBlockThreads, smem, s>>>(a, hubs, cnt, coff.p, owner.p);
+          const u32* order = nullptr;
+          if (hub_interleave()) {
+            const u64 cap = a.g.arcs / kHubChunk + cnt + 1;
+            hkey.ensure(cap), hval.ensure(cap), hkey2.ensure(cap), hval2.ensure(cap);
+            hub_order_keys_k<<<unsigned(std::min<u64>((cap + 255) / 256, u64(sms) * 8)), 256, 0, s>>>(
+                coff.p, owner.p, cnt, cap, hkey.p, hval.p);
+            LVN_LAUNCH();
+            size_t bytes = 0;
+            LVN_CUDA(cub::DeviceRadixSort::SortPairs(nullptr, bytes, hkey.p, hkey2.p, hval.p, hval2.p, cap, 0, 32, s));
+            DBuf<unsigned char> tmp(bytes);
+            LVN_CUDA(cub::DeviceRadixSort::SortPairs(tmp.p, bytes, hkey.p, hkey2.p, hval.p, hval2.p, cap, 0, 32, s));
+            order = hval2.p;
+          }
+          kc<<<unsigned(sms * occ), kBlockThreads, smem, s>>>(a, hubs, cnt, coff.p, owner.p, order);
           LVN_LAUNCH();
           lm_hub_rank<Tab, DRY><<<unsigned(sms * 4), kBlockThreads, 0, s>>>(a, hubs, cnt, coff.p, owner.p, hbest.p);
           LVN_LAUNCH();
