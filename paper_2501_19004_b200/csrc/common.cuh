@@ -206,9 +206,11 @@ __host__ __device__ inline u32 ceil_log2_u64(u64 x) {
 // L2 eviction priority for the random gathers of a sweep (C[t], Sigma[c]):
 // evict_last keeps those arrays resident while the streamed rows (loaded
 // evict-first) pass through L2.
-__device__ __forceinline__ ull l2_keep_policy() {
+__device__ __forceinline__ ull l2_keep_policy(int mode = 1) {
   ull p;
-  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  if (mode == 0) asm("createpolicy.fractional.L2::evict_normal.b64 %0, 1.0;" : "=l"(p));
+  else if (mode == 2) asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  else asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
   return p;
 }
 __device__ __forceinline__ u32 ld_keep(const u32* a, ull pol) {

@@ -1514,6 +1514,7 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     // LVN_HUB_CHUNK=k: decide the block / hub bins k vertices per launch, so
     // later hubs see earlier hubs' moves (tuning aid; +0.0003 Q on RMAT-24)
     if (const char* e = std::getenv("LVN_HUB_CHUNK")) a.hub_chunk = std::strtoull(e, nullptr, 10);
+    if (const char* e = std::getenv("LVN_L2_KEEP")) a.l2_keep = std::atoi(e);
     a.hubs_first = p.sweep_order == 1;
     if (p.singleton_rule) {
       csize.ensure(nv ? nv : 1);

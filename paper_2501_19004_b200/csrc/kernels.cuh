@@ -108,6 +108,9 @@ struct MoveArgs {
   float uniform_w = 0.f;
   double inv_m = 0.0, inv_2m2 = 0.0;  // set by move_sweep
   int hubs_first = 0;          // bin order of a sweep: highest degree class first
+  // L2 priority of the sort kernels' C / Sigma gathers: 1 evict_last (default),
+  // 0 evict_normal, 2 evict_first (LVN_L2_KEEP, tuning aid)
+  int l2_keep = 1;
   // full bin lists (graph-mode passes): every kernel skips the rows whose
   // prune flag is clear instead of relying on a compacted active list
   int full_lists = 0;

@@ -409,7 +409,7 @@ __global__ void __launch_bounds__(256) lm_sort(MoveArgs x, const u32* __restrict
   const u32 lane = threadIdx.x & (G - 1);
   const u32 gi = threadIdx.x / G;
   const u64 stride = u64(gridDim.x) * GPB;
-  const ull keep = l2_keep_policy();
+  const ull keep = l2_keep_policy(x.l2_keep);
   Tally tl;
   // vertex in flight (the trip count is uniform across the block, so every
   // lane reaches every shuffle)
@@ -570,7 +570,7 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
   V* gbuf = vbuf + (K > 1 ? gi * N : 0);
   const ull dirs = psort_dirs<G, K>(lane);
   const u64 stride = u64(gridDim.x) * GPB;
-  const ull keep = l2_keep_policy();
+  const ull keep = l2_keep_policy(x.l2_keep);
   Tally tl;
 
   auto load_row = [&](u32 v, u64 rlo, u64 rhi, u32 (&t)[K], V (&w)[K]) {
