@@ -1515,7 +1515,6 @@ void run_louvain(const lvn_csr* in, const lvn_params& p, lvn_result* r, Comm* co
     // later hubs see earlier hubs' moves (tuning aid; +0.0003 Q on RMAT-24)
     if (const char* e = std::getenv("LVN_HUB_CHUNK")) a.hub_chunk = std::strtoull(e, nullptr, 10);
     if (const char* e = std::getenv("LVN_L2_KEEP")) a.l2_keep = std::atoi(e);
-    if (const char* e = std::getenv("LVN_BOUND_RANK")) a.bound_rank = std::atoi(e);
     a.hubs_first = p.sweep_order == 1;
     if (p.singleton_rule) {
       csize.ensure(nv ? nv : 1);
@@ -2361,7 +2360,6 @@ int evaluate_moves_impl(const lvn_csr* g, const uint32_t* membership, const doub
     a.m = m;
     a.dry = probe ? 0 : 1;
     a.probe = probe ? 1 : 0;
-    if (const char* e = std::getenv("LVN_BOUND_RANK")) a.bound_rank = std::atoi(e);  // the engine's ranking
     a.value_f32 = pp.value_bits == 32 ? 1 : 0;
     a.prune = 0;
     DBuf<u8> flags(n ? n : 1);

@@ -111,10 +111,6 @@ struct MoveArgs {
   // L2 priority of the sort kernels' C / Sigma gathers: 1 evict_last (default),
   // 0 evict_normal, 2 evict_first (LVN_L2_KEEP, tuning aid)
   int l2_keep = 1;
-  // sort kernels: score the heaviest candidate first and skip the Sigma
-  // gathers of candidates whose Sigma-free bound is below its gain (exact;
-  // LVN_BOUND_RANK)
-  int bound_rank = 0;
   // full bin lists (graph-mode passes): every kernel skips the rows whose
   // prune flag is clear instead of relying on a compacted active list
   int full_lists = 0;

@@ -697,62 +697,10 @@ __global__ void __launch_bounds__(256, K == 1 ? 4 : (K <= 4 ? 3 : 2)) lm_psort(M
     const V own = ob ? own_s : V(0);
     double sc[K];
 #pragma unroll
-    for (int r = 0; r < K; ++r)
+    for (int r = 0; r < K; ++r) {
       if (cand[r]) cand[r] = key_ok(x, ck[r]) && (DRY || may_gain(x, double(run[r]), double(own), ku, sf));
-    if (!DRY && x.bound_rank) {
-      // Bounded ranking: the candidate with the largest K_{u->c} (lowest id on
-      // ties) is scored first; every other candidate whose Sigma-free bound
-      // (the score at Sigma_c = 0, monotone in Sigma_c in floating point too)
-      // is below that gain can neither win nor tie, so its Sigma gather is
-      // skipped. Exact: the decision is unchanged.
-      V km = V(-1);
-#pragma unroll
-      for (int r = 0; r < K; ++r)
-        if (cand[r] && run[r] > km) km = run[r];
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) km = max(km, __shfl_xor_sync(FULL, km, o, G));
-      u32 c1 = kEmpty;
-#pragma unroll
-      for (int r = 0; r < K; ++r)
-        if (cand[r] && run[r] == km && ck[r] < c1) c1 = ck[r];
-#pragma unroll
-      for (int o = G / 2; o > 0; o >>= 1) c1 = min(c1, __shfl_xor_sync(FULL, c1, o, G));
-      int r1 = -1;
-#pragma unroll
-      for (int r = 0; r < K; ++r)
-        if (cand[r] && ck[r] == c1) r1 = r;
-      double s1 = 0.0, g1 = -INFINITY;
-      if (r1 >= 0) {
-        s1 = ld_keep(x.sigma + c1, keep);
-        V k1 = V(0);
-#pragma unroll
-        for (int r = 0; r < K; ++r)
-          if (r == r1) k1 = run[r];
-        g1 = score<DRY, V>(x, double(k1), double(own), ku, s1, sf);
-      }
-      const u32 hb = (__ballot_sync(FULL, r1 >= 0) >> gshift) & GMASK;
-      g1 = __shfl_sync(FULL, g1, hb ? __ffs(hb) - 1 : 0, G);
-      if (!hb) g1 = -INFINITY;
-#pragma unroll
-      for (int r = 0; r < K; ++r) {
-        sc[r] = 0.0;
-        if (!cand[r]) continue;
-        if (r == r1) {
-          sc[r] = s1;
-        } else if (score<DRY, V>(x, double(run[r]), double(own), ku, 0.0, sf) < g1) {
-          cand[r] = false;
-          continue;
-        } else {
-          sc[r] = ld_keep(x.sigma + ck[r], keep);
-        }
-        ++tl.rand;
-      }
-    } else {
-#pragma unroll
-      for (int r = 0; r < K; ++r) {
-        sc[r] = cand[r] ? ld_keep(x.sigma + ck[r], keep) : 0.0;
-        tl.rand += cand[r] ? 1 : 0;
-      }
+      sc[r] = cand[r] ? ld_keep(x.sigma + ck[r], keep) : 0.0;
+      tl.rand += cand[r] ? 1 : 0;
     }
 
     // (i+2) row bounds, community, vertex weight
